@@ -1,0 +1,305 @@
+"""Generate golden vectors by running the REFERENCE implementation.
+
+Run in the build container only (the reference is not on the GPU box):
+
+    python tests/golden/make_golden.py
+
+It imports ``bdem`` read-only from ``/root/reference/pkg/src``, feeds it the
+seeded synthetic inputs of ``paper_2308_10459_b200.configs`` (the same
+generator the GPU path and the oracle use) and stores inputs + reference
+outputs as small ``.npz`` fixtures next to this script.  The fixtures pin the
+CPU oracle (``tests/test_oracle_golden.py``) and the CUDA path
+(``tests/test_gpu_*.py``).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.dont_write_bytecode = True
+
+from bdem import bonds as rb            # noqa: E402
+from bdem import contact as rc          # noqa: E402
+from bdem import elements as re_        # noqa: E402
+from bdem import geometry as rg         # noqa: E402
+from bdem import integrator as ri       # noqa: E402
+from bdem import linalg as rl           # noqa: E402
+from bdem import scenes as rs           # noqa: E402
+from bdem import solver as rsv          # noqa: E402
+from bdem.quat import quat_normalize    # noqa: E402
+
+from paper_2308_10459_b200 import configs as C   # noqa: E402
+
+BOND_FIELDS = ("i", "j", "rest_length", "radius", "d0", "q0", "frame", "kn", "kt", "k_diag",
+               "section", "second_moment", "polar_moment", "tensile_strength",
+               "shear_strength", "status", "stiffness_scale", "damage", "plastic_strain",
+               "sigma", "tau")
+ELEM_FIELDS = ("p", "q", "v", "qdot", "mass", "radius", "pinned")
+
+
+def ref_bonds(b):
+    kw = {f: np.array(getattr(b, f), copy=True) for f in BOND_FIELDS}
+    kw["face_i"] = np.zeros(b.n, dtype=np.int64)
+    kw["face_j"] = np.zeros(b.n, dtype=np.int64)
+    return rb.BondSet(**kw)
+
+
+def ref_elements(el):
+    return re_.ElementSet(*(np.array(getattr(el, f), copy=True) for f in ELEM_FIELDS))
+
+
+def pack(prefix, obj, fields):
+    return {f"{prefix}{f}": np.asarray(getattr(obj, f)) for f in fields}
+
+
+def dummy_mesh():
+    v = np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]])
+    return rg.TetMesh(v, np.array([[0, 1, 2, 3]]))
+
+
+def ref_scene(spec, driver=None, colliders=None):
+    el = ref_elements(spec.elements)
+    return rs.Scene(spec.name, dummy_mesh(), el, ref_bonds(spec.bonds),
+                    colliders=ref_colliders(spec.colliders) if colliders is None else list(colliders),
+                    gravity=np.array(spec.gravity), dt=spec.dt, youngs=spec.youngs,
+                    shear_modulus=spec.shear_modulus, density=spec.density,
+                    k_contact=spec.k_contact, k_element=spec.k_element,
+                    plastic=spec.plastic, driver=driver,
+                    surface_flags=np.zeros(el.n, dtype=bool))
+
+
+def ref_colliders(cols):
+    return [rc.HalfSpace(tuple(c.normal), c.offset) for c in cols]
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name)
+    np.savez_compressed(path, **arrays)
+    print(f"  wrote {name}: {os.path.getsize(path) / 1024:.1f} KiB")
+
+
+# ---------------------------------------------------------------------------
+
+def gold_bond_terms():
+    """BondSet.energy_terms (bonds.py:473-504) on random and near-rest states."""
+    spec = C.cube(n_side=5, r=0.002, seed=11, random_q=True)
+    rng = np.random.default_rng(101)
+    b = spec.bonds
+    nb = b.n
+    b.status[rng.choice(nb, 12, replace=False)] = 2
+    b.stiffness_scale[:] = rng.uniform(0.4, 1.0, nb)
+    out = pack("b_", b, BOND_FIELDS)
+    rbs = ref_bonds(b)
+    p = spec.elements.p + 0.02 * 0.002 * rng.normal(size=spec.elements.p.shape)
+    cases = {
+        "randq": spec.elements.q,
+        "nearq": quat_normalize(np.tile([0.0, 0, 0, 1], (spec.elements.n, 1))
+                                + 0.05 * rng.normal(size=(spec.elements.n, 4))),
+        "ident": np.tile([0.0, 0, 0, 1], (spec.elements.n, 1)),
+    }
+    for tag, q in cases.items():
+        q = np.array(q)
+        idx, e, gpi, gpj, gqi, gqj, hpp, hqq = rbs.energy_terms(p, q, want_hess=True)
+        out.update({f"{tag}_q": q, f"{tag}_idx": idx, f"{tag}_E": e, f"{tag}_gpi": gpi,
+                    f"{tag}_gpj": gpj, f"{tag}_gqi": gqi, f"{tag}_gqj": gqj,
+                    f"{tag}_hpp": hpp, f"{tag}_hqq": hqq})
+    out["p"] = p
+    save("bond_terms.npz", **out)
+
+
+def _small_problem(seed=21, random_q=False, qspread=0.05):
+    spec = C.cube(n_side=4, r=0.002, seed=seed, random_q=random_q, youngs=3e8,
+                  k_contact=1e8)
+    rng = np.random.default_rng(seed + 1)
+    el = spec.elements
+    el.v[:] = 0.05 * rng.normal(size=el.v.shape)
+    if not random_q:
+        el.q[:] = quat_normalize(el.q + qspread * rng.normal(size=el.q.shape))
+    el.qdot[:] = ri.tangent_project(el.q, 2.0 * rng.normal(size=el.q.shape))
+    # plane cuts through the top layer so the collider curvature is active
+    z_top = float(el.p[:, 2].max())
+    cols = [C.HalfSpace((0.0, 0.0, -1.0), -(z_top - 0.3 * 0.002))]
+    spec.colliders = cols
+    spec.k_element = 1e6
+    return spec, rng
+
+
+def gold_newton_pieces():
+    """value_and_gradient, build_clamped_pieces, assemble_reduced_system,
+    BlockJacobi, pcg on one ImplicitProblem (integrator.py / solver.py / linalg.py)."""
+    out = {}
+    for tag, rq in (("near", False), ("rand", True)):
+        spec, rng = _small_problem(seed=21 if not rq else 31, random_q=rq)
+        sc = ref_scene(spec, colliders=ref_colliders(spec.colliders))
+        el = sc.elements
+        pairs = rc.broad_phase(el.p, el.radius, 2.0 * float(el.radius.max()) + 1e-12)
+        ctx = ri.StepContext(sc.dt, sc.p_prev.copy(), sc.q_prev.copy(), el.p.copy(), el.q.copy())
+        model = ri.PotentialModel(el, sc.bonds, pairs, sc.colliders, sc.gravity,
+                                  sc.k_contact, sc.k_element)
+        prob = ri.ImplicitProblem(model, ctx)
+        p, q = ri.predict_state(ctx, el.v, el.qdot, prob.free)
+        p = p + 1e-5 * rng.normal(size=p.shape) * prob.free[:, None]
+        f, gp, gq = prob.value_and_gradient(p, q)
+        z = rsv.reduced_gradient(q, gp, gq, prob.free)
+        gnorm = float(np.linalg.norm(z))
+        pieces = rsv.build_clamped_pieces(prob, p, q, gq)
+        mat, diag = rsv.assemble_reduced_system(pieces, q, prob.free)
+        pre = rl.BlockJacobi(diag)
+        tol = rl.relative_tolerance(gnorm)
+        res = rl.pcg(lambda v: mat @ v, -z, pre.apply, tol, 2000)
+        res_tight = rl.pcg(lambda v: mat @ v, -z, pre.apply, 1e-10, 2000)
+        out.update(pack(f"{tag}_el_", spec.elements, ELEM_FIELDS))
+        out.update(pack(f"{tag}_b_", spec.bonds, BOND_FIELDS))
+        hs = spec.colliders[0]
+        out.update({
+            f"{tag}_dt": sc.dt, f"{tag}_kc": sc.k_contact, f"{tag}_ke": sc.k_element,
+            f"{tag}_gravity": sc.gravity, f"{tag}_hs": np.array([*hs.normal, hs.offset]),
+            f"{tag}_p_prev": ctx.p_prev, f"{tag}_q_prev": ctx.q_prev,
+            f"{tag}_pairs": pairs, f"{tag}_p": p, f"{tag}_q": q,
+            f"{tag}_f": f, f"{tag}_gp": gp, f"{tag}_gq": gq, f"{tag}_z": z,
+            f"{tag}_gnorm": gnorm,
+            f"{tag}_bond_pp": pieces.bond_pp, f"{tag}_bond_qq_red": pieces.bond_qq_red,
+            f"{tag}_pair_pp": pieces.pair_pp, f"{tag}_elem_pos": pieces.elem_pos,
+            f"{tag}_elem_rot": pieces.elem_rot,
+            f"{tag}_A": mat.toarray(), f"{tag}_diag": diag, f"{tag}_minv": pre.inverse_blocks,
+            f"{tag}_pcg_x": res.x, f"{tag}_pcg_it": res.iterations, f"{tag}_pcg_tol": tol,
+            f"{tag}_pcg_tight_x": res_tight.x, f"{tag}_pcg_tight_it": res_tight.iterations,
+            f"{tag}_value": prob.value(p, q),
+        })
+        if tag == "near":
+            cfg = rsv.SolverConfig(epsilon=1e-7, max_iterations=30)
+            sol = rsv.minimize_second_order(prob, p, q, cfg)
+            out.update({
+                "solve_p": sol.p, "solve_q": sol.q, "solve_converged": sol.converged,
+                "solve_iterations": sol.iterations, "solve_gnorm": sol.grad_norm,
+                "solve_pcg_total": sol.pcg_total, "solve_reason": sol.reason,
+                "solve_rec_f": np.array([r.f for r in sol.records]),
+                "solve_rec_gnorm": np.array([r.grad_norm for r in sol.records]),
+                "solve_rec_alpha": np.array([r.alpha for r in sol.records]),
+                "solve_rec_pcg": np.array([r.pcg_iterations for r in sol.records]),
+            })
+    save("newton_pieces.npz", **out)
+
+
+def _run_traj(name, spec, steps, eps, driver=None, schedule=None, max_iter=300):
+    sc = ref_scene(spec, driver=driver)
+    cfg = rsv.SolverConfig(epsilon=eps, max_iterations=max_iter)
+    rec = {k: [] for k in ("p", "q", "v", "qdot", "newton", "pcg", "committed", "reason",
+                           "pairs", "gnorm")}
+    events = []
+    out = pack("init_el_", spec.elements, ELEM_FIELDS)
+    out.update(pack("init_b_", spec.bonds, BOND_FIELDS))
+    t0 = time.time()
+    for s in range(steps):
+        if schedule is not None:
+            sc.colliders = ref_colliders(schedule(sc.time + sc.dt))
+        rep = rsv.stable_step(sc, cfg)
+        el = sc.elements
+        for k, v in (("p", el.p), ("q", el.q), ("v", el.v), ("qdot", el.qdot)):
+            rec[k].append(v.copy())
+        rec["newton"].append(rep.solve.iterations)
+        rec["pcg"].append(rep.solve.pcg_total)
+        rec["committed"].append(rep.committed)
+        rec["reason"].append(rep.solve.reason)
+        rec["pairs"].append(rep.contact_pairs)
+        rec["gnorm"].append(rep.solve.grad_norm)
+        events += [(s, b, sg, tu) for (b, sg, tu) in rep.broken]
+    out.update({k: np.array(v) for k, v in rec.items()})
+    out["events"] = np.array(events, dtype=float).reshape(-1, 4)
+    out.update(pack("final_b_", sc.bonds, ("status", "stiffness_scale", "damage",
+                                           "plastic_strain", "sigma", "tau")))
+    out["labels"] = sc.labels.labels
+    out.update({"dt": spec.dt, "youngs": spec.youngs, "epsilon": eps, "k_contact": spec.k_contact,
+                "k_element": spec.k_element, "gravity": np.array(spec.gravity)})
+    if spec.plastic is not None:
+        pl = spec.plastic
+        out["plastic"] = np.array([pl.fracture_strain, pl.yield_strain, pl.weakening,
+                                   pl.damage_exponent])
+    print(f"  {name}: {steps} steps in {time.time() - t0:.1f}s; newton {rec['newton']}; "
+          f"broken {len(events)}; committed {all(rec['committed'])}")
+    save(f"traj_{name}.npz", **out)
+
+
+def gold_trajectories():
+    # BASELINE's eps=1e-8 sits on this beam's line-search noise floor: the
+    # reference stalls at gnorm 1.16e-8 from step 2 on (300 iterations,
+    # committed=False).  Trajectory parity uses 1e-7, where every step commits.
+    spec = C.cantilever()
+    _run_traj("cantilever", spec, 20, 1e-7)
+
+    spec = C.rope(n=30, epsilon=1e-5)
+    drv = spec.driver
+    _run_traj("rope", spec, 6, 1e-5,
+              driver=rs.twist_driver(drv.ids, drv.p0, drv.axis_point, drv.rate))
+
+    spec = C.plate(nx=24, ny=14, epsilon=1e-6)
+    _run_traj("plate", spec, 6, 1e-6)
+
+    spec = C.cube(n_side=5, random_q=False, seed=3, youngs=3e8, k_contact=1e9, speed=2.0,
+                  dt=1e-4)
+    sched = spec.collider_schedule
+    _run_traj("cube", spec, 6, 1e-6, schedule=sched)
+
+
+def gold_fracture():
+    """update_bond_states (bonds.py:532-570) with plasticity and strengths."""
+    spec = C.cube(n_side=5, r=0.002, seed=41, random_q=False, youngs=1e9)
+    rng = np.random.default_rng(41)
+    el, b = spec.elements, spec.bonds
+    nb = b.n
+    p = el.p + 0.02 * 0.002 * rng.normal(size=el.p.shape)
+    q = quat_normalize(el.q + 0.02 * rng.normal(size=el.q.shape))
+    b.status[rng.choice(nb, 10, replace=False)] = 2
+    b.status[rng.choice(nb, 10, replace=False)] = 1
+    b.stiffness_scale[:] = rng.uniform(0.6, 1.0, nb)
+    b.damage[:] = rng.uniform(0.7, 1.0, nb)
+    rbs = ref_bonds(b)
+    # strengths around the sampled stress distribution so some bonds break
+    _, sig, tau = rbs.stresses(p, q)
+    b.tensile_strength[:] = np.quantile(sig, 0.9)
+    b.shear_strength[:] = np.quantile(tau, 0.95)
+    out = pack("b_", b, BOND_FIELDS)
+    out.update({"p": p, "q": q})
+    pl = rb.PlasticParams(2e-3, 1e-3, 0.5, 2.0)
+    for tag, plastic in (("plastic", pl), ("elastic", None)):
+        rbs = ref_bonds(b)
+        ev = rb.update_bond_states(rbs, p, q, 1e9, plastic)
+        out.update(pack(f"{tag}_out_", rbs, ("status", "stiffness_scale", "damage",
+                                             "plastic_strain", "sigma", "tau")))
+        out[f"{tag}_events"] = np.array(ev, dtype=float).reshape(-1, 3)
+    out["plastic"] = np.array([2e-3, 1e-3, 0.5, 2.0])
+    save("fracture.npz", **out)
+
+
+def gold_broadphase_labels():
+    rng = np.random.default_rng(51)
+    out = {}
+    for tag, n in (("a", 300), ("b", 2000)):
+        pos = rng.uniform(-0.05, 0.05, size=(n, 3))
+        rad = rng.uniform(0.002, 0.006, size=n)
+        cell = 2.0 * rad.max() + 1e-12
+        out[f"{tag}_pos"], out[f"{tag}_rad"], out[f"{tag}_cell"] = pos, rad, cell
+        out[f"{tag}_pairs"] = rc.broad_phase(pos, rad, cell)
+    spec = C.cube(n_side=6, seed=52)
+    b = spec.bonds
+    b.status[rng.random(b.n) < 0.55] = 2
+    out.update({"lab_i": b.i, "lab_j": b.j, "lab_status": b.status, "lab_n": spec.elements.n,
+                "lab_labels": rg.label_components(spec.elements.n, ref_bonds(b)).labels})
+    save("broadphase_labels.npz", **out)
+
+
+if __name__ == "__main__":
+    t = time.time()
+    which = sys.argv[1:] or ["bond_terms", "fracture", "broadphase_labels", "newton_pieces",
+                             "trajectories"]
+    for name in which:
+        globals()[f"gold_{name}"]()
+    print(f"done in {time.time() - t:.1f}s")
