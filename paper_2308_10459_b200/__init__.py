@@ -1,0 +1,36 @@
+"""B200-native Newton hot path of the variational bonded discrete element
+method with quaternion manifold optimisation (arXiv 2308.10459).
+
+Drop-in for the reference package ``bdem``'s stepping API: scene and bond
+topology setup, ``stable_step``, the energy/gradient/Hessian entry points and
+the fracture update, all computed by hand-written sm_100a FP64 CUDA kernels
+in ``lib/libbdem_sm100.so`` (C ABI: ``include/bdem_sm100.h``).
+"""
+
+from .colliders import BoxCollider, HalfSpace, SphereCollider
+from .newton import (IterationRecord, LineSearchError, SolveResult, SolverConfig,
+                     minimize_second_order, relative_tolerance)
+from .scene import FragmentLabeling, Scene, stretch_driver, twist_driver
+from .state import (BROKEN, INTACT, WEAKENED, BondSet, DegenerateBondError,
+                    DegenerateShearError, ElementSet, PlasticParams)
+
+__all__ = [
+    "BondSet", "BoxCollider", "DegenerateBondError", "DegenerateShearError", "ElementSet",
+    "FragmentLabeling", "HalfSpace", "IterationRecord", "LineSearchError", "PlasticParams",
+    "Scene", "SolveResult", "SolverConfig", "SphereCollider", "StepReport", "broad_phase",
+    "energy_terms", "label_components", "minimize_second_order", "relative_tolerance",
+    "stable_step", "stretch_driver", "twist_driver", "update_bond_states",
+    "BROKEN", "INTACT", "WEAKENED",
+]
+
+
+def __getattr__(name):
+    # GPU-facing entry points import torch lazily so host-only use stays light
+    if name in ("stable_step", "StepReport", "broad_phase", "label_components",
+                "update_bond_states", "contact_candidates"):
+        from . import step
+        return getattr(step, name)
+    if name == "energy_terms":
+        from .bond_api import energy_terms
+        return energy_terms
+    raise AttributeError(name)

@@ -1,0 +1,93 @@
+// bdem_common.cuh -- launch helpers and deterministic reductions.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/bdem_sm100.h"
+
+namespace bdem {
+
+constexpr int kRedBlocks = BDEM_RED_BLOCKS;
+constexpr int kThreads = 256;
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int launch_status() {
+  return cudaGetLastError() == cudaSuccess ? BDEM_OK : BDEM_ERR_CUDA;
+}
+
+inline unsigned int grid_for(int64_t n, int threads = kThreads, int cap = 1 << 20) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<unsigned int>(g);
+}
+
+// Deterministic block sum: fixed xor-butterfly inside warps, fixed order
+// across warps.  Result valid in thread 0.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NT / 32; ++k) s += sh[k];
+  }
+  return s;
+}
+
+template <int NT>
+__device__ __forceinline__ double block_max(double v, double *sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NT / 32; ++k) s = fmax(s, sh[k]);
+  }
+  return s;
+}
+
+// partial layout: red[col * kRedBlocks + block]
+__device__ __forceinline__ double *red_slot(double *red, int col, int block) {
+  return red + static_cast<int64_t>(col) * kRedBlocks + block;
+}
+
+// "last block finishes" pattern: every block has stored its partials; the
+// block that increments `counter` last sums them in a fixed order.  Returns
+// true in all threads of the last block.
+__device__ __forceinline__ bool last_block(unsigned int *counter) {
+  __shared__ bool am_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int t = atomicAdd(counter, 1u);
+    am_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (am_last) {
+    __threadfence();
+    if (threadIdx.x == 0) *counter = 0u;
+  }
+  return am_last;
+}
+
+// fixed-order sum of nb partials of one column, by one block
+template <int NT>
+__device__ __forceinline__ double sum_partials(const double *red, int col, int nb, double *sh) {
+  double v = 0.0;
+  const volatile double *col_ptr = red + static_cast<int64_t>(col) * kRedBlocks;
+  for (int b = threadIdx.x; b < nb; b += NT) v += col_ptr[b];
+  return block_sum<NT>(v, sh);
+}
+
+}  // namespace bdem

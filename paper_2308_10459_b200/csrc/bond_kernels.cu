@@ -1,0 +1,405 @@
+// bond_kernels.cu -- per-bond kernels: ambient debug evaluation, the fused
+// production assembly (energy + gradient + SPD-clamped reduced blocks),
+// the line-search energy pass and the fracture/plasticity update.
+//
+// One thread per bond; bond data are structure-of-arrays planes so every
+// load and store of a warp is a coalesced 256-byte transaction.  Endpoint
+// states (p: 24 B, q: 32 B rows) are gathered through L1/L2.
+#include "bdem_common.cuh"
+#include "bdem_math.cuh"
+
+namespace bdem {
+
+struct BondIn {
+  int i, j;
+  int8_t status;
+  double l0, d0[3], F[3][3], kn, kt, kd[3], scale;
+};
+
+__device__ __forceinline__ void load_bond(const bdem_system_t &S, int64_t b, BondIn &B) {
+  const int64_t nb = S.n_bond;
+  const double *g = S.geom;
+  B.i = S.bond_i[b];
+  B.j = S.bond_j[b];
+  B.status = S.status[b];
+  B.l0 = g[BDEM_BG_L0 * nb + b];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) B.d0[c] = g[(BDEM_BG_D0 + c) * nb + b];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) B.F[r][c] = g[(BDEM_BG_FRAME + 3 * r + c) * nb + b];
+  B.kn = g[BDEM_BG_KN * nb + b];
+  B.kt = g[BDEM_BG_KT * nb + b];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) B.kd[c] = g[(BDEM_BG_KDIAG + c) * nb + b];
+  B.scale = S.bstate[BDEM_BS_SCALE * nb + b];
+}
+
+__device__ __forceinline__ void load_pq(const double *p, const double *q, int e, double pe[3],
+                                        double qe[4]) {
+  pe[0] = p[3 * (int64_t)e + 0];
+  pe[1] = p[3 * (int64_t)e + 1];
+  pe[2] = p[3 * (int64_t)e + 2];
+  const double2 *q2 = reinterpret_cast<const double2 *>(q) + 2 * (int64_t)e;
+  const double2 a = q2[0], c = q2[1];
+  qe[0] = a.x; qe[1] = a.y; qe[2] = c.x; qe[3] = c.y;
+}
+
+__device__ __forceinline__ void flag_error(int32_t *err, int kind, int64_t b) {
+  const int cnt = kind == BDEM_ERR_DEGENERATE_BOND ? BDEM_ERRSLOT_DEGENERATE_COUNT
+                                                    : BDEM_ERRSLOT_ANTIPODAL_COUNT;
+  atomicAdd(&err[cnt], 1);
+  atomicMin(&err[cnt + 1], static_cast<int32_t>(b));
+}
+
+// ---------------------------------------------------------------------------
+// ambient debug kernel: BondSet.energy_terms (bonds.py:473-504)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_bond_ambient(bdem_system_t S, const double *p,
+                                                      const double *q, int64_t n_idx,
+                                                      const int32_t *idx, double *E,
+                                                      double *gpi, double *gpj, double *gqi,
+                                                      double *gqj, double *hpp, double *hqq,
+                                                      int want_hess) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n_idx) return;
+  const int64_t b = idx[t];
+  BondIn B;
+  load_bond(S, b, B);
+  double pi[3], pj[3], qi[4], qj[4];
+  load_pq(p, q, B.i, pi, qi);
+  load_pq(p, q, B.j, pj, qj);
+  const double ks = B.scale * B.kn, kts = B.scale * B.kt;
+  double kds[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) kds[c] = B.scale * B.kd[c];
+  const Stretch st = stretch_eval(pi, pj, B.l0, ks);
+  const Shear sh = shear_eval(qi, qj, B.d0, kts);
+  const BendTwist bt = bendtwist_eval(qi, qj, B.F, kds);
+  if (st.degenerate) flag_error(S.err, BDEM_ERR_DEGENERATE_BOND, b);
+  if (sh.antipodal) flag_error(S.err, BDEM_ERR_ANTIPODAL, b);
+  E[t] = (st.E + sh.E) + bt.E;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    gpi[3 * t + c] = -st.gj[c];
+    gpj[3 * t + c] = st.gj[c];
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    gqi[4 * t + c] = sh.g[c] + bt.gi[c];
+    gqj[4 * t + c] = sh.g[c] + bt.gj[c];
+  }
+  if (!want_hess) return;
+  double a[6];
+  stretch_block(st, st.c_over_l, a);
+  double *H = hpp + 36 * t;
+  const int sym3[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double v = a[sym3[r][c]];
+      H[6 * r + c] = v;
+      H[6 * (r + 3) + c + 3] = v;
+      H[6 * r + c + 3] = -v;
+      H[6 * (r + 3) + c] = -v;
+    }
+  double hu[4][4], Hb[4][4];
+  shear_hu(sh, B.d0, hu);
+  double *Q = hqq + 64 * t;
+  for (int which = 0; which < 3; ++which) {
+    bendtwist_block(bt, B.F, which, Hb);
+    const int r0 = (which == 1) ? 4 : 0, c0 = (which == 0) ? 0 : 4;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double v = hu[r][c] + Hb[r][c];
+        Q[8 * (r0 + r) + c0 + c] = v;
+        if (which == 2) Q[8 * (c0 + c) + r0 + r] = hu[c][r] + Hb[r][c];
+      }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fused production kernel: energy, gradient contributions and the clamped
+// reduced blocks (energy_terms + build_clamped_pieces, solver.py:141-162)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_bond_assemble(bdem_system_t S, const double *p,
+                                                       const double *q) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nb = S.n_bond;
+  if (b >= nb) return;
+  double *st_out = S.stage;
+  if (S.status[b] == 2) {
+#pragma unroll
+    for (int k = 0; k < BDEM_ST_COUNT; ++k) st_out[k * nb + b] = 0.0;
+    return;
+  }
+  BondIn B;
+  load_bond(S, b, B);
+  double pi[3], pj[3], qi[4], qj[4];
+  load_pq(p, q, B.i, pi, qi);
+  load_pq(p, q, B.j, pj, qj);
+  const double ks = B.scale * B.kn, kts = B.scale * B.kt;
+  double kds[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) kds[c] = B.scale * B.kd[c];
+
+  // stretch: energy, gradient and the closed-form clamp of [[a,-a],[-a,a]]
+  const Stretch st = stretch_eval(pi, pj, B.l0, ks);
+  if (st.degenerate) flag_error(S.err, BDEM_ERR_DEGENERATE_BOND, b);
+  double apos[6];
+  stretch_block(st, st.c_over_l > 0.0 ? st.c_over_l : 0.0, apos);
+
+  const Shear sh = shear_eval(qi, qj, B.d0, kts);
+  if (sh.antipodal) flag_error(S.err, BDEM_ERR_ANTIPODAL, b);
+  const BendTwist bt = bendtwist_eval(qi, qj, B.F, kds);
+
+  st_out[BDEM_ST_E * nb + b] = (st.E + sh.E) + bt.E;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) st_out[(BDEM_ST_GPJ + c) * nb + b] = st.gj[c];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    st_out[(BDEM_ST_GQI + c) * nb + b] = sh.g[c] + bt.gi[c];
+    st_out[(BDEM_ST_GQJ + c) * nb + b] = sh.g[c] + bt.gj[c];
+  }
+#pragma unroll
+  for (int c = 0; c < 6; ++c) st_out[(BDEM_ST_APOS + c) * nb + b] = apos[c];
+
+  // reduced rotation block T H_qq T^T with T = blockdiag(G_l(q_i), G_l(q_j))
+  double Gi[3][4], Gj[3][4];
+  gl_mat(qi, Gi);
+  gl_mat(qj, Gj);
+  double hu[4][4], H[4][4], R[3][3];
+  shear_hu(sh, B.d0, hu);
+  double S6[21];
+  // (i,i)
+  bendtwist_block(bt, B.F, 0, H);
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) H[r][c] = hu[r][c] + H[r][c];
+  reduce_block(Gi, H, Gi, R);
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = r; c < 3; ++c) S6[sidx<6>(r, c)] = 0.5 * (R[r][c] + R[c][r]);
+  // (j,j)
+  bendtwist_block(bt, B.F, 1, H);
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) H[r][c] = hu[r][c] + H[r][c];
+  reduce_block(Gj, H, Gj, R);
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = r; c < 3; ++c) S6[sidx<6>(r + 3, c + 3)] = 0.5 * (R[r][c] + R[c][r]);
+  // (i,j)
+  bendtwist_block(bt, B.F, 2, H);
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) H[r][c] = hu[r][c] + H[r][c];
+  reduce_block(Gi, H, Gj, R);
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) S6[sidx<6>(r, c + 3)] = R[r][c];
+
+  psd_clamp<6>(S6);
+
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) st_out[(BDEM_ST_C + 3 * r + c) * nb + b] = S6[sidx<6>(r, c + 3)];
+  const int pr[6] = {0, 0, 0, 1, 1, 2}, pc[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+  for (int t = 0; t < 6; ++t) {
+    st_out[(BDEM_ST_A + t) * nb + b] = S6[sidx<6>(pr[t], pc[t])];
+    st_out[(BDEM_ST_D + t) * nb + b] = S6[sidx<6>(pr[t] + 3, pc[t] + 3)];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// energy-only pass (PotentialModel.value, integrator.py:87-89)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_bond_energy(bdem_system_t S, const double *p,
+                                                          const double *q, int col) {
+  __shared__ double sh_red[kThreads / 32];
+  double acc = 0.0;
+  const int64_t nb = S.n_bond;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    if (S.status[b] == 2) continue;
+    const int i = S.bond_i[b], j = S.bond_j[b];
+    const double *g = S.geom;
+    const double sc = S.bstate[BDEM_BS_SCALE * nb + b];
+    double pi[3], pj[3], qi[4], qj[4];
+    load_pq(p, q, i, pi, qi);
+    load_pq(p, q, j, pj, qj);
+    // stretch
+    const double l0 = g[BDEM_BG_L0 * nb + b];
+    const double d0_ = pj[0] - pi[0], d1_ = pj[1] - pi[1], d2_ = pj[2] - pi[2];
+    const double len = sqrt((d0_ * d0_ + d1_ * d1_) + d2_ * d2_);
+    if (len < kDegenerateRel * l0) flag_error(S.err, BDEM_ERR_DEGENERATE_BOND, b);
+    const double c = len - l0;
+    const double e_s = 0.5 * (sc * g[BDEM_BG_KN * nb + b]) * (c * c);
+    // shear
+    double d0[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) d0[k] = g[(BDEM_BG_D0 + k) * nb + b];
+    double u[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) u[k] = qi[k] + qj[k];
+    const double un2 = ((u[0] * u[0] + u[1] * u[1]) + u[2] * u[2]) + u[3] * u[3];
+    if (un2 < kAntipodalTol * kAntipodalTol) flag_error(S.err, BDEM_ERR_ANTIPODAL, b);
+    const double proj = (d0[0] * u[0] + d0[1] * u[1]) + d0[2] * u[2];
+    const double utut = (u[0] * u[0] + u[1] * u[1]) + u[2] * u[2];
+    double rho = ((2.0 * (proj * proj)) - utut + u[3] * u[3]) / un2;
+    rho = rho < -1.0 + 1e-12 ? -1.0 + 1e-12 : rho;
+    rho = rho > 1.0 ? 1.0 : rho;
+    const double th = acos(rho);
+    const double e_h = 0.5 * (sc * g[BDEM_BG_KT * nb + b]) * (th * th);
+    // bend/twist: t = F G_l(q_j) q_i
+    double v[3];
+    gl_apply(qj, qi, v);
+    double e_b = 0.0;
+    {
+      double t[3], kt[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        t[r] = (g[(BDEM_BG_FRAME + 3 * r) * nb + b] * v[0] +
+                g[(BDEM_BG_FRAME + 3 * r + 1) * nb + b] * v[1]) +
+               g[(BDEM_BG_FRAME + 3 * r + 2) * nb + b] * v[2];
+        kt[r] = (sc * g[(BDEM_BG_KDIAG + r) * nb + b]) * t[r];
+      }
+      e_b = 0.5 * ((t[0] * kt[0] + t[1] * kt[1]) + t[2] * kt[2]);
+    }
+    acc += (e_s + e_h) + e_b;
+  }
+  const double s = block_sum<kThreads>(acc, sh_red);
+  if (threadIdx.x == 0) *red_slot(S.red, col, blockIdx.x) = s;
+}
+
+// ---------------------------------------------------------------------------
+// fracture / plasticity update (bonds.py:506-570)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double pow_np(double x, double a) {
+  // numpy's float power fast paths for the scalar exponents it special-cases
+  if (a == 2.0) return x * x;
+  if (a == 1.0) return x;
+  if (a == 0.5) return sqrt(x);
+  return pow(x, a);
+}
+
+__global__ void __launch_bounds__(kThreads) k_bond_update(bdem_system_t S, const double *p,
+                                                          const double *q, double youngs,
+                                                          int plastic_on, double eps_c,
+                                                          double eps_y, double weak,
+                                                          double dexp, uint8_t *flags) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nb = S.n_bond;
+  if (b >= nb) return;
+  const int8_t status = S.status[b];
+  if (status == 2) {
+    flags[b] = 0;
+    return;
+  }
+  const double *g = S.geom;
+  double *bs = S.bstate;
+  const int i = S.bond_i[b], j = S.bond_j[b];
+  double pi[3], pj[3], qi[4], qj[4];
+  load_pq(p, q, i, pi, qi);
+  load_pq(p, q, j, pj, qj);
+  double scale = bs[BDEM_BS_SCALE * nb + b];
+  const double l0 = g[BDEM_BG_L0 * nb + b];
+  const double d0_ = pj[0] - pi[0], d1_ = pj[1] - pi[1], d2_ = pj[2] - pi[2];
+  const double len = sqrt((d0_ * d0_ + d1_ * d1_) + d2_ * d2_);
+  const double fn = (scale * g[BDEM_BG_KN * nb + b]) * fabs(len - l0);
+  double v[3], t[3], kt[3];
+  gl_apply(qj, qi, v);
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    t[r] = (g[(BDEM_BG_FRAME + 3 * r) * nb + b] * v[0] +
+            g[(BDEM_BG_FRAME + 3 * r + 1) * nb + b] * v[1]) +
+           g[(BDEM_BG_FRAME + 3 * r + 2) * nb + b] * v[2];
+    kt[r] = (scale * g[(BDEM_BG_KDIAG + r) * nb + b]) * t[r];
+  }
+  const double mt = fabs(kt[0]);
+  const double mb = hypot(kt[1], kt[2]);
+  const double r0 = g[BDEM_BG_RADIUS * nb + b];
+  const double section = bs[BDEM_BS_DAMAGE * nb + b] * g[BDEM_BG_SECTION * nb + b];
+  const double sigma = fn / section + (mb * r0) / g[BDEM_BG_SECOND * nb + b];
+  const double tau = (mt * r0) / g[BDEM_BG_POLAR * nb + b];
+  bs[BDEM_BS_SIGMA * nb + b] = sigma;
+  bs[BDEM_BS_TAU * nb + b] = tau;
+  bool broke = false;
+  int8_t new_status = status;
+  if (plastic_on) {
+    const double strain = (len - l0) / l0;
+    const double sy = youngs * eps_y;
+    const double vm = sqrt(sigma * sigma + 3.0 * (tau * tau));
+    if (vm > sy) {
+      const double k_new = 1.0 - weak * (1.0 - sy / vm);
+      scale = fmin(scale, k_new);
+      bs[BDEM_BS_SCALE * nb + b] = scale;
+      const double ep = fmax(0.0, strain - eps_y);
+      bs[BDEM_BS_PLASTIC * nb + b] = fmax(bs[BDEM_BS_PLASTIC * nb + b], ep);
+      bs[BDEM_BS_DAMAGE * nb + b] = fmin(bs[BDEM_BS_DAMAGE * nb + b], exp(-pow_np(ep, dexp)));
+      if (new_status < 1) new_status = 1;
+    }
+    broke |= strain > eps_c;
+  }
+  broke |= (sigma > g[BDEM_BG_TENSILE * nb + b]) || (tau > g[BDEM_BG_SHEAR * nb + b]);
+  if (broke) new_status = 2;
+  if (new_status != status) S.status[b] = new_status;
+  flags[b] = broke ? 1 : 0;
+}
+
+}  // namespace bdem
+
+using namespace bdem;
+
+extern "C" {
+
+int bdem_bond_eval_ambient(const bdem_system_t *sys, const double *p, const double *q,
+                           int64_t n_idx, const int32_t *idx, double *E, double *gpi,
+                           double *gpj, double *gqi, double *gqj, double *hpp, double *hqq,
+                           int want_hess, void *stream) {
+  if (!sys || n_idx < 0) return BDEM_ERR_ARG;
+  if (n_idx == 0) return BDEM_OK;
+  k_bond_ambient<<<grid_for(n_idx, 128), 128, 0, as_stream(stream)>>>(
+      *sys, p, q, n_idx, idx, E, gpi, gpj, gqi, gqj, hpp, hqq, want_hess);
+  return launch_status();
+}
+
+int bdem_bond_assemble(const bdem_system_t *sys, const double *p, const double *q,
+                       void *stream) {
+  if (!sys) return BDEM_ERR_ARG;
+  if (sys->n_bond == 0) return BDEM_OK;
+  k_bond_assemble<<<grid_for(sys->n_bond, 128), 128, 0, as_stream(stream)>>>(*sys, p, q);
+  return launch_status();
+}
+
+int bdem_bond_energy(const bdem_system_t *sys, const double *p, const double *q, int col,
+                     void *stream) {
+  if (!sys || col < 0 || col >= BDEM_SC_COUNT) return BDEM_ERR_ARG;
+  k_bond_energy<<<kRedBlocks, kThreads, 0, as_stream(stream)>>>(*sys, p, q, col);
+  return launch_status();
+}
+
+int bdem_bond_update(const bdem_system_t *sys, const double *p, const double *q,
+                     double youngs, const double *plastic, uint8_t *flags, void *stream) {
+  if (!sys) return BDEM_ERR_ARG;
+  if (sys->n_bond == 0) return BDEM_OK;
+  const int on = plastic != nullptr;
+  k_bond_update<<<grid_for(sys->n_bond), kThreads, 0, as_stream(stream)>>>(
+      *sys, p, q, youngs, on, on ? plastic[0] : 0.0, on ? plastic[1] : 0.0,
+      on ? plastic[2] : 0.0, on ? plastic[3] : 1.0, flags);
+  return launch_status();
+}
+
+}  // extern "C"

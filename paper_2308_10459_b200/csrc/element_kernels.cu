@@ -1,0 +1,540 @@
+// element_kernels.cu -- per-element kernels: ordered gradient gather,
+// reduced gradient, diagonal blocks + block-Jacobi inverses, objective
+// reductions, line-search trial point, predictor and velocity update.
+//
+// The gather reproduces np.add.at's sequential order (integrator.py:98-103):
+// for element e, first the bonds with i == e (ascending), then the bonds
+// with j == e (ascending), then contact pairs the same way, then colliders,
+// then gravity and inertia.  No atomics: results are deterministic and,
+// up to the per-bond arithmetic, bit-identical in summation order.
+#include "bdem_common.cuh"
+#include "bdem_math.cuh"
+
+namespace bdem {
+
+__device__ __forceinline__ void load_p(const double *p, int64_t e, double pe[3]) {
+  pe[0] = p[3 * e + 0];
+  pe[1] = p[3 * e + 1];
+  pe[2] = p[3 * e + 2];
+}
+__device__ __forceinline__ void load_q(const double *q, int64_t e, double qe[4]) {
+  const double2 *q2 = reinterpret_cast<const double2 *>(q) + 2 * e;
+  const double2 a = q2[0], c = q2[1];
+  qe[0] = a.x; qe[1] = a.y; qe[2] = c.x; qe[3] = c.y;
+}
+__device__ __forceinline__ void store_q(double *q, int64_t e, const double qe[4]) {
+  double2 *q2 = reinterpret_cast<double2 *>(q) + 2 * e;
+  q2[0] = make_double2(qe[0], qe[1]);
+  q2[1] = make_double2(qe[2], qe[3]);
+}
+
+// collider SDF value, gradient and Hessian (contact.py:38-133)
+__device__ void collider_eval(const bdem_collider_t &C, const double p[3], double &g,
+                              double dg[3], double H[6]) {
+#pragma unroll
+  for (int t = 0; t < 6; ++t) H[t] = 0.0;
+  if (C.kind == BDEM_COLLIDER_HALFSPACE) {
+    g = ((p[0] * C.a[0] + p[1] * C.a[1]) + p[2] * C.a[2]) - C.a[3];
+    dg[0] = C.a[0]; dg[1] = C.a[1]; dg[2] = C.a[2];
+  } else if (C.kind == BDEM_COLLIDER_SPHERE) {
+    const double d[3] = {p[0] - C.a[0], p[1] - C.a[1], p[2] - C.a[2]};
+    const double r = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+    const double rs = fmax(r, 1e-12);
+    g = r - C.a[3];
+    double n[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) { n[c] = d[c] / rs; dg[c] = n[c]; }
+    const int pr[6] = {0, 0, 0, 1, 1, 2}, pc[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+    for (int t = 0; t < 6; ++t) H[t] = ((pr[t] == pc[t] ? 1.0 : 0.0) - n[pr[t]] * n[pc[t]]) / rs;
+  } else {  // box
+    double loc[3], d[3], pos[3], sign[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      loc[c] = p[c] - C.a[c];
+      d[c] = fabs(loc[c]) - C.a[3 + c];
+      pos[c] = fmax(d[c], 0.0);
+      sign[c] = loc[c] >= 0.0 ? 1.0 : -1.0;
+    }
+    const double on = sqrt((pos[0] * pos[0] + pos[1] * pos[1]) + pos[2] * pos[2]);
+    const double inside = fmin(fmax(fmax(d[0], d[1]), d[2]), 0.0);
+    g = on + inside;
+    if (on > 0.0) {
+      const double ons = fmax(on, 1e-300);
+      double n[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) { n[c] = sign[c] * pos[c] / ons; dg[c] = n[c]; }
+      const int pr[6] = {0, 0, 0, 1, 1, 2}, pc[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+      for (int t = 0; t < 6; ++t) {
+        const double act = (pr[t] == pc[t] && pos[pr[t]] > 0.0) ? 1.0 : 0.0;
+        H[t] = (act - n[pr[t]] * n[pc[t]]) / ons;
+      }
+    } else {
+      int ax = 0;
+      if (d[1] > d[ax]) ax = 1;
+      if (d[2] > d[ax]) ax = 2;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) dg[c] = (c == ax ? 1.0 : 0.0) * sign[c];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// element assembly
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_element_assemble(bdem_system_t S, const double *p,
+                                                               const double *q, double *z) {
+  __shared__ double sh[kThreads / 32];
+  double acc_f = 0.0, acc_g2 = 0.0, acc_c2 = 0.0, acc_dev = 0.0, acc_sing = 0.0;
+  const int64_t nb = S.n_bond, pc = S.pair_cap;
+  const double *st = S.stage;
+  bool any_col_hess = false;
+  for (int i = 0; i < S.n_colliders; ++i) any_col_hess |= S.colliders[i].kind != BDEM_COLLIDER_HALFSPACE;
+
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < S.n_elem;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double pe[3], qe[4];
+    load_p(p, e, pe);
+    load_q(q, e, qe);
+    double gp[3] = {0.0, 0.0, 0.0}, gq[4] = {0.0, 0.0, 0.0, 0.0};
+    double P[6] = {0, 0, 0, 0, 0, 0}, R[6] = {0, 0, 0, 0, 0, 0};
+    double ebond = 0.0;
+    const int a0 = S.adj_ptr[e], am = S.adj_mid[e], a1 = S.adj_ptr[e + 1];
+    for (int k = a0; k < am; ++k) {  // bonds with i == e
+      const int64_t b = S.adj_bond[k];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) gp[c] += -st[(BDEM_ST_GPJ + c) * nb + b];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) gq[c] += st[(BDEM_ST_GQI + c) * nb + b];
+#pragma unroll
+      for (int t = 0; t < 6; ++t) {
+        P[t] += st[(BDEM_ST_APOS + t) * nb + b];
+        R[t] += st[(BDEM_ST_A + t) * nb + b];
+      }
+      ebond += st[BDEM_ST_E * nb + b];
+    }
+    for (int k = am; k < a1; ++k) {  // bonds with j == e
+      const int64_t b = S.adj_bond[k];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) gp[c] += st[(BDEM_ST_GPJ + c) * nb + b];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) gq[c] += st[(BDEM_ST_GQJ + c) * nb + b];
+#pragma unroll
+      for (int t = 0; t < 6; ++t) {
+        P[t] += st[(BDEM_ST_APOS + t) * nb + b];
+        R[t] += st[(BDEM_ST_D + t) * nb + b];
+      }
+    }
+    // contacts: pairs then colliders into a separate accumulator (integrator.py:56-85,104-105)
+    double gc[3] = {0.0, 0.0, 0.0};
+    double epair = 0.0, ecol = 0.0;
+    if (S.n_pair > 0) {
+      const double *ps = S.pstage;
+      for (int k = S.pi_ptr[e]; k < S.pi_ptr[e + 1]; ++k) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) gc[c] += ps[(BDEM_PS_GI + c) * pc + k];
+#pragma unroll
+        for (int t = 0; t < 6; ++t) P[t] += ps[(BDEM_PS_A + t) * pc + k];
+        epair += ps[BDEM_PS_E * pc + k];
+      }
+      for (int kk = S.pj_ptr[e]; kk < S.pj_ptr[e + 1]; ++kk) {
+        const int64_t k = S.pj_idx[kk];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) gc[c] += -ps[(BDEM_PS_GI + c) * pc + k];
+#pragma unroll
+        for (int t = 0; t < 6; ++t) P[t] += ps[(BDEM_PS_A + t) * pc + k];
+      }
+    }
+    double Hc[6] = {0, 0, 0, 0, 0, 0};
+    bool hc_nonzero = false;
+    for (int ci = 0; ci < S.n_colliders; ++ci) {
+      double g, dg[3], Hs[6];
+      collider_eval(S.colliders[ci], pe, g, dg, Hs);
+      if (g < 0.0) {
+        const double k = S.k_contact;
+        ecol += 0.5 * k * (g * g);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) gc[c] += (k * g) * dg[c];
+        const int pr[6] = {0, 0, 0, 1, 1, 2}, pcc[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+        for (int t = 0; t < 6; ++t) Hc[t] += k * (dg[pr[t]] * dg[pcc[t]] + g * Hs[t]);
+        hc_nonzero = true;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) gp[c] += gc[c];
+    const double m = S.mass[e];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) gp[c] -= m * S.gravity[c];
+    const double pg = (pe[0] * S.gravity[0] + pe[1] * S.gravity[1]) + pe[2] * S.gravity[2];
+    double fe = ((ebond + epair) + ecol) - m * pg;
+
+    const int s = S.slot[e];
+    if (s >= 0) {
+      const double mp = S.mp_dt2[e], mq = S.mq_dt2[e];
+      double dpv[3], dqv[4];
+      const double2 *ph2 = nullptr;
+      (void)ph2;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) dpv[c] = pe[c] - S.p_hat[3 * e + c];
+      double qh[4];
+      load_q(S.q_hat, e, qh);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dqv[c] = qe[c] - qh[c];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) gp[c] = gp[c] + mp * dpv[c];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) gq[c] = gq[c] + mq * dqv[c];
+      fe += 0.5 * (mp * ((dpv[0] * dpv[0] + dpv[1] * dpv[1]) + dpv[2] * dpv[2])) +
+            0.5 * (mq * (((dqv[0] * dqv[0] + dqv[1] * dqv[1]) + dqv[2] * dqv[2]) + dqv[3] * dqv[3]));
+      // reduced gradient (solver.py:116-123)
+      double zr[3];
+      gl_apply(qe, gq, zr);
+      double *zs = z + 6 * (int64_t)s;
+      zs[0] = gp[0]; zs[1] = gp[1]; zs[2] = gp[2];
+      zs[3] = zr[0]; zs[4] = zr[1]; zs[5] = zr[2];
+      acc_g2 += (((gp[0] * gp[0] + gp[1] * gp[1]) + gp[2] * gp[2]) +
+                 ((zr[0] * zr[0] + zr[1] * zr[1]) + zr[2] * zr[2]));
+      const double qq = ((qe[0] * qe[0] + qe[1] * qe[1]) + qe[2] * qe[2]) + qe[3] * qe[3];
+      const double cons = 0.5 * (qq - 1.0);
+      acc_c2 += cons * cons;
+      acc_dev = fmax(acc_dev, fabs(sqrt(qq) - 1.0));
+      // element terms (solver.py:164-173) and diagonal blocks (solver.py:231-237)
+      double Ep[6] = {mp, 0.0, 0.0, mp, 0.0, mp};
+      if (hc_nonzero) {
+#pragma unroll
+        for (int t = 0; t < 6; ++t) Ep[t] = Hc[t] + Ep[t];
+        if (any_col_hess) psd_clamp<3>(Ep);
+      }
+      const double curv = -(((qe[0] * gq[0] + qe[1] * gq[1]) + qe[2] * gq[2]) + qe[3] * gq[3]);
+      const double erot = fmax(mq + curv, 0.0);
+#pragma unroll
+      for (int t = 0; t < 6; ++t) P[t] += Ep[t];
+      R[0] += erot; R[3] += erot; R[5] += erot;
+      double *dg = S.diag + 12 * (int64_t)s;
+      double *mi = S.minv + 12 * (int64_t)s;
+#pragma unroll
+      for (int t = 0; t < 6; ++t) { dg[t] = P[t]; dg[6 + t] = R[t]; }
+      // block-Jacobi (linalg.py:100-121): singular -> identity
+      double lp, ap_, lr, ar;
+      eig3_minmax(P, lp, ap_);
+      eig3_minmax(R, lr, ar);
+      const double scale = fmax(fmax(ap_, ar), 1e-300);
+      if (fmin(lp, lr) <= 1e-12 * scale) {
+        const double I6[6] = {1, 0, 0, 1, 0, 1};
+#pragma unroll
+        for (int t = 0; t < 6; ++t) { mi[t] = I6[t]; mi[6 + t] = I6[t]; }
+        acc_sing += 1.0;
+      } else {
+        double Pi[6], Ri[6];
+        inv3_sym(P, Pi);
+        inv3_sym(R, Ri);
+#pragma unroll
+        for (int t = 0; t < 6; ++t) { mi[t] = Pi[t]; mi[6 + t] = Ri[t]; }
+      }
+    }
+    acc_f += fe;
+  }
+  double v;
+  v = block_sum<kThreads>(acc_f, sh);
+  if (threadIdx.x == 0) *red_slot(S.red, BDEM_SC_F, blockIdx.x) = v;
+  v = block_sum<kThreads>(acc_g2, sh);
+  if (threadIdx.x == 0) *red_slot(S.red, BDEM_SC_GNORM2, blockIdx.x) = v;
+  v = block_sum<kThreads>(acc_c2, sh);
+  if (threadIdx.x == 0) *red_slot(S.red, BDEM_SC_CNORM2, blockIdx.x) = v;
+  v = block_max<kThreads>(acc_dev, sh);
+  if (threadIdx.x == 0) *red_slot(S.red, BDEM_SC_MAXDEV, blockIdx.x) = v;
+  v = block_sum<kThreads>(acc_sing, sh);
+  if (threadIdx.x == 0) *red_slot(S.red, BDEM_SC_NSING, blockIdx.x) = v;
+}
+
+// fixed-order finish of per-block partials -> scalars
+__global__ void __launch_bounds__(kThreads) k_reduce_finish(bdem_system_t S, int col0, int ncol,
+                                                            int nblocks) {
+  __shared__ double sh[kThreads / 32];
+  for (int c = col0; c < col0 + ncol; ++c) {
+    double v;
+    if (c == BDEM_SC_MAXDEV) {
+      double m = 0.0;
+      for (int b = threadIdx.x; b < nblocks; b += kThreads) m = fmax(m, *red_slot(S.red, c, b));
+      v = block_max<kThreads>(m, sh);
+    } else {
+      v = sum_partials<kThreads>(S.red, c, nblocks, sh);
+    }
+    if (threadIdx.x == 0) S.scalars[c] = v;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// element part of the objective at an (optionally moved) point
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_element_energy(bdem_system_t S, const double *p,
+                                                             const double *q, const double *dp,
+                                                             const double *dq, double alpha,
+                                                             double *pt, double *qt,
+                                                             int with_inertia) {
+  __shared__ double sh[kThreads / 32];
+  double acc_in = 0.0, acc_col = 0.0, acc_g = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < S.n_elem;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double pe[3], qe[4];
+    load_p(p, e, pe);
+    load_q(q, e, qe);
+    const bool fr = S.slot[e] >= 0;
+    if (dp != nullptr) {
+      // p_t = p + alpha dp ; q_t = normalize(geodesic(q, alpha dq)) on free rows
+      double dpe[3];
+      load_p(dp, e, dpe);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) pe[c] = pe[c] + alpha * dpe[c];
+      if (fr) {
+        double dqe[4], ad[4], out[4];
+        load_q(dq, e, dqe);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) ad[c] = alpha * dqe[c];
+        retract_normalize(qe, ad, out);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) qe[c] = out[c];
+      }
+      pt[3 * e + 0] = pe[0]; pt[3 * e + 1] = pe[1]; pt[3 * e + 2] = pe[2];
+      store_q(qt, e, qe);
+    }
+    for (int ci = 0; ci < S.n_colliders; ++ci) {
+      double g, dg[3], Hs[6];
+      collider_eval(S.colliders[ci], pe, g, dg, Hs);
+      if (g < 0.0) acc_col += 0.5 * S.k_contact * (g * g);
+    }
+    acc_g += -(S.mass[e] * ((pe[0] * S.gravity[0] + pe[1] * S.gravity[1]) + pe[2] * S.gravity[2]));
+    if (with_inertia && fr) {
+      double dpv[3], dqv[4], qh[4];
+      load_q(S.q_hat, e, qh);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) dpv[c] = pe[c] - S.p_hat[3 * e + c];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dqv[c] = qe[c] - qh[c];
+      acc_in += 0.5 * (S.mp_dt2[e] * ((dpv[0] * dpv[0] + dpv[1] * dpv[1]) + dpv[2] * dpv[2])) +
+                0.5 * (S.mq_dt2[e] *
+                       (((dqv[0] * dqv[0] + dqv[1] * dqv[1]) + dqv[2] * dqv[2]) + dqv[3] * dqv[3]));
+    }
+  }
+  double v;
+  v = block_sum<kThreads>(acc_in, sh);
+  if (threadIdx.x == 0) *red_slot(S.red, BDEM_SC_FT, blockIdx.x) = v;
+  v = block_sum<kThreads>(acc_col, sh);
+  if (threadIdx.x == 0) *red_slot(S.red, BDEM_SC_ECOL, blockIdx.x) = v;
+  v = block_sum<kThreads>(acc_g, sh);
+  if (threadIdx.x == 0) *red_slot(S.red, BDEM_SC_EGRAV, blockIdx.x) = v;
+}
+
+// kinetic energy (elements.py:114-117) -> partial column EKIN
+__global__ void __launch_bounds__(kThreads) k_kinetic(bdem_system_t S, const double *v,
+                                                      const double *qd) {
+  __shared__ double sh[kThreads / 32];
+  double acc = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < S.n_elem;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double ve[3], we[4];
+    load_p(v, e, ve);
+    load_q(qd, e, we);
+    const double m = S.mass[e], r = S.radius[e];
+    acc += 0.5 * (m * ((ve[0] * ve[0] + ve[1] * ve[1]) + ve[2] * ve[2])) +
+           0.5 * (((1.6 * m) * (r * r)) * (((we[0] * we[0] + we[1] * we[1]) + we[2] * we[2]) + we[3] * we[3]));
+  }
+  const double s = block_sum<kThreads>(acc, sh);
+  if (threadIdx.x == 0) *red_slot(S.red, BDEM_SC_EKIN, blockIdx.x) = s;
+}
+
+// ---------------------------------------------------------------------------
+// direction, predictor, velocity update, normalisation
+// ---------------------------------------------------------------------------
+__global__ void k_direction(bdem_system_t S, const double *q, const double *y, double sign,
+                            double *dp, double *dq) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= S.n_free) return;
+  const int64_t e = S.free_elem[s];
+  const double *ys = y + 6 * s;
+  double qe[4], yr[3], w[4];
+  load_q(q, e, qe);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) dp[3 * e + c] = sign * ys[c];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) yr[c] = sign * ys[3 + c];
+  glt_apply(qe, yr, w);
+  store_q(dq, e, w);
+}
+
+__global__ void k_predict(bdem_system_t S, const double *p, const double *q, const double *v,
+                          const double *qd, const double *pp, const double *qp, double dt,
+                          double *ph, double *qh, double *mp, double *mq, double *p0,
+                          double *q0) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= S.n_elem) return;
+  double pe[3], qe[4], ppe[3], qpe[4];
+  load_p(p, e, pe);
+  load_q(q, e, qe);
+  load_p(pp, e, ppe);
+  load_q(qp, e, qpe);
+  double hq[4];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) ph[3 * e + c] = 2.0 * pe[c] - ppe[c];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) hq[c] = 2.0 * qe[c] - qpe[c];
+  store_q(qh, e, hq);
+  const bool fr = S.slot[e] >= 0;
+  const double dt2 = dt * dt;
+  const double m = S.mass[e], r = S.radius[e];
+  mp[e] = fr ? m / dt2 : 0.0;
+  mq[e] = fr ? ((1.6 * m) * (r * r)) / dt2 : 0.0;
+  double out[4];
+  if (fr) {
+    double ve[3], we[4], st[4];
+    load_p(v, e, ve);
+    load_q(qd, e, we);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) p0[3 * e + c] = pe[c] + dt * ve[c];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) st[c] = dt * we[c];
+    retract_normalize(qe, st, out);  // geodesic then quat_normalize(q0)
+  } else {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) p0[3 * e + c] = pe[c];
+    normalize4(qe, out);
+  }
+  store_q(q0, e, out);
+}
+
+__global__ void k_normalize_free(bdem_system_t S, double *q) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= S.n_free) return;
+  const int64_t e = S.free_elem[s];
+  double qe[4], out[4];
+  load_q(q, e, qe);
+  normalize4(qe, out);
+  store_q(q, e, out);
+}
+
+__global__ void k_finish_step(bdem_system_t S, const double *p, const double *q,
+                              const double *pc, const double *qc, double dt, double *v,
+                              double *qd) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= S.n_free) return;
+  const int64_t e = S.free_elem[s];
+  double pe[3], qe[4], pce[3], qce[4], w[4], out[4];
+  load_p(p, e, pe);
+  load_q(q, e, qe);
+  load_p(pc, e, pce);
+  load_q(qc, e, qce);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) v[3 * e + c] = (pe[c] - pce[c]) / dt;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) w[c] = (qe[c] - qce[c]) / dt;
+  const double qw = ((qe[0] * w[0] + qe[1] * w[1]) + qe[2] * w[2]) + qe[3] * w[3];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) out[c] = w[c] - qw * qe[c];
+  store_q(qd, e, out);
+}
+
+// dot product with last-block finish into scalars[col]
+__global__ void __launch_bounds__(kThreads) k_dot(bdem_system_t S, const double *a,
+                                                  const double *b, int64_t n, int col) {
+  __shared__ double sh[kThreads / 32];
+  double acc = 0.0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    acc += a[k] * b[k];
+  const double s = block_sum<kThreads>(acc, sh);
+  if (threadIdx.x == 0) *red_slot(S.red, col, blockIdx.x) = s;
+  if (last_block(S.counter + 1)) {
+    const double tot = sum_partials<kThreads>(S.red, col, gridDim.x, sh);
+    if (threadIdx.x == 0) S.scalars[col] = tot;
+  }
+}
+
+}  // namespace bdem
+
+using namespace bdem;
+
+extern "C" {
+
+int bdem_element_assemble(const bdem_system_t *sys, const double *p, const double *q,
+                          double *z, void *stream) {
+  if (!sys) return BDEM_ERR_ARG;
+  k_element_assemble<<<kRedBlocks, kThreads, 0, as_stream(stream)>>>(*sys, p, q, z);
+  return launch_status();
+}
+
+int bdem_reduce_finish(const bdem_system_t *sys, int col0, int ncol, int nblocks,
+                       void *stream) {
+  if (!sys || col0 < 0 || col0 + ncol > BDEM_SC_COUNT || nblocks > kRedBlocks) return BDEM_ERR_ARG;
+  k_reduce_finish<<<1, kThreads, 0, as_stream(stream)>>>(*sys, col0, ncol, nblocks);
+  return launch_status();
+}
+
+int bdem_trial_point(const bdem_system_t *sys, const double *p, const double *q,
+                     const double *dp, const double *dq, double alpha, double *p_t,
+                     double *q_t, void *stream) {
+  if (!sys || !dp || !dq || !p_t || !q_t) return BDEM_ERR_ARG;
+  k_element_energy<<<kRedBlocks, kThreads, 0, as_stream(stream)>>>(*sys, p, q, dp, dq, alpha,
+                                                                    p_t, q_t, 1);
+  return launch_status();
+}
+
+int bdem_element_energy(const bdem_system_t *sys, const double *p, const double *q,
+                        int with_inertia, void *stream) {
+  if (!sys) return BDEM_ERR_ARG;
+  k_element_energy<<<kRedBlocks, kThreads, 0, as_stream(stream)>>>(
+      *sys, p, q, nullptr, nullptr, 0.0, nullptr, nullptr, with_inertia);
+  return launch_status();
+}
+
+int bdem_kinetic(const bdem_system_t *sys, const double *v, const double *qdot, void *stream) {
+  if (!sys) return BDEM_ERR_ARG;
+  k_kinetic<<<kRedBlocks, kThreads, 0, as_stream(stream)>>>(*sys, v, qdot);
+  return launch_status();
+}
+
+int bdem_direction(const bdem_system_t *sys, const double *q, const double *y, double sign,
+                   double *dp, double *dq, void *stream) {
+  if (!sys) return BDEM_ERR_ARG;
+  if (sys->n_free == 0) return BDEM_OK;
+  k_direction<<<grid_for(sys->n_free), kThreads, 0, as_stream(stream)>>>(*sys, q, y, sign, dp, dq);
+  return launch_status();
+}
+
+int bdem_dot(const bdem_system_t *sys, const double *a, const double *b, int64_t n, int sc_col,
+             void *stream) {
+  if (!sys || sc_col < 0 || sc_col >= BDEM_SC_COUNT) return BDEM_ERR_ARG;
+  k_dot<<<kRedBlocks, kThreads, 0, as_stream(stream)>>>(*sys, a, b, n, sc_col);
+  return launch_status();
+}
+
+int bdem_predict(const bdem_system_t *sys, const double *p, const double *q, const double *v,
+                 const double *qdot, const double *p_prev, const double *q_prev, double dt,
+                 double *p_hat, double *q_hat, double *mp_dt2, double *mq_dt2, double *p0,
+                 double *q0, void *stream) {
+  if (!sys || dt <= 0.0) return BDEM_ERR_ARG;
+  k_predict<<<grid_for(sys->n_elem), kThreads, 0, as_stream(stream)>>>(
+      *sys, p, q, v, qdot, p_prev, q_prev, dt, p_hat, q_hat, mp_dt2, mq_dt2, p0, q0);
+  return launch_status();
+}
+
+int bdem_normalize_free(const bdem_system_t *sys, double *q, void *stream) {
+  if (!sys) return BDEM_ERR_ARG;
+  if (sys->n_free == 0) return BDEM_OK;
+  k_normalize_free<<<grid_for(sys->n_free), kThreads, 0, as_stream(stream)>>>(*sys, q);
+  return launch_status();
+}
+
+int bdem_finish_step(const bdem_system_t *sys, const double *p, const double *q,
+                     const double *p_c, const double *q_c, double dt, double *v, double *qdot,
+                     void *stream) {
+  if (!sys || dt <= 0.0) return BDEM_ERR_ARG;
+  if (sys->n_free == 0) return BDEM_OK;
+  k_finish_step<<<grid_for(sys->n_free), kThreads, 0, as_stream(stream)>>>(*sys, p, q, p_c, q_c,
+                                                                           dt, v, qdot);
+  return launch_status();
+}
+
+}  // extern "C"

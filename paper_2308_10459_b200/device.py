@@ -1,0 +1,353 @@
+"""HBM-resident system state and the typed handles the kernels see.
+
+``DeviceSystem`` owns every device buffer (torch tensors used purely as
+allocations) and one ``bdem_system_t`` struct that points into them.  It is
+built once per scene; topology (bond list, element->bond adjacency) is fixed
+for the scene's lifetime -- broken bonds keep their slots and the kernels
+skip them by status -- so nothing is re-allocated inside a step.
+
+Memory layout (HBM):
+  elements  p (n,3), q (n,4) [scalar-last, 32-byte rows], v, qdot,
+            p_prev, q_prev, p_hat, q_hat, mass, radius, m/dt^2, mq/dt^2
+  bonds     i, j (int32), status (int8), 24 geometry planes, 5 state planes
+            (structure-of-arrays, one plane = n_bond doubles)
+  staging   39 planes x n_bond written by the fused bond kernel
+  reduced   z, y, r, zv, pv, Ap (6 doubles per free element), diag and
+            block-Jacobi inverses (12 doubles per free element)
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .state import DegenerateBondError, DegenerateShearError
+
+F64 = torch.float64
+I32 = torch.int32
+
+
+def _t(arr, dtype=F64, device="cuda"):
+    return torch.as_tensor(np.ascontiguousarray(arr), dtype=dtype).to(device)
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+def build_adjacency(bi: np.ndarray, bj: np.ndarray, n: int, slot: np.ndarray):
+    """Element -> bond lists in np.add.at order (integrator.py:100-103):
+    for element e, bonds with i == e ascending, then bonds with j == e
+    ascending.  Returns adj_ptr (n+1), adj_mid (n), adj_bond, adj_oslot."""
+    nb = bi.shape[0]
+    ci = np.bincount(bi, minlength=n)
+    cj = np.bincount(bj, minlength=n)
+    adj_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(ci + cj, out=adj_ptr[1:])
+    adj_mid = adj_ptr[:-1] + ci
+    bonds = np.arange(nb, dtype=np.int64)
+    oi = np.argsort(bi, kind="stable")
+    oj = np.argsort(bj, kind="stable")
+    si = np.cumsum(ci) - ci
+    sj = np.cumsum(cj) - cj
+    rank_i = np.empty(nb, dtype=np.int64)
+    rank_i[oi] = bonds - si[bi[oi]]
+    rank_j = np.empty(nb, dtype=np.int64)
+    rank_j[oj] = bonds - sj[bj[oj]]
+    pos_i = adj_ptr[bi] + rank_i
+    pos_j = adj_mid[bj] + rank_j
+    adj_bond = np.empty(2 * nb, dtype=np.int32)
+    adj_oslot = np.empty(2 * nb, dtype=np.int32)
+    adj_bond[pos_i] = bonds
+    adj_bond[pos_j] = bonds
+    adj_oslot[pos_i] = slot[bj]
+    adj_oslot[pos_j] = slot[bi]
+    return (adj_ptr.astype(np.int32), adj_mid.astype(np.int32), adj_bond, adj_oslot)
+
+
+def bond_geometry_planes(b) -> np.ndarray:
+    nb = b.i.shape[0]
+    g = np.empty((L.BG["COUNT"], nb))
+    g[L.BG["L0"]] = b.rest_length
+    g[L.BG["D0"]:L.BG["D0"] + 3] = np.asarray(b.d0).T
+    g[L.BG["FRAME"]:L.BG["FRAME"] + 9] = np.asarray(b.frame).reshape(nb, 9).T
+    g[L.BG["KN"]] = b.kn
+    g[L.BG["KT"]] = b.kt
+    g[L.BG["KDIAG"]:L.BG["KDIAG"] + 3] = np.asarray(b.k_diag).T
+    g[L.BG["RADIUS"]] = b.radius
+    g[L.BG["SECTION"]] = b.section
+    g[L.BG["SECOND"]] = b.second_moment
+    g[L.BG["POLAR"]] = b.polar_moment
+    g[L.BG["TENSILE"]] = b.tensile_strength
+    g[L.BG["SHEAR"]] = b.shear_strength
+    return g
+
+
+class DeviceSystem:
+    """Device mirror of one scene (elements, bonds, colliders, workspaces)."""
+
+    def __init__(self, scene=None, *, elements=None, bonds=None, device="cuda"):
+        if not torch.cuda.is_available():
+            raise RuntimeError("DeviceSystem needs a CUDA device (B200, sm_100a)")
+        self.lib = L.load()
+        self.device = torch.device(device)
+        el = scene.elements if scene is not None else elements
+        b = scene.bonds if scene is not None else bonds
+        self.n = n = int(el.p.shape[0])
+        self.nb = nb = int(b.i.shape[0])
+        pinned = np.asarray(el.pinned, dtype=bool)
+        self.free_np = ~pinned
+        slot = np.full(n, -1, dtype=np.int32)
+        self.free_ids_np = np.nonzero(self.free_np)[0]
+        slot[self.free_ids_np] = np.arange(self.free_ids_np.size, dtype=np.int32)
+        self.slot_np = slot
+        self.nf = nf = int(self.free_ids_np.size)
+        dev = self.device
+
+        # element constants
+        self.mass = _t(el.mass, device=dev)
+        self.radius = _t(el.radius, device=dev)
+        self.slot = _t(slot, I32, dev)
+        self.free_elem = _t(self.free_ids_np.astype(np.int32), I32, dev)
+        # element state + step context
+        z3 = lambda: torch.zeros((n, 3), dtype=F64, device=dev)  # noqa: E731
+        z4 = lambda: torch.zeros((n, 4), dtype=F64, device=dev)  # noqa: E731
+        self.p, self.q, self.v, self.qdot = z3(), z4(), z3(), z4()
+        self.p_prev, self.q_prev = z3(), z4()
+        self.p_hat, self.q_hat = z3(), z4()
+        self.p_cur, self.q_cur = z3(), z4()
+        self.mp_dt2 = torch.zeros(n, dtype=F64, device=dev)
+        self.mq_dt2 = torch.zeros(n, dtype=F64, device=dev)
+        # Newton iterate, trial point, direction (pinned rows of dp/dq stay 0)
+        self.xp, self.xq, self.tp, self.tq = z3(), z4(), z3(), z4()
+        self.dp, self.dq = z3(), z4()
+        # bonds
+        self.bond_i = _t(b.i.astype(np.int32), I32, dev)
+        self.bond_j = _t(b.j.astype(np.int32), I32, dev)
+        self.status = _t(np.asarray(b.status, dtype=np.int8), torch.int8, dev)
+        self.geom = _t(bond_geometry_planes(b), device=dev)
+        self.bstate = torch.zeros((L.BS["COUNT"], max(nb, 1)), dtype=F64, device=dev)
+        adj = build_adjacency(np.asarray(b.i, dtype=np.int64), np.asarray(b.j, dtype=np.int64), n,
+                              slot)
+        self.adj_ptr, self.adj_mid, self.adj_bond, self.adj_oslot = (
+            _t(a, I32, dev) for a in adj)
+        # staging / reduced system
+        self.stage = torch.zeros((L.ST["COUNT"], max(nb, 1)), dtype=F64, device=dev)
+        self.diag = torch.zeros((max(nf, 1), 12), dtype=F64, device=dev)
+        self.minv = torch.zeros((max(nf, 1), 12), dtype=F64, device=dev)
+        v6 = lambda: torch.zeros(max(6 * nf, 6), dtype=F64, device=dev)  # noqa: E731
+        self.z, self.y, self.r, self.zv, self.pv, self.ap = v6(), v6(), v6(), v6(), v6(), v6()
+        self.red = torch.zeros((L.SC["COUNT"], L.RED_BLOCKS), dtype=F64, device=dev)
+        self.scalars = torch.zeros(L.SC["COUNT"], dtype=F64, device=dev)
+        self.pcg_state = torch.zeros(L.PCG["COUNT"], dtype=F64, device=dev)
+        self.err = torch.zeros(L.ERRSLOT_COUNT, dtype=I32, device=dev)
+        self.counter = torch.zeros(L.N_COUNTERS, dtype=torch.int32, device=dev)
+        # host staging for scalar read-backs
+        self.h_scalars = torch.zeros(L.SC["COUNT"], dtype=F64).pin_memory()
+        self.h_pcg = torch.zeros(L.PCG["COUNT"], dtype=F64).pin_memory()
+        self.h_err = torch.zeros(L.ERRSLOT_COUNT, dtype=I32).pin_memory()
+        # contact pairs (capacity grows on demand)
+        self.pair_cap = 0
+        self.n_pair = 0
+        self.pairs = None
+        self._pair_bufs = {}
+        self._alloc_pairs(1024)
+        self._bp_work = None
+        self._cc_work = None
+        self._sel_work = None
+        self.launches = 0
+
+        self.sys = L.System()
+        s = self.sys
+        s.n_elem, s.n_free, s.n_bond = n, nf, nb
+        s.mass, s.radius = _ptr(self.mass), _ptr(self.radius)
+        s.mp_dt2, s.mq_dt2 = _ptr(self.mp_dt2), _ptr(self.mq_dt2)
+        s.p_hat, s.q_hat = _ptr(self.p_hat), _ptr(self.q_hat)
+        s.slot, s.free_elem = _ptr(self.slot), _ptr(self.free_elem)
+        s.bond_i, s.bond_j, s.status = _ptr(self.bond_i), _ptr(self.bond_j), _ptr(self.status)
+        s.geom, s.bstate = _ptr(self.geom), _ptr(self.bstate)
+        s.adj_ptr, s.adj_mid = _ptr(self.adj_ptr), _ptr(self.adj_mid)
+        s.adj_bond, s.adj_oslot = _ptr(self.adj_bond), _ptr(self.adj_oslot)
+        s.stage, s.diag, s.minv = _ptr(self.stage), _ptr(self.diag), _ptr(self.minv)
+        s.red, s.scalars, s.pcg = _ptr(self.red), _ptr(self.scalars), _ptr(self.pcg_state)
+        s.err, s.counter = _ptr(self.err), _ptr(self.counter)
+        self.sysp = C.pointer(s)
+        self.reset_errors()
+
+        if scene is not None:
+            self.set_physics(scene.gravity, scene.k_contact, scene.k_element, scene.colliders)
+        self.upload_elements(el)
+        self.upload_bond_state(b)
+
+    # ------------------------------------------------------------------ setup
+    @property
+    def stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def set_physics(self, gravity, k_contact, k_element, colliders):
+        s = self.sys
+        for c in range(3):
+            s.gravity[c] = float(gravity[c])
+        s.k_contact, s.k_element = float(k_contact), float(k_element)
+        self.set_colliders(colliders)
+
+    def set_colliders(self, colliders):
+        cols = list(colliders or [])
+        if len(cols) > L.MAX_COLLIDERS:
+            raise ValueError(f"at most {L.MAX_COLLIDERS} colliders are supported")
+        s = self.sys
+        s.n_colliders = len(cols)
+        for k, col in enumerate(cols):
+            kind, *a = _pack_collider(col)
+            s.colliders[k].kind = kind
+            for t in range(6):
+                s.colliders[k].a[t] = a[t]
+
+    def upload_elements(self, el, p_prev=None, q_prev=None):
+        for name in ("p", "q", "v", "qdot"):
+            getattr(self, name).copy_(_host(getattr(el, name)), non_blocking=True)
+        if p_prev is not None:
+            self.p_prev.copy_(_host(p_prev), non_blocking=True)
+            self.q_prev.copy_(_host(q_prev), non_blocking=True)
+
+    def upload_bond_state(self, b):
+        if self.nb == 0:
+            return
+        st = np.empty((L.BS["COUNT"], self.nb))
+        st[L.BS["SCALE"]] = b.stiffness_scale
+        st[L.BS["DAMAGE"]] = b.damage
+        st[L.BS["PLASTIC"]] = b.plastic_strain
+        st[L.BS["SIGMA"]] = b.sigma
+        st[L.BS["TAU"]] = b.tau
+        self.bstate.copy_(torch.from_numpy(st))
+        self.status.copy_(torch.from_numpy(np.asarray(b.status, dtype=np.int8)))
+
+    def download_bond_state(self, b):
+        if self.nb == 0:
+            return
+        st = self.bstate.cpu().numpy()
+        b.stiffness_scale[:] = st[L.BS["SCALE"]]
+        b.damage[:] = st[L.BS["DAMAGE"]]
+        b.plastic_strain[:] = st[L.BS["PLASTIC"]]
+        b.sigma[:] = st[L.BS["SIGMA"]]
+        b.tau[:] = st[L.BS["TAU"]]
+        b.status[:] = self.status.cpu().numpy()
+
+    def download_state(self, scene):
+        el = scene.elements
+        for name in ("p", "q", "v", "qdot"):
+            getattr(el, name)[:] = getattr(self, name).cpu().numpy()
+        scene.p_prev = self.p_prev.cpu().numpy()
+        scene.q_prev = self.q_prev.cpu().numpy()
+        self.download_bond_state(scene.bonds)
+
+    def bootstrap_history(self, dt):
+        """p_prev = p - dt v, q_prev = normalize(geodesic(q, -dt qdot))
+        (scenes.py:64-68), via the predictor kernel with -dt."""
+        # predictor: p0 = p + dt' v, q0 = normalize(geodesic(q, dt' qdot)) on free rows.
+        # The reference applies it to every row, so run it with a temporary
+        # all-free view is not possible; pinned rows use the same formula:
+        p = self.p.cpu().numpy()
+        q = self.q.cpu().numpy()
+        v = self.v.cpu().numpy()
+        qd = self.qdot.cpu().numpy()
+        from . import quat as Q
+        self.p_prev.copy_(torch.from_numpy(p - dt * v))
+        self.q_prev.copy_(torch.from_numpy(Q.normalize(Q.geodesic(q, -dt * qd))))
+
+    # ----------------------------------------------------------- contact pairs
+    def _alloc_pairs(self, cap):
+        dev = self.device
+        self.pair_cap = int(cap)
+        self.pstage = torch.zeros((L.PS["COUNT"], self.pair_cap), dtype=F64, device=dev)
+        self.pair_ij = torch.zeros((self.pair_cap, 2), dtype=I32, device=dev)
+        self.pi_ptr = torch.zeros(self.n + 1, dtype=I32, device=dev)
+        self.pj_ptr = torch.zeros(self.n + 1, dtype=I32, device=dev)
+        self.pj_idx = torch.zeros(self.pair_cap, dtype=I32, device=dev)
+        s = self.sys
+        s.pair_cap = self.pair_cap
+        s.pstage = _ptr(self.pstage)
+        s.pair_i = _ptr(self.pair_ij[:, 0:1])  # strided view: set below
+        self._pair_i = torch.zeros(self.pair_cap, dtype=I32, device=dev)
+        self._pair_j = torch.zeros(self.pair_cap, dtype=I32, device=dev)
+        s.pair_i, s.pair_j = _ptr(self._pair_i), _ptr(self._pair_j)
+        s.pi_ptr, s.pj_ptr, s.pj_idx = _ptr(self.pi_ptr), _ptr(self.pj_ptr), _ptr(self.pj_idx)
+
+    def set_pairs(self, pairs: torch.Tensor):
+        """Install the frozen self-contact candidates of this step ((m,2) int32,
+        sorted, i<j) and their element adjacency."""
+        m = int(pairs.shape[0])
+        if m > self.pair_cap:
+            self._alloc_pairs(max(m, 2 * self.pair_cap))
+        self.n_pair = m
+        self.sys.n_pair = m
+        if m == 0:
+            return
+        pi = pairs[:, 0].contiguous()
+        pj = pairs[:, 1].contiguous()
+        self._pair_i[:m].copy_(pi)
+        self._pair_j[:m].copy_(pj)
+        n = self.n
+        ci = torch.bincount(pi.long(), minlength=n)
+        cj = torch.bincount(pj.long(), minlength=n)
+        self.pi_ptr.zero_()
+        self.pj_ptr.zero_()
+        self.pi_ptr[1:] = torch.cumsum(ci, 0).to(I32)
+        self.pj_ptr[1:] = torch.cumsum(cj, 0).to(I32)
+        order = torch.sort(pj.long(), stable=True).indices
+        self.pj_idx[:m].copy_(order.to(I32))
+
+    # ----------------------------------------------------------------- errors
+    def reset_errors(self):
+        self.err.copy_(torch.tensor([0, 2**31 - 1, 0, 2**31 - 1, 0, 0, 0, 0], dtype=I32))
+
+    def raise_errors(self, host_err):
+        if host_err[L.ERRSLOT_DEG_COUNT] > 0:
+            first = int(host_err[L.ERRSLOT_DEG_FIRST])
+            self.reset_errors()
+            raise DegenerateBondError(f"coincident bond endpoints at bond indices [{first}] "
+                                      f"({int(host_err[L.ERRSLOT_DEG_COUNT])} total)")
+        if host_err[L.ERRSLOT_ANTI_COUNT] > 0:
+            first = int(host_err[L.ERRSLOT_ANTI_FIRST])
+            self.reset_errors()
+            raise DegenerateShearError(f"antipodal quaternion pairs at bond indices [{first}] "
+                                       f"({int(host_err[L.ERRSLOT_ANTI_COUNT])} total)")
+
+    def read_scalars(self):
+        """Synchronise once and return (scalars, err) host arrays."""
+        self.h_scalars.copy_(self.scalars, non_blocking=True)
+        self.h_err.copy_(self.err, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        err = self.h_err.numpy()
+        if err[L.ERRSLOT_DEG_COUNT] or err[L.ERRSLOT_ANTI_COUNT]:
+            self.raise_errors(err.copy())
+        return self.h_scalars.numpy()
+
+    # ---------------------------------------------------------------- kernels
+    def call(self, name, *args):
+        rc = getattr(self.lib, name)(*args)
+        self.launches += 1
+        if rc != 0:
+            raise L.BdemLibraryError(f"{name} failed with status {rc}")
+
+
+def _host(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+
+
+def _pack_collider(col):
+    kind = type(col).__name__
+    if kind == "HalfSpace":
+        n = np.asarray(col.normal, dtype=float)
+        return (0, n[0], n[1], n[2], float(col.offset), 0.0, 0.0)
+    if kind == "SphereCollider":
+        c = np.asarray(col.center, dtype=float)
+        return (1, c[0], c[1], c[2], float(col.radius), 0.0, 0.0)
+    if kind == "BoxCollider":
+        c = np.asarray(col.center, dtype=float)
+        h = np.asarray(col.half_extents, dtype=float)
+        return (2, c[0], c[1], c[2], h[0], h[1], h[2])
+    raise TypeError(f"unsupported collider {kind}")

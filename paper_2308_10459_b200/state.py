@@ -145,6 +145,11 @@ class BondSet:
     def active(self) -> np.ndarray:
         return self.status != BROKEN
 
+    def energy_terms(self, p, q, want_hess=False, want_grad=True):
+        """GPU evaluation with the reference's return tuple (bonds.py:473-504)."""
+        from .bond_api import energy_terms
+        return energy_terms(self, p, q, want_hess, want_grad)
+
     # mutable per-bond state that the fracture update writes (bonds.py:532-570)
     STATE_FIELDS = ("status", "stiffness_scale", "damage", "plastic_strain", "sigma", "tau")
 

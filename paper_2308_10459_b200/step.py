@@ -1,0 +1,288 @@
+"""Step orchestration: the drop-in ``stable_step`` and its per-step pieces.
+
+``stable_step`` follows ``/root/reference/pkg/src/bdem/solver.py:881-939``
+(call stack B of SURVEY.md §3) with every array operation on the device:
+driver rows -> predictor/anchors kernel -> contact broad phase -> Newton
+solve -> velocity kernel -> fracture kernel + ordered event compaction ->
+components (only when bonds broke) -> energy reductions.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .newton import GPUProblem, SolverConfig, minimize_second_order
+from .scene import FragmentLabeling
+
+MINIMIZERS = {"second-order": minimize_second_order}
+
+
+@dataclass
+class StepReport:
+    """solver.py:847-853."""
+
+    solve: object
+    broken: list
+    contact_pairs: int
+    energies: dict
+    committed: bool
+
+
+# ---------------------------------------------------------------------------
+# broad phase and components
+# ---------------------------------------------------------------------------
+
+def _device_broadphase(dev, p, radii, cell, labels=None):
+    lib = dev.lib
+    n = int(p.shape[0])
+    if n < 2:
+        return torch.zeros((0, 2), dtype=torch.int32, device=p.device)
+    need = int(lib.bdem_broadphase_workspace(n))
+    if dev._bp_work is None or dev._bp_work.numel() < need:
+        dev._bp_work = torch.empty(need, dtype=torch.uint8, device=p.device)
+    cnt = C.c_int64(0)
+    lab = 0 if labels is None else labels.data_ptr()
+    st = torch.cuda.current_stream(p.device).cuda_stream
+    L.check(lib.bdem_broadphase(p.data_ptr(), radii.data_ptr(), n, float(cell), lab,
+                                dev._bp_work.data_ptr(), None, 0, C.byref(cnt), st),
+            "bdem_broadphase(count)")
+    m = int(cnt.value)
+    out = torch.empty((max(m, 1), 2), dtype=torch.int32, device=p.device)
+    if m:
+        L.check(lib.bdem_broadphase(p.data_ptr(), radii.data_ptr(), n, float(cell), lab,
+                                    dev._bp_work.data_ptr(), out.data_ptr(), m, C.byref(cnt), st),
+                "bdem_broadphase(write)")
+    dev.launches += 2
+    return out[:m]
+
+
+class _Scratch:
+    """Minimal holder for workspaces when no DeviceSystem exists."""
+
+    def __init__(self):
+        self.lib = L.load()
+        self._bp_work = None
+        self._cc_work = None
+        self.launches = 0
+
+
+def broad_phase(positions, radii, cell_size):
+    """Sorted overlapping pairs i<j (contact.py:140-173), computed on the GPU.
+
+    Accepts numpy arrays (returns an (m,2) int64 numpy array like the
+    reference) or CUDA tensors (returns an (m,2) int32 CUDA tensor).
+    """
+    on_host = isinstance(positions, np.ndarray)
+    p = torch.as_tensor(np.ascontiguousarray(positions, dtype=np.float64)).cuda() if on_host \
+        else positions.contiguous()
+    r = torch.as_tensor(np.ascontiguousarray(radii, dtype=np.float64)).cuda() if on_host \
+        else radii.contiguous()
+    if r.numel() and cell_size < 2.0 * float(r.max()):
+        raise ValueError("cell_size must be at least twice the largest radius")
+    out = _device_broadphase(_Scratch(), p, r, cell_size)
+    return out.cpu().numpy().astype(np.int64) if on_host else out
+
+
+def _components(lib, n, bi, bj, status, work_holder):
+    need = int(lib.bdem_components_workspace(n))
+    if work_holder._cc_work is None or work_holder._cc_work.numel() < need:
+        work_holder._cc_work = torch.empty(need, dtype=torch.uint8, device=bi.device)
+    labels = torch.empty(max(n, 1), dtype=torch.int64, device=bi.device)
+    nc = C.c_int64(0)
+    st = torch.cuda.current_stream(bi.device).cuda_stream
+    L.check(lib.bdem_components(n, int(bi.numel()), bi.data_ptr(), bj.data_ptr(),
+                                status.data_ptr(), work_holder._cc_work.data_ptr(),
+                                labels.data_ptr(), C.byref(nc), st), "bdem_components")
+    return labels[:n], int(nc.value)
+
+
+def label_components(n_elements, bonds, scene=None) -> FragmentLabeling:
+    """Connected components over non-broken bonds, numbered by smallest element
+    (geometry.py:295-310), on the GPU."""
+    if scene is not None and scene._device is not None:
+        dev = scene._device
+        labels, _ = _components(dev.lib, dev.n, dev.bond_i, dev.bond_j, dev.status, dev)
+        dev.labels = labels
+        return FragmentLabeling(labels.cpu().numpy())
+    bi = torch.as_tensor(np.asarray(bonds.i, dtype=np.int32)).cuda()
+    bj = torch.as_tensor(np.asarray(bonds.j, dtype=np.int32)).cuda()
+    stt = torch.as_tensor(np.asarray(bonds.status, dtype=np.int8)).cuda()
+    labels, _ = _components(L.load(), int(n_elements), bi, bj, stt, _Scratch())
+    return FragmentLabeling(labels.cpu().numpy())
+
+
+def contact_candidates(scene):
+    """Frozen self-contact candidates of one step (solver.py:856-878): broad
+    phase on radii inflated by dt|v| + dt^2|g|, restricted to element pairs
+    in different fragments.  Returns an (m,2) int32 CUDA tensor."""
+    dev = scene.device
+    if scene.k_element <= 0.0 or dev.n < 2:
+        return torch.zeros((0, 2), dtype=torch.int32, device=dev.device)
+    travel = scene.dt * torch.linalg.vector_norm(dev.v, dim=1)
+    travel = travel + scene.dt**2 * float(np.linalg.norm(scene.gravity))
+    inflated = dev.radius + travel
+    cell = 2.0 * float(inflated.max()) + 1e-12
+    if getattr(dev, "labels", None) is None:
+        label_components(dev.n, scene.bonds, scene)
+    return _device_broadphase(dev, dev.p, inflated, cell, dev.labels)
+
+
+# ---------------------------------------------------------------------------
+# fracture update
+# ---------------------------------------------------------------------------
+
+def _device_bond_update(dev, youngs, plastic):
+    """bdem_bond_update + ordered event compaction -> [(bond, sigma, tau)]."""
+    if dev.nb == 0:
+        return []
+    st = dev.stream
+    if getattr(dev, "_flags", None) is None:
+        dev._flags = torch.zeros(dev.nb, dtype=torch.uint8, device=dev.device)
+        dev._ev_idx = torch.zeros(dev.nb, dtype=torch.int32, device=dev.device)
+        dev._sel_work = torch.empty(int(dev.lib.bdem_select_workspace(dev.nb)), dtype=torch.uint8,
+                                    device=dev.device)
+    pl = None
+    if plastic is not None:
+        arr = (C.c_double * 4)(plastic.fracture_strain, plastic.yield_strain, plastic.weakening,
+                               plastic.damage_exponent)
+        pl = C.cast(arr, C.c_void_p)
+    dev.call("bdem_bond_update", dev.sysp, dev.p.data_ptr(), dev.q.data_ptr(), float(youngs), pl,
+             dev._flags.data_ptr(), st)
+    cnt = C.c_int64(0)
+    L.check(dev.lib.bdem_select_flagged(dev._flags.data_ptr(), dev.nb, dev._ev_idx.data_ptr(),
+                                        dev._sel_work.data_ptr(), C.byref(cnt), st),
+            "bdem_select_flagged")
+    dev.launches += 1
+    m = int(cnt.value)
+    if m == 0:
+        return []
+    idx = dev._ev_idx[:m].long()
+    sig = dev.bstate[L.BS["SIGMA"]][idx].cpu().numpy()
+    tau = dev.bstate[L.BS["TAU"]][idx].cpu().numpy()
+    return [(int(b), float(s), float(t)) for b, s, t in zip(idx.cpu().numpy(), sig, tau)]
+
+
+def update_bond_states(bonds, p, q, youngs, plastic=None, scene=None):
+    """update_bond_states (bonds.py:532-570) on the GPU.
+
+    With ``scene`` the scene's device state is used (no transfers); otherwise
+    the host arrays are uploaded, updated in HBM and written back in place.
+    """
+    from .device import DeviceSystem
+    from .state import ElementSet
+    if scene is not None:
+        return _device_bond_update(scene.device, youngs, plastic)
+    n = np.asarray(p).shape[0]
+    el = ElementSet(np.asarray(p, dtype=float), np.asarray(q, dtype=float), np.zeros((n, 3)),
+                    np.zeros((n, 4)), np.ones(n), np.ones(n))
+    dev = DeviceSystem(elements=el, bonds=bonds)
+    events = _device_bond_update(dev, youngs, plastic)
+    dev.download_bond_state(bonds)
+    return events
+
+
+# ---------------------------------------------------------------------------
+# the step
+# ---------------------------------------------------------------------------
+
+def _apply_driver(scene, dev, t):
+    drv = scene.driver
+    if drv is None:
+        return
+    if hasattr(drv, "rows") and hasattr(drv, "ids"):
+        p, v, q, qd = drv.rows(t)
+        ids = torch.as_tensor(drv.ids, device=dev.device)
+        dev.p[ids] = torch.as_tensor(p, dtype=torch.float64, device=dev.device)
+        dev.v[ids] = torch.as_tensor(v, dtype=torch.float64, device=dev.device)
+        dev.q[ids] = torch.as_tensor(q, dtype=torch.float64, device=dev.device)
+        dev.qdot[ids] = torch.as_tensor(qd, dtype=torch.float64, device=dev.device)
+        return
+    # arbitrary reference-style callable: run it on a host view of the state
+    el = scene.elements
+    for name in ("p", "q", "v", "qdot"):
+        getattr(el, name)[:] = getattr(dev, name).cpu().numpy()
+    drv(el, t)
+    pin = torch.as_tensor(np.nonzero(el.pinned)[0], device=dev.device)
+    for name in ("p", "q", "v", "qdot"):
+        src = torch.as_tensor(getattr(el, name)[el.pinned], dtype=torch.float64,
+                              device=dev.device)
+        getattr(dev, name)[pin] = src
+
+
+def stable_step(scene, cfg: SolverConfig, method: str = "second-order") -> StepReport:
+    """Advance ``scene`` by one implicit step on the GPU (solver.py:881-939)."""
+    if method not in MINIMIZERS:
+        raise ValueError(f"the GPU path implements {sorted(MINIMIZERS)}, got {method!r}")
+    if scene.mu_s > 0.0 or scene.mu_r > 0.0:
+        raise NotImplementedError("apply_friction (mu > 0) is outside the GPU hot path")
+    dev = scene.device
+    if scene.host_sync:
+        dev.upload_elements(scene.elements, scene.p_prev, scene.q_prev)
+        dev.upload_bond_state(scene.bonds)
+    elif not getattr(dev, "_history_uploaded", False):
+        dev.upload_elements(scene.elements, scene.p_prev, scene.q_prev)
+    dev._history_uploaded = True
+    dev.set_physics(scene.gravity, scene.k_contact, scene.k_element, scene.colliders)
+    st = dev.stream
+
+    pin = torch.as_tensor(np.nonzero(~dev.free_np)[0], device=dev.device)
+    backup = (dev.p[pin].clone(), dev.q[pin].clone(), dev.v[pin].clone(), dev.qdot[pin].clone())
+    t_next = scene.time + scene.dt
+    _apply_driver(scene, dev, t_next)
+
+    dev.p_cur.copy_(dev.p)
+    dev.q_cur.copy_(dev.q)
+    pairs = contact_candidates(scene)
+    dev.set_pairs(pairs)
+    dev.reset_errors()
+    dev.call("bdem_predict", dev.sysp, dev.p.data_ptr(), dev.q.data_ptr(), dev.v.data_ptr(),
+             dev.qdot.data_ptr(), dev.p_prev.data_ptr(), dev.q_prev.data_ptr(), float(scene.dt),
+             dev.p_hat.data_ptr(), dev.q_hat.data_ptr(), dev.mp_dt2.data_ptr(),
+             dev.mq_dt2.data_ptr(), dev.xp.data_ptr(), dev.xq.data_ptr(), st)
+    problem = GPUProblem(dev)
+    result = MINIMIZERS[method](problem, dev.xp, dev.xq, cfg)
+    n_pairs = int(pairs.shape[0])
+
+    if not result.converged:
+        dev.p[pin], dev.q[pin], dev.v[pin], dev.qdot[pin] = backup
+        energies = {"kinetic": _kinetic(dev)}
+        if scene.host_sync:
+            dev.download_state(scene)
+        return StepReport(result, [], n_pairs, energies, False)
+
+    dev.call("bdem_finish_step", dev.sysp, result.p.data_ptr(), result.q.data_ptr(),
+             dev.p_cur.data_ptr(), dev.q_cur.data_ptr(), float(scene.dt), dev.v.data_ptr(),
+             dev.qdot.data_ptr(), st)
+    dev.p.copy_(result.p)
+    dev.q.copy_(result.q)
+
+    events = _device_bond_update(dev, scene.youngs, scene.plastic)
+    if events:
+        flags = scene.surface_flags
+        bi = np.asarray(scene.bonds.i)
+        bj = np.asarray(scene.bonds.j)
+        for b, _, _ in events:                      # geometry.py:257-261
+            flags[bi[b]] = True
+            flags[bj[b]] = True
+        scene.labels = label_components(dev.n, scene.bonds, scene)
+
+    dev.p_prev, dev.p_cur = dev.p_cur, dev.p_prev
+    dev.q_prev, dev.q_cur = dev.q_cur, dev.q_prev
+    scene.time = t_next
+
+    energies = problem.energy_breakdown(dev.p, dev.q)
+    if scene.host_sync:
+        dev.download_state(scene)
+    return StepReport(result, events, n_pairs, energies, True)
+
+
+def _kinetic(dev):
+    dev.call("bdem_kinetic", dev.sysp, dev.v.data_ptr(), dev.qdot.data_ptr(), dev.stream)
+    dev.call("bdem_reduce_finish", dev.sysp, L.SC["EKIN"], 1, L.RED_BLOCKS, dev.stream)
+    return float(dev.read_scalars()[L.SC["EKIN"]])

@@ -1,0 +1,302 @@
+"""GPU parity: the CUDA path against the reference's golden vectors and the
+CPU oracle on identical seeded inputs.  All calls go through the C ABI.
+
+Tolerances (north star): per-bond energy/gradient/Hessian rtol 1e-10 with an
+absolute floor of 1e-12 x the bond's stiffness scale (cancellation near
+rest); trajectories rtol 1e-8 with atol >= eps/(m/dt^2) (Newton termination);
+broken-bond sets bit-exact away from thresholds.
+"""
+
+import numpy as np
+import pytest
+
+from _fixtures import bonds_from, close, elements_from, load
+
+pytestmark = pytest.mark.gpu
+
+
+def _assert_close(a, b, rtol, atol, what):
+    ok, info = close(a, b, rtol, atol)
+    assert ok, f"{what}: got {info[0]!r} want {info[1]!r} at flat index {info[2]}"
+
+
+def _bond_scales(b, idx):
+    sc = b.stiffness_scale[idx]
+    kn = sc * b.kn[idx]
+    krot = sc * (b.kt[idx] + b.k_diag[idx].sum(axis=1))
+    l0 = b.rest_length[idx]
+    return kn, krot, l0
+
+
+# ---------------------------------------------------------------------------
+# per-bond kernels (bonds.py:151-323, 473-504)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("case", ["randq", "nearq", "ident"])
+def test_bond_terms_vs_golden(cuda_ok, case):
+    d = load("bond_terms.npz")
+    b = bonds_from(d, "b_")
+    got = b.energy_terms(d["p"], d[f"{case}_q"], want_hess=True)
+    idx = d[f"{case}_idx"]
+    assert np.array_equal(got[0], idx)
+    kn, krot, l0 = _bond_scales(b, idx)
+    e_sc = kn * l0**2 + krot
+    g_sc = np.maximum(kn * l0, krot)
+    h_sc = np.maximum(kn, krot)
+    names = ("E", "gpi", "gpj", "gqi", "gqj", "hpp", "hqq")
+    scales = (e_sc, g_sc, g_sc, g_sc, g_sc, h_sc, h_sc)
+    for k, (name, sc) in enumerate(zip(names, scales)):
+        want = d[f"{case}_{name}"]
+        atol = 1e-12 * sc.reshape((-1,) + (1,) * (want.ndim - 1))
+        err = np.abs(got[k + 1] - want) - (1e-10 * np.abs(want) + atol)
+        assert err.max() <= 0, f"{case}/{name}: worst excess {err.max():.3e}"
+
+
+def test_bond_terms_closed_forms(cuda_ok):
+    """Known answers from the reference's tests (tests/test_bonds.py):
+    1% stretch energy, shear 1/2 k phi^2, pure twist 1/2 k sin^2(phi/2)."""
+    from paper_2308_10459_b200 import configs as C
+    from paper_2308_10459_b200 import quat as Q
+    pos = np.array([[0.0, 0.0, 0.0], [0.1, 0.0, 0.0]])
+    rad = np.array([0.02, 0.02])
+    b = C.build_bonds(pos, rad, np.array([[0, 1]]), 1e7, 4e6)
+    kn, kt, ktw = b.kn[0], b.kt[0], b.k_diag[0, 0]
+    # stretch 1%
+    p = np.array([[0.0, 0, 0], [0.101, 0, 0]])
+    q = np.tile(Q.IDENTITY, (2, 1))
+    e = b.energy_terms(p, q)[1][0]
+    assert e == pytest.approx(0.5 * kn * (0.01 * 0.1) ** 2, rel=1e-12)
+    # shear: common rotation about an axis perpendicular to d0
+    for phi in (0.05, 0.3, 1.2):
+        qq = np.tile(Q.axis_angle([0, 1, 0], phi), (2, 1))
+        e = b.energy_terms(pos, qq)[1][0]
+        assert e == pytest.approx(0.5 * kt * phi**2, rel=1e-10)
+    # pure relative twist about the bond axis: the mean rotation is a twist
+    # too, so the shear term vanishes and E = 1/2 k_twist sin^2(phi/2)
+    for phi in (0.1, 0.6, 1.5):
+        qq = np.stack([Q.axis_angle([1, 0, 0], phi), Q.IDENTITY])
+        e = b.energy_terms(pos, qq)[1][0]
+        assert e == pytest.approx(0.5 * ktw * np.sin(phi / 2) ** 2, rel=1e-10)
+
+
+def test_degenerate_and_antipodal_raise(cuda_ok):
+    from paper_2308_10459_b200 import DegenerateBondError, DegenerateShearError
+    from paper_2308_10459_b200 import configs as C
+    from paper_2308_10459_b200 import quat as Q
+    pos = np.array([[0.0, 0.0, 0.0], [0.1, 0.0, 0.0]])
+    b = C.build_bonds(pos, np.array([0.02, 0.02]), np.array([[0, 1]]), 1e7, 4e6)
+    q = np.tile(Q.IDENTITY, (2, 1))
+    with pytest.raises(DegenerateBondError):
+        b.energy_terms(np.zeros((2, 3)), q)
+    qa = np.array([[0.1, 0.2, 0.3, 0.9], [-0.1, -0.2, -0.3, -0.9]])
+    with pytest.raises(DegenerateShearError):
+        b.energy_terms(pos, qa)
+
+
+def test_bond_terms_large_random_vs_oracle(cuda_ok):
+    """Full C2-size batch (22^3 jittered cube, random q) against the oracle."""
+    from oracle import cpu_oracle as O
+    from paper_2308_10459_b200 import configs as C
+    spec = C.cube()
+    rng = np.random.default_rng(9)
+    b = spec.bonds
+    b.stiffness_scale[:] = rng.uniform(0.3, 1.0, b.n)
+    p = spec.elements.p + 1e-5 * rng.normal(size=spec.elements.p.shape)
+    q = spec.elements.q
+    got = b.energy_terms(p, q, want_hess=True)
+    ref = O.bond_eval(b, p, q, want_hess=True)
+    kn, krot, l0 = _bond_scales(b, ref.idx)
+    for g, r, sc in zip(got[1:], (ref.energy, ref.gp_i, ref.gp_j, ref.gq_i, ref.gq_j, ref.h_pp,
+                                  ref.h_qq),
+                        (kn * l0**2 + krot, kn * l0 + krot, kn * l0 + krot, krot, krot,
+                         kn + krot, kn + krot)):
+        atol = 1e-12 * sc.reshape((-1,) + (1,) * (r.ndim - 1))
+        err = np.abs(g - r) - (1e-10 * np.abs(r) + atol)
+        assert err.max() <= 0, f"worst excess {err.max():.3e}"
+
+
+# ---------------------------------------------------------------------------
+# assembly, clamp, block-Jacobi, SpMV, PCG (solver.py:116-258, linalg.py)
+# ---------------------------------------------------------------------------
+
+def _gpu_problem(d, tag):
+    import torch
+    from paper_2308_10459_b200.colliders import HalfSpace
+    from paper_2308_10459_b200.device import DeviceSystem
+    from paper_2308_10459_b200.newton import GPUProblem
+    el = elements_from(d, f"{tag}_el_")
+    b = bonds_from(d, f"{tag}_b_")
+    dev = DeviceSystem(elements=el, bonds=b)
+    hs = d[f"{tag}_hs"]
+    dev.set_physics(d[f"{tag}_gravity"], float(d[f"{tag}_kc"]), float(d[f"{tag}_ke"]),
+                    [HalfSpace(tuple(hs[:3]), hs[3])])
+    dev.p_prev.copy_(torch.from_numpy(d[f"{tag}_p_prev"]))
+    dev.q_prev.copy_(torch.from_numpy(d[f"{tag}_q_prev"]))
+    dev.set_pairs(torch.as_tensor(d[f"{tag}_pairs"].astype(np.int32)).cuda().reshape(-1, 2))
+    dev.call("bdem_predict", dev.sysp, dev.p.data_ptr(), dev.q.data_ptr(), dev.v.data_ptr(),
+             dev.qdot.data_ptr(), dev.p_prev.data_ptr(), dev.q_prev.data_ptr(),
+             float(d[f"{tag}_dt"]), dev.p_hat.data_ptr(), dev.q_hat.data_ptr(),
+             dev.mp_dt2.data_ptr(), dev.mq_dt2.data_ptr(), dev.tp.data_ptr(), dev.tq.data_ptr(),
+             dev.stream)
+    dev.xp.copy_(torch.from_numpy(d[f"{tag}_p"]))
+    dev.xq.copy_(torch.from_numpy(d[f"{tag}_q"]))
+    return dev, GPUProblem(dev)
+
+
+def _sym6_to_mat(s):
+    m = np.empty(s.shape[:-1] + (3, 3))
+    idx = [(0, 0, 0), (1, 0, 1), (2, 0, 2), (3, 1, 1), (4, 1, 2), (5, 2, 2)]
+    for t, r, c in idx:
+        m[..., r, c] = s[..., t]
+        m[..., c, r] = s[..., t]
+    return m
+
+
+@pytest.mark.parametrize("tag", ["near", "rand"])
+def test_assembly_vs_golden(cuda_ok, tag):
+    import torch
+    from paper_2308_10459_b200 import _lib as L
+    d = load("newton_pieces.npz")
+    dev, prob = _gpu_problem(d, tag)
+    f, gnorm, cnorm, _ = prob.assemble(dev.xp, dev.xq)
+    assert f == pytest.approx(float(d[f"{tag}_f"]), rel=1e-12)
+    assert gnorm == pytest.approx(float(d[f"{tag}_gnorm"]), rel=1e-10)
+    z = dev.z[:6 * dev.nf].cpu().numpy()
+    _assert_close(z, d[f"{tag}_z"], 1e-9, 1e-11 * np.abs(z).max(), "z")
+    # clamped bond blocks against build_clamped_pieces (active bonds)
+    b = bonds_from(d, f"{tag}_b_")
+    act = np.nonzero(b.status != 2)[0]
+    st = dev.stage.cpu().numpy()
+    apos = _sym6_to_mat(st[L.ST["APOS"]:L.ST["APOS"] + 6].T[act])
+    want_pp = d[f"{tag}_bond_pp"]
+    hs = np.abs(want_pp).max()
+    _assert_close(apos, want_pp[:, :3, :3], 1e-10, 1e-12 * hs, "a+ (ii)")
+    _assert_close(-apos, want_pp[:, :3, 3:], 1e-10, 1e-12 * hs, "-a+ (ij)")
+    rot = d[f"{tag}_bond_qq_red"]
+    hr = np.abs(rot).max()
+    A = _sym6_to_mat(st[L.ST["A"]:L.ST["A"] + 6].T[act])
+    D = _sym6_to_mat(st[L.ST["D"]:L.ST["D"] + 6].T[act])
+    Cb = st[L.ST["C"]:L.ST["C"] + 9].T[act].reshape(-1, 3, 3)
+    _assert_close(A, rot[:, :3, :3], 1e-9, 1e-11 * hr, "rot (ii)")
+    _assert_close(D, rot[:, 3:, 3:], 1e-9, 1e-11 * hr, "rot (jj)")
+    _assert_close(Cb, rot[:, :3, 3:], 1e-9, 1e-11 * hr, "rot (ij)")
+    # diagonal blocks and block-Jacobi inverses
+    diag = dev.diag[:dev.nf].cpu().numpy()
+    P, R = _sym6_to_mat(diag[:, :6]), _sym6_to_mat(diag[:, 6:])
+    want = d[f"{tag}_diag"]
+    sc = np.abs(want).max()
+    _assert_close(P, want[:, :3, :3], 1e-9, 1e-11 * sc, "diag pos")
+    _assert_close(R, want[:, 3:, 3:], 1e-9, 1e-11 * sc, "diag rot")
+    minv = dev.minv[:dev.nf].cpu().numpy()
+    wm = d[f"{tag}_minv"]
+    _assert_close(_sym6_to_mat(minv[:, :6]), wm[:, :3, :3], 1e-7, 1e-9 * np.abs(wm).max(), "Pinv")
+    _assert_close(_sym6_to_mat(minv[:, 6:]), wm[:, 3:, 3:], 1e-7, 1e-9 * np.abs(wm).max(), "Rinv")
+    # SpMV against the reference's assembled CSR (as dense)
+    Adense = d[f"{tag}_A"]
+    rng = np.random.default_rng(3)
+    x = rng.normal(size=Adense.shape[0])
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.zeros_like(xd)
+    dev.call("bdem_spmv", dev.sysp, xd.data_ptr(), yd.data_ptr(), dev.stream)
+    want_y = Adense @ x
+    _assert_close(yd.cpu().numpy(), want_y, 1e-9, 1e-11 * np.abs(want_y).max(), "A x")
+    # PCG at the reference's inner tolerance
+    res = prob.solve_pcg(float(d[f"{tag}_pcg_tol"]), 2000)
+    assert abs(res.iterations - int(d[f"{tag}_pcg_it"])) <= 1
+    y = dev.y[:6 * dev.nf].cpu().numpy()
+    if res.iterations == int(d[f"{tag}_pcg_it"]):
+        _assert_close(y, d[f"{tag}_pcg_x"], 1e-6, 1e-8 * np.abs(y).max(), "pcg x")
+    # tight solve is path independent: compare to the exact solution
+    res = prob.solve_pcg(1e-10, 2000)
+    y = dev.y[:6 * dev.nf].cpu().numpy()
+    _assert_close(y, d[f"{tag}_pcg_tight_x"], 1e-7, 1e-9 * np.abs(y).max(), "tight pcg x")
+    # objective value at the iterate
+    val = prob.value(dev.xp, dev.xq)
+    assert val == pytest.approx(float(d[f"{tag}_value"]), rel=1e-12)
+
+
+def test_newton_solve_vs_golden(cuda_ok):
+    from paper_2308_10459_b200 import SolverConfig, minimize_second_order
+    d = load("newton_pieces.npz")
+    dev, prob = _gpu_problem(d, "near")
+    sol = minimize_second_order(prob, dev.xp.clone(), dev.xq.clone(),
+                                SolverConfig(epsilon=1e-7, max_iterations=30))
+    assert sol.converged == bool(d["solve_converged"])
+    assert abs(sol.iterations - int(d["solve_iterations"])) <= 1
+    _assert_close(sol.p.cpu().numpy(), d["solve_p"], 1e-9, 1e-11, "p")
+    _assert_close(sol.q.cpu().numpy(), d["solve_q"], 1e-9, 1e-11, "q")
+
+
+# ---------------------------------------------------------------------------
+# step level (solver.py:881-939)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["cantilever", "rope", "plate", "cube"])
+def test_trajectory_vs_golden(cuda_ok, name):
+    from paper_2308_10459_b200 import HalfSpace, PlasticParams, Scene, SolverConfig, stable_step
+    from paper_2308_10459_b200 import configs as C
+    from paper_2308_10459_b200.scene import TwistDriver
+    d = load(f"traj_{name}.npz")
+    el = elements_from(d, "init_el_")
+    b = bonds_from(d, "init_b_")
+    driver, sched, cols = None, None, []
+    if name == "rope":
+        spec = C.rope(n=30)
+        driver = TwistDriver(spec.driver.ids, spec.driver.p0, spec.driver.axis_point,
+                             spec.driver.rate)
+    if name == "cube":
+        spec = C.cube(n_side=5, random_q=False, seed=3, youngs=3e8, k_contact=1e9, speed=2.0,
+                      dt=1e-4)
+        sched = spec.collider_schedule
+    if name == "plate":
+        cols = [HalfSpace((0.0, 0.0, 1.0), 0.0)]
+    plastic = PlasticParams(*d["plastic"]) if "plastic" in d else None
+    scene = Scene(name, el, b, colliders=cols, gravity=d["gravity"], dt=float(d["dt"]),
+                  youngs=float(d["youngs"]), k_contact=float(d["k_contact"]),
+                  k_element=float(d["k_element"]), plastic=plastic, driver=driver)
+    cfg = SolverConfig(epsilon=float(d["epsilon"]), max_iterations=300)
+    m_dt2 = (el.mass / float(d["dt"]) ** 2).min()
+    atol_p = max(10 * float(d["epsilon"]) / m_dt2, 1e-12)
+    events = []
+    for s in range(d["p"].shape[0]):
+        if sched is not None:
+            scene.colliders = sched(scene.time + scene.dt)
+        rep = stable_step(scene, cfg)
+        assert rep.committed == bool(d["committed"][s])
+        events += [(s, bb) for (bb, _, _) in rep.broken]
+        _assert_close(scene.elements.p, d["p"][s], 1e-8, atol_p, f"step {s} p")
+        _assert_close(scene.elements.q, d["q"][s], 1e-8, 1e-9, f"step {s} q")
+        _assert_close(scene.elements.v, d["v"][s], 1e-6, atol_p / float(d["dt"]), f"step {s} v")
+    assert [tuple(e) for e in events] == [(int(a), int(bb)) for a, bb, _, _ in d["events"]]
+    assert np.array_equal(scene.bonds.status, d["final_b_status"])
+
+
+@pytest.mark.parametrize("mode", ["plastic", "elastic"])
+def test_fracture_vs_golden(cuda_ok, mode):
+    from paper_2308_10459_b200 import PlasticParams, update_bond_states
+    d = load("fracture.npz")
+    b = bonds_from(d, "b_")
+    pl = PlasticParams(*d["plastic"]) if mode == "plastic" else None
+    ev = update_bond_states(b, d["p"], d["q"], 1e9, pl)
+    want = d[f"{mode}_events"]
+    assert [e[0] for e in ev] == [int(x) for x in want[:, 0]]
+    if ev:
+        _assert_close(np.array([e[1:] for e in ev]), want[:, 1:], 1e-12, 0.0, "event stresses")
+    for f in ("stiffness_scale", "damage", "plastic_strain", "sigma", "tau"):
+        _assert_close(getattr(b, f), d[f"{mode}_out_{f}"], 1e-12, 0.0, f)
+    assert np.array_equal(b.status, d[f"{mode}_out_status"])
+
+
+def test_broadphase_and_components_vs_golden(cuda_ok):
+    from paper_2308_10459_b200 import broad_phase, label_components
+    d = load("broadphase_labels.npz")
+    for tag in ("a", "b"):
+        got = broad_phase(d[f"{tag}_pos"], d[f"{tag}_rad"], float(d[f"{tag}_cell"]))
+        assert np.array_equal(got, d[f"{tag}_pairs"])
+
+    class B:
+        pass
+    b = B()
+    b.i, b.j, b.status = d["lab_i"], d["lab_j"], d["lab_status"]
+    lab = label_components(int(d["lab_n"]), b)
+    assert np.array_equal(lab.labels, d["lab_labels"])
