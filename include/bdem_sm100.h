@@ -181,6 +181,7 @@ typedef struct {
 /* ---- library ----------------------------------------------------------- */
 int bdem_abi_version(void);
 int64_t bdem_system_size(void); /* sizeof(bdem_system_t), for binding checks */
+int64_t bdem_launch_count(void); /* kernels launched by this library so far */
 int bdem_device_sm(void); /* compute capability of device 0, e.g. 100 */
 
 /* ---- bonds ------------------------------------------------------------- */
@@ -294,6 +295,13 @@ int bdem_pcg_init(const bdem_system_t *sys, const double *b, double sign, double
                   void *stream);
 int bdem_pcg_iterate(const bdem_system_t *sys, double *x, double *r, double *zv, double *pv,
                      double *ap, int n_iter, void *stream);
+
+/* The two halves of one PCG iteration, for callers that time the SpMV
+ * separately: Ap = A p (+ boost p) with p.Ap and the breakdown test, then
+ * x/r/z updates, r.r, r.z, convergence test and p = z + beta p. */
+int bdem_pcg_spmv(const bdem_system_t *sys, const double *pv, double *ap, void *stream);
+int bdem_pcg_update(const bdem_system_t *sys, double *x, double *r, double *zv, double *pv,
+                    const double *ap, void *stream);
 
 /* Block-Jacobi apply z = M^-1 r (linalg.py:124-126). */
 int bdem_precond_apply(const bdem_system_t *sys, const double *r, double *zv, void *stream);

@@ -65,6 +65,9 @@ SIGNATURES = {
     "bdem_abi_version": (_int, []),
     "bdem_system_size": (_i64, []),
     "bdem_device_sm": (_int, []),
+    "bdem_launch_count": (_i64, []),
+    "bdem_pcg_spmv": (_int, [_sys, _p, _p, _p]),
+    "bdem_pcg_update": (_int, [_sys, _p, _p, _p, _p, _p, _p]),
     "bdem_bond_eval_ambient": (_int, [_sys, _p, _p, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _int, _p]),
     "bdem_bond_assemble": (_int, [_sys, _p, _p, _p]),
     "bdem_bond_energy": (_int, [_sys, _p, _p, _int, _p]),

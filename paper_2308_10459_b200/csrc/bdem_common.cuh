@@ -12,7 +12,11 @@ constexpr int kThreads = 256;
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
-inline int launch_status() {
+// kernels launched by this library (defined in topology_kernels.cu)
+void count_launches(int64_t k);
+
+inline int launch_status(int64_t kernels = 1) {
+  count_launches(kernels);
   return cudaGetLastError() == cudaSuccess ? BDEM_OK : BDEM_ERR_CUDA;
 }
 

@@ -354,7 +354,22 @@ int bdem_pcg_iterate(const bdem_system_t *sys, double *x, double *r, double *zv,
     k_pcg_update<<<kRedBlocks, kThreads, 0, st>>>(*sys, x, r, zv, pv, ap);
     k_pcg_pupdate<<<kRedBlocks, kThreads, 0, st>>>(*sys, pv, zv);
   }
+  return launch_status(3 * (int64_t)n_iter);
+}
+
+int bdem_pcg_spmv(const bdem_system_t *sys, const double *pv, double *ap, void *stream) {
+  if (!sys) return BDEM_ERR_ARG;
+  k_spmv<<<kRedBlocks, kThreads, 0, as_stream(stream)>>>(*sys, pv, ap, 1);
   return launch_status();
+}
+
+int bdem_pcg_update(const bdem_system_t *sys, double *x, double *r, double *zv, double *pv,
+                    const double *ap, void *stream) {
+  if (!sys) return BDEM_ERR_ARG;
+  cudaStream_t st = as_stream(stream);
+  k_pcg_update<<<kRedBlocks, kThreads, 0, st>>>(*sys, x, r, zv, pv, ap);
+  k_pcg_pupdate<<<kRedBlocks, kThreads, 0, st>>>(*sys, pv, zv);
+  return launch_status(2);
 }
 
 int bdem_pair_assemble(const bdem_system_t *sys, const double *p, int energy_only,

@@ -3,6 +3,8 @@
 //
 // Sorting / scans use CUB (header library shipped with the CUDA toolkit)
 // inside this library; everything else is hand-written.
+#include <atomic>
+
 #include <cub/cub.cuh>
 
 #include "bdem_common.cuh"
@@ -139,9 +141,16 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace bdem
 
+namespace bdem {
+static std::atomic<long long> g_launches{0};
+void count_launches(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+}  // namespace bdem
+
 using namespace bdem;
 
 extern "C" {
+
+int64_t bdem_launch_count(void) { return (int64_t)g_launches.load(); }
 
 // workspace layout for the broad phase
 static size_t bp_cub_bytes(int64_t n) {
@@ -209,11 +218,11 @@ int bdem_broadphase(const double *p, const double *radii, int64_t n, double cell
   cudaMemcpyAsync(&total, offs + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) return BDEM_ERR_CUDA;
   *n_out = total;
-  if (pairs == nullptr || total == 0) return launch_status();
+  if (pairs == nullptr || total == 0) return launch_status(5);
   if (total > cap) return BDEM_ERR_ARG;
   k_pairs<<<grid_for(n), kThreads, 0, st>>>(p, radii, n, cxyz, h, ny, nz, skeys, sids, labels, cnt,
                                             offs, pairs, 1);
-  return launch_status();
+  return launch_status(1);
 }
 
 static size_t cc_cub_bytes(int64_t n) {
@@ -262,6 +271,7 @@ int bdem_components(int64_t n, int64_t n_bond, const int32_t *bi, const int32_t 
   cudaMemsetAsync(isroot + n, 0, sizeof(int32_t), st);
   cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, isroot, rank, (int)n + 1, st);
   k_cc_label<<<grid_for(n), kThreads, 0, st>>>(parent, rank, n, labels);
+  count_launches(4);
   if (n_comp) {
     int32_t nc = 0;
     cudaMemcpyAsync(&nc, rank + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st);

@@ -149,16 +149,12 @@ class DeviceSystem:
         self.h_scalars = torch.zeros(L.SC["COUNT"], dtype=F64).pin_memory()
         self.h_pcg = torch.zeros(L.PCG["COUNT"], dtype=F64).pin_memory()
         self.h_err = torch.zeros(L.ERRSLOT_COUNT, dtype=I32).pin_memory()
-        # contact pairs (capacity grows on demand)
-        self.pair_cap = 0
-        self.n_pair = 0
-        self.pairs = None
-        self._pair_bufs = {}
-        self._alloc_pairs(1024)
         self._bp_work = None
         self._cc_work = None
         self._sel_work = None
         self.launches = 0
+        self.labels = None
+        self.timer = None   # optional timing.KernelTimer picked up by GPUProblem
 
         self.sys = L.System()
         s = self.sys
@@ -175,6 +171,9 @@ class DeviceSystem:
         s.red, s.scalars, s.pcg = _ptr(self.red), _ptr(self.scalars), _ptr(self.pcg_state)
         s.err, s.counter = _ptr(self.err), _ptr(self.counter)
         self.sysp = C.pointer(s)
+        # contact pairs (capacity grows on demand)
+        self.n_pair = 0
+        self._alloc_pairs(1024)
         self.reset_errors()
 
         if scene is not None:
@@ -263,14 +262,12 @@ class DeviceSystem:
         dev = self.device
         self.pair_cap = int(cap)
         self.pstage = torch.zeros((L.PS["COUNT"], self.pair_cap), dtype=F64, device=dev)
-        self.pair_ij = torch.zeros((self.pair_cap, 2), dtype=I32, device=dev)
         self.pi_ptr = torch.zeros(self.n + 1, dtype=I32, device=dev)
         self.pj_ptr = torch.zeros(self.n + 1, dtype=I32, device=dev)
         self.pj_idx = torch.zeros(self.pair_cap, dtype=I32, device=dev)
         s = self.sys
         s.pair_cap = self.pair_cap
         s.pstage = _ptr(self.pstage)
-        s.pair_i = _ptr(self.pair_ij[:, 0:1])  # strided view: set below
         self._pair_i = torch.zeros(self.pair_cap, dtype=I32, device=dev)
         self._pair_j = torch.zeros(self.pair_cap, dtype=I32, device=dev)
         s.pair_i, s.pair_j = _ptr(self._pair_i), _ptr(self._pair_j)

@@ -14,6 +14,7 @@ import math
 from dataclasses import dataclass, field
 
 import numpy as np
+import torch
 
 from . import _lib as L
 
@@ -93,9 +94,12 @@ class GPUProblem:
     colliders, frozen pairs) has been prepared by the predictor.
     """
 
-    def __init__(self, dev):
+    def __init__(self, dev, timer=None):
         self.dev = dev
         self.free = dev.free_np
+        # optional KernelTimer: CUDA events around the fused bond kernel and
+        # every SpMV launch (bench.py's live roofline measurement)
+        self.timer = timer if timer is not None else getattr(dev, "timer", None)
 
     @property
     def n(self):
@@ -106,7 +110,12 @@ class GPUProblem:
         d = self.dev
         s, st = d.sysp, d.stream
         if d.nb:
+            tm = self.timer
+            if tm is not None:
+                tm.begin("bond_assemble")
             d.call("bdem_bond_assemble", s, p.data_ptr(), q.data_ptr(), st)
+            if tm is not None:
+                tm.end("bond_assemble")
         if d.n_pair:
             d.call("bdem_pair_assemble", s, p.data_ptr(), 0, st)
         d.call("bdem_element_assemble", s, p.data_ptr(), q.data_ptr(), d.z.data_ptr(), st)
@@ -166,13 +175,27 @@ class GPUProblem:
             d.call("bdem_pcg_init", s, d.z.data_ptr(), -1.0, *ptrs, float(tol), int(max_iter),
                    float(boost), st)
             chunk = chunk0
+            tm = self.timer
+            k_before = 0
             while True:
-                d.call("bdem_pcg_iterate", s, *ptrs, d.ap.data_ptr(), int(chunk), st)
+                if tm is None:
+                    d.call("bdem_pcg_iterate", s, *ptrs, d.ap.data_ptr(), int(chunk), st)
+                else:
+                    for _ in range(chunk):
+                        tm.begin("spmv")
+                        d.call("bdem_pcg_spmv", s, ptrs[3], d.ap.data_ptr(), st)
+                        tm.end("spmv")
+                        d.call("bdem_pcg_update", s, *ptrs, d.ap.data_ptr(), st)
                 d.h_pcg.copy_(d.pcg_state, non_blocking=True)
-                import torch
                 torch.cuda.current_stream(d.device).synchronize()
                 h = d.h_pcg.numpy()
                 state = int(h[L.PCG["STATE"]])
+                if tm is not None:
+                    # SpMV launches after the solve stopped exited early: drop them
+                    k_now = int(h[L.PCG["K"]])
+                    worked = k_now - k_before + (1 if state == L.PCG_BREAKDOWN else 0)
+                    tm.drop_last("spmv", chunk - min(worked, chunk))
+                    k_before = k_now
                 if state == L.PCG_RUNNING:
                     chunk = min(chunk * 2, chunk_max)
                     continue

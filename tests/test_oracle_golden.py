@@ -104,10 +104,16 @@ def test_newton_pieces(tag):
 
 
 def test_newton_solve():
-    d = load("newton_pieces.npz")
-    obj = _objective(d, "near")
-    sol = O.newton(obj, d["near_p"], d["near_q"], O.Config(epsilon=1e-7, max_iterations=30))
-    assert sol.converged == bool(d["solve_converged"])
+    d = load("newton_solve.npz")
+    el = elements_from(d, "el_")
+    b = bonds_from(d, "b_")
+    hs = d["hs"]
+    obj = O.Objective(el, b, d["pairs"], [HalfSpace(tuple(hs[:3]), hs[3])], d["gravity"],
+                      float(d["kc"]), float(d["ke"]), float(d["dt"]), d["p_prev"], d["q_prev"],
+                      el.p.copy(), el.q.copy())
+    sol = O.newton(obj, d["p0"], d["q0"], O.Config(epsilon=float(d["epsilon"]),
+                                                   max_iterations=200))
+    assert sol.converged
     assert sol.iterations == int(d["solve_iterations"])
     assert sol.pcg_total == int(d["solve_pcg_total"])
     _assert_close(sol.p, d["solve_p"], 1e-10, 1e-12, "p")
