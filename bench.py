@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Benchmark: Newton iterations/s of the implicit BDEM step on the 600K plate.
+
+Workload (BASELINE.json configs[2]): 1000x600 triangular
+ceramic plate, 600,000 spheres, 3,591,004 bonds, E=3e11, dropped at 5 m/s
+onto a half-space, tilted 10 deg, plasticity/fracture on, dt=5e-6,
+eps=1e-3 (the fp64 gradient noise floor at 600K is ~3e-5 N).
+Synthetic, seeded inputs; no dataset.
+
+A bench "step" is one implicit time step (``stable_step``: broad phase,
+predictor, full manifold Newton solve with PCG and line search, velocity
+update, fracture update, energies).  ``value`` = Newton iterations (all
+ranks) / max-over-ranks device time.  ``e2e`` repeats the measurement through
+the same public call with host buffers (``Scene(host_sync=True)``: host->device
+upload of the element and bond state before, device->host download after,
+every step).  Per-kernel durations (fused bond assembly, every SpMV) are
+taken live with CUDA events on the launching stream inside the timed region.
+
+``--impl reference`` times the reference's algorithm on the host cores: the
+CPU oracle (``oracle/cpu_oracle.py``, a restatement of the reference pinned to
+its golden vectors; the reference itself is Python and cannot travel) on a
+bounded sample of the same workload -- Newton iterations of the first step of
+a 100x60 crop of the plate -- scaled to 600K-equivalent Newton it/s by the
+bond-count ratio (the reference's per-iteration cost is linear in bonds,
+SURVEY §2/§6).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "Newton iters/sec @600K particles; bonds/sec assembled; SpMV HBM GB/s vs peak"
+UNIT = "Newton it/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nx", type=int, default=1000)
+    ap.add_argument("--ny", type=int, default=600)
+    ap.add_argument("--epsilon", type=float, default=1e-3)
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--crop", type=int, nargs=2, default=(100, 60),
+                    help="plate crop for the CPU sample (nx ny)")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (oracle on a bounded crop)
+# ---------------------------------------------------------------------------
+
+def cpu_sample(nx, ny, eps, warmup, steps, threads):
+    """Oracle Newton iterations on the first step of an nx x ny plate crop.
+    Returns (it/s on the crop, crop bonds, iterations, pcg per it, seconds)."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import cpu_oracle as O
+    from paper_2308_10459_b200 import configs as C
+    spec = C.plate(nx=nx, ny=ny, epsilon=eps)
+    el = spec.elements
+    st = O.OracleState(el.copy(), spec.bonds.copy(), spec.dt, spec.youngs,
+                       colliders=spec.colliders, gravity=spec.gravity, k_contact=spec.k_contact,
+                       k_element=spec.k_element, plastic=spec.plastic)
+    pairs = O.candidates(st, st.labels)
+    obj = O.Objective(st.elements, st.bonds, pairs, st.colliders, st.gravity, st.k_contact,
+                      st.k_element, st.dt, st.p_prev.copy(), st.q_prev.copy(),
+                      st.elements.p.copy(), st.elements.q.copy())
+    p0, q0 = O.predictor(st.elements, st.dt, obj.free)
+    with threadpool_limits(limits=threads):
+        res = O.newton(obj, p0, q0, O.Config(epsilon=eps, max_iterations=max(warmup, 1)))
+        t0 = time.perf_counter()
+        res2 = O.newton(obj, res.p, res.q, O.Config(epsilon=eps * 1e-3, max_iterations=steps))
+        dt = time.perf_counter() - t0
+    its = max(len([r for r in res2.records if r.alpha > 0 or r.pcg_iterations]), 1)
+    pcg = res2.pcg_total / its
+    return its / dt, spec.bonds.n, its, pcg, dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_2308_10459_b200 import configs as C
+    nb_full = 3_591_004 if (args.nx, args.ny) == (1000, 600) else \
+        C.plate(nx=args.nx, ny=args.ny).bonds.n
+    cores = os.cpu_count() or 1
+    rate, nb_crop, its, pcg, sec = cpu_sample(args.crop[0], args.crop[1], args.epsilon,
+                                              args.warmup, args.steps, cores)
+    value = rate * nb_crop / nb_full
+    sample = (f"oracle Newton iterations {args.warmup}+1..{args.warmup + its} of step 1 on a "
+              f"{args.crop[0]}x{args.crop[1]} crop ({nb_crop} bonds, {pcg:.1f} PCG/it, "
+              f"{sec:.1f}s), scaled by bonds {nb_crop}/{nb_full}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": its, "warmup": args.warmup,
+        "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_block(args):
+    return {"workload": f"C3 plate impact {args.nx}x{args.ny} (BASELINE configs[2])",
+            "spheres": args.nx * args.ny, "epsilon": args.epsilon, "dt": 5e-6,
+            "l2": "inputs larger than L2 (bond staging 39 x n_bond fp64 >> 126 MB)",
+            "parallelism": f"replicas x{args.gpus}"}
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join(timeout=1.0)
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def spmv_bytes(dev):
+    """Algorithmic bytes of one SpMV in this library's format:
+    per bond with both ends free: a+ (6) + C (9) fp64 read once = 120 B, plus
+    two adjacency entries (bond id + other slot, int32) = 16 B; per free row:
+    x and y (48 + 48 B), diagonal P, R (96 B), adj_ptr/adj_mid/free_elem (12 B)."""
+    import numpy as np
+    oslot = dev.adj_oslot.cpu().numpy()
+    entries = int((oslot >= 0).sum())          # 2 per free-free bond
+    return 60 * entries + 8 * entries + dev.nf * (48 + 48 + 96 + 12)
+
+
+def assembly_bytes(dev):
+    """Algorithmic bytes of one fused bond-assembly launch: per bond 161 B in
+    (i, j, status, 18 geometry fp64, scale) + 312 B staged out (39 fp64); per
+    element the gathered p, q rows once (56 B)."""
+    return dev.nb * (161 + 312) + dev.n * 56
+
+
+def load_ncu_traffic():
+    path = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+
+    from paper_2308_10459_b200 import SolverConfig, configs, stable_step
+    from paper_2308_10459_b200 import _lib as L
+    from paper_2308_10459_b200.scene import Scene
+    from paper_2308_10459_b200.timing import KernelTimer
+
+    lib = L.load()
+    spec = configs.plate(nx=args.nx, ny=args.ny, epsilon=args.epsilon)
+    scene = Scene.from_spec(spec, host_sync=False)
+    cfg = SolverConfig(epsilon=args.epsilon, max_iterations=300)
+    dev = scene.device
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        stable_step(scene, cfg)
+
+    timer = KernelTimer()
+    dev.timer = timer
+    stats = {"newton": 0, "pcg": 0, "ls": 0, "committed": 0, "broken": 0, "pairs": 0}
+    barrier()
+    launches0 = lib.bdem_launch_count()
+    with ClockSampler(local) as clocks:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(args.steps):
+            rep = stable_step(scene, cfg)
+            stats["newton"] += rep.solve.iterations
+            stats["pcg"] += rep.solve.pcg_total
+            stats["ls"] += sum(r.ls_trials for r in rep.solve.records)
+            stats["committed"] += int(rep.committed)
+            stats["broken"] += len(rep.broken)
+            stats["pairs"] = max(stats["pairs"], rep.contact_pairs)
+        t1.record()
+        barrier()
+    launches = lib.bdem_launch_count() - launches0
+    ms = t0.elapsed_time(t1)
+    durations = timer.resolve()
+    dev.timer = None
+
+    # e2e through the same public call with host buffers every step
+    n_e2e = args.e2e_steps if args.e2e_steps is not None else args.steps
+    scene.sync_to_host()
+    scene.host_sync = True
+    e2e_newton = 0
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(n_e2e):
+        rep = stable_step(scene, cfg)
+        e2e_newton += rep.solve.iterations
+    e1.record()
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    h2d = dev.n * (3 + 4 + 3 + 4 + 3 + 4) * 8 + dev.nb * (5 * 8 + 1)
+    d2h = h2d
+
+    ms_t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device="cuda")
+    cnt_t = torch.tensor([stats["newton"], e2e_newton], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(cnt_t, op=dist.ReduceOp.SUM)
+    ms_max, e2e_ms_max = float(ms_t[0]), float(ms_t[1])
+    newton_all, e2e_newton_all = float(cnt_t[0]), float(cnt_t[1])
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    peak, peak_kind = peaks()
+    spmv = durations.get("spmv", [])
+    asm = durations.get("bond_assemble", [])
+    spmv_ms = statistics.mean(spmv) if spmv else float("nan")
+    asm_ms = statistics.mean(asm) if asm else float("nan")
+    sb = spmv_bytes(dev)
+    ab = assembly_bytes(dev)
+    achieved = sb / (spmv_ms * 1e-3) / 1e9
+    traffic = load_ncu_traffic()
+    value = newton_all / (ms_max * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, paper_2308_10459_b200/configs.py)",
+        "config": config_block(args),
+        "newton_iterations": stats["newton"], "pcg_per_newton": stats["pcg"] / max(stats["newton"], 1),
+        "ls_trials_per_newton": stats["ls"] / max(stats["newton"], 1),
+        "committed_steps": stats["committed"], "broken_bonds": stats["broken"],
+        "bonds_per_sec_assembled": dev.nb / (asm_ms * 1e-3),
+        "assembly": {"ms": asm_ms, "launches": len(asm), "bytes": ab,
+                     "achieved_gbs": ab / (asm_ms * 1e-3) / 1e9,
+                     "frac": ab / (asm_ms * 1e-3) / 1e9 / peak},
+        "spmv": {"ms": spmv_ms, "launches": len(spmv), "bytes": sb, "achieved_gbs": achieved},
+        "roofline": {"kernel": "bdem::k_spmv (PCG SpMV)", "bound": "hbm", "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "peak_source": peak_kind,
+                     "traffic": traffic.get("k_spmv", {}).get("dram_bytes_per_launch")},
+        "e2e": {"value": e2e_newton_all / (e2e_ms_max * 1e-3) if n_e2e else None, "unit": UNIT,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n_e2e},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+    }
+    if not args.no_cpu_baseline and world == 1:
+        rate, nb_crop, its, pcg, sec = cpu_sample(args.crop[0], args.crop[1], args.epsilon,
+                                                  2, 6, 1)
+        nb_full = dev.nb
+        line["cpu_baseline"] = {
+            "value": rate * nb_crop / nb_full, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": (f"oracle (numpy/scipy, 1 thread) Newton iterations 3..{2 + its} of step 1"
+                       f" on a {args.crop[0]}x{args.crop[1]} crop ({nb_crop} bonds, "
+                       f"{pcg:.1f} PCG/it, {sec:.1f}s), scaled by bonds {nb_crop}/{nb_full}")}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
