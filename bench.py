@@ -197,9 +197,7 @@ def spmv_bytes(dev):
     per bond with both ends free: a+ (6) + C (9) fp64 read once = 120 B, plus
     two adjacency entries (bond id + other slot, int32) = 16 B; per free row:
     x and y (48 + 48 B), diagonal P, R (96 B), adj_ptr/adj_mid/free_elem (12 B)."""
-    import numpy as np
-    oslot = dev.adj_oslot.cpu().numpy()
-    entries = int((oslot >= 0).sum())          # 2 per free-free bond
+    entries = int((dev.sell.pos_oslot >= 0).sum() + (dev.sell.jslot >= 0).sum())
     return 60 * entries + 8 * entries + dev.nf * (48 + 48 + 96 + 12)
 
 

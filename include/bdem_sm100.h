@@ -18,7 +18,9 @@
  *    device int array `sys->err` (see BDEM_ERRSLOT_*), read back by the host
  *    together with the scalar results it synchronises on anyway.
  *  - Layouts: p (n,3), q (n,4) scalar-last row-major like the reference;
- *    per-bond data in structure-of-arrays planes of length n_bond.
+ *    per-bond data in structure-of-arrays planes of length n_bond, indexed
+ *    by SELL-32 position (see bdem_system_t); per-free-element blocks in
+ *    planes of length n_free.
  *    Reduced vectors hold 6 doubles per free element [pos(3), rot(3)].
  */
 #ifndef BDEM_SM100_H
@@ -153,18 +155,28 @@ typedef struct {
   int8_t *status;                /* INTACT 0, WEAKENED 1, BROKEN 2      */
   const double *geom;            /* BDEM_BG_COUNT planes                */
   double *bstate;                /* BDEM_BS_COUNT planes                */
-  /* element -> bond adjacency in reference gather order: for element e the
-   * entries [adj_ptr[e], adj_mid[e]) are bonds with i == e (ascending),
-   * [adj_mid[e], adj_ptr[e+1]) bonds with j == e (ascending). */
-  const int32_t *adj_ptr, *adj_mid, *adj_bond, *adj_oslot;
+  /* SELL-32 bond layout.  Every per-bond plane (geometry, state, staging,
+   * bond_i/j, status) is indexed by POSITION, not by the caller's bond id.
+   * Elements are cut into slices of 32 consecutive ids; slice s owns the
+   * positions [slice_base[s], slice_base[s+1]), laid out slot-major
+   * (pos = slice_base[s] + 32 k + (e & 31)), slot k = the k-th bond with
+   * i == e in ascending bond id (np.add.at order, integrator.py:100-103).
+   * Padding positions have status BROKEN.  n_bond is the padded length.
+   * The j-role lists use the same shape: jpos[jslice_base[s] + 32 k + lane]
+   * is the position of the k-th bond with j == e (ascending id), -1 pad. */
+  const int32_t *slice_base;     /* (n_slices + 1)                      */
+  const int32_t *pos_oslot;      /* (n_bond) free slot of the j end, -1 */
+  const int32_t *jslice_base;    /* (n_slices + 1)                      */
+  const int32_t *jpos;           /* position of a j-role bond, -1 pad   */
+  const int32_t *jslot;          /* free slot of its i end, -1          */
   /* contact pairs (sorted i<j); pairs with i == e are [pi_ptr[e], pi_ptr[e+1]),
    * pairs with j == e are pj_idx[pj_ptr[e] .. pj_ptr[e+1]) ascending */
   const int32_t *pair_i, *pair_j, *pi_ptr, *pj_ptr, *pj_idx;
   /* staging / workspace */
   double *stage;                 /* BDEM_ST_COUNT planes x n_bond      */
   double *pstage;                /* BDEM_PS_COUNT planes x pair_cap    */
-  double *diag;                  /* (n_free, 12): P sym6, R sym6       */
-  double *minv;                  /* (n_free, 12): P^-1 sym6, R^-1 sym6 */
+  double *diag;                  /* 12 planes x n_free: P sym6, R sym6  */
+  double *minv;                  /* 12 planes x n_free: P^-1, R^-1      */
   double *red;                   /* BDEM_RED_BLOCKS x BDEM_SC_COUNT    */
   double *scalars;               /* BDEM_SC_COUNT                      */
   double *pcg;                   /* BDEM_PCG_COUNT                     */

@@ -31,7 +31,8 @@ def _nvcc():
 
 
 def lib_path() -> str:
-    return os.path.join(LIBDIR, LIBNAME)
+    # BDEM_LIB selects an alternative build of the same library (A/B tests)
+    return os.environ.get("BDEM_LIB") or os.path.join(LIBDIR, LIBNAME)
 
 
 def _stale(target: str, deps: list[str]) -> bool:
@@ -41,17 +42,22 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(OBJDIR, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, extra=None, out=None) -> str:
+    """Compile csrc/*.cu for sm_100a and link lib/libbdem_sm100.so.
+
+    ``extra`` adds nvcc flags and ``out`` redirects the library (A/B builds
+    of kernel variants, selected at run time with BDEM_LIB)."""
+    objdir = OBJDIR if out is None else out + ".obj"
+    os.makedirs(objdir, exist_ok=True)
     nvcc = _nvcc()
     sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     headers = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(INCLUDE, "bdem_sm100.h")]
     objs, jobs = [], []
     for src in sources:
-        obj = os.path.join(OBJDIR, os.path.basename(src)[:-3] + ".o")
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + headers):
-            cmd = [nvcc, *ARCH, *FLAGS, "-I", INCLUDE, "-c", src, "-o", obj]
+            cmd = [nvcc, *ARCH, *FLAGS, *(extra or []), "-I", INCLUDE, "-c", src, "-o", obj]
             if verbose:
                 cmd += ["-Xptxas", "-v"]
             jobs.append(cmd)
@@ -63,10 +69,10 @@ def build(verbose: bool = False, force: bool = False) -> str:
         return r.stdout + r.stderr
 
     with cf.ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 4))) as ex:
-        for out in ex.map(run, jobs):
-            if verbose and out:
-                print(out)
-    target = lib_path()
+        for log in ex.map(run, jobs):
+            if verbose and log:
+                print(log)
+    target = out or os.path.join(LIBDIR, LIBNAME)
     if force or jobs or _stale(target, objs):
         run([nvcc, *ARCH, "-shared", "-o", target, *objs])
     return target
@@ -74,4 +80,6 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
 if __name__ == "__main__":
     import sys
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    extra = [a for a in sys.argv[1:] if a.startswith("-D")]
+    out = next((a[6:] for a in sys.argv[1:] if a.startswith("--out=")), None)
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, extra=extra, out=out))

@@ -45,7 +45,7 @@ class System(C.Structure):
         ("mass", _p), ("radius", _p), ("mp_dt2", _p), ("mq_dt2", _p), ("p_hat", _p),
         ("q_hat", _p), ("slot", _p), ("free_elem", _p),
         ("bond_i", _p), ("bond_j", _p), ("status", _p), ("geom", _p), ("bstate", _p),
-        ("adj_ptr", _p), ("adj_mid", _p), ("adj_bond", _p), ("adj_oslot", _p),
+        ("slice_base", _p), ("pos_oslot", _p), ("jslice_base", _p), ("jpos", _p), ("jslot", _p),
         ("pair_i", _p), ("pair_j", _p), ("pi_ptr", _p), ("pj_ptr", _p), ("pj_idx", _p),
         ("stage", _p), ("pstage", _p), ("diag", _p), ("minv", _p), ("red", _p),
         ("scalars", _p), ("pcg", _p), ("err", _p), ("counter", _p),

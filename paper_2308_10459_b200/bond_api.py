@@ -31,7 +31,7 @@ def energy_terms(bonds, p, q, want_hess=False, want_grad=True, dev=None):
     dd = dev.device
     pd = torch.as_tensor(p).to(dd)
     qd = torch.as_tensor(q).to(dd)
-    idx_d = torch.as_tensor(idx.astype(np.int32)).to(dd)
+    idx_d = torch.as_tensor(dev.sell.pos_of_bond[idx].astype(np.int32)).to(dd)
     out = {k: torch.empty((m,) + s, dtype=torch.float64, device=dd)
            for k, s in (("E", ()), ("gpi", (3,)), ("gpj", (3,)), ("gqi", (4,)), ("gqj", (4,)))}
     hpp = torch.empty((m, 6, 6), dtype=torch.float64, device=dd) if want_hess else None

@@ -100,9 +100,9 @@ __global__ void __launch_bounds__(kThreads) k_element_assemble(bdem_system_t S, 
     double gp[3] = {0.0, 0.0, 0.0}, gq[4] = {0.0, 0.0, 0.0, 0.0};
     double P[6] = {0, 0, 0, 0, 0, 0}, R[6] = {0, 0, 0, 0, 0, 0};
     double ebond = 0.0;
-    const int a0 = S.adj_ptr[e], am = S.adj_mid[e], a1 = S.adj_ptr[e + 1];
-    for (int k = a0; k < am; ++k) {  // bonds with i == e
-      const int64_t b = S.adj_bond[k];
+    const int sl = (int)(e >> 5), lane = (int)(e & 31);
+    // bonds with i == e: this element's SELL row (padding stages zeros)
+    for (int64_t b = S.slice_base[sl] + lane; b < S.slice_base[sl + 1]; b += 32) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) gp[c] += -st[(BDEM_ST_GPJ + c) * nb + b];
 #pragma unroll
@@ -114,8 +114,10 @@ __global__ void __launch_bounds__(kThreads) k_element_assemble(bdem_system_t S, 
       }
       ebond += st[BDEM_ST_E * nb + b];
     }
-    for (int k = am; k < a1; ++k) {  // bonds with j == e
-      const int64_t b = S.adj_bond[k];
+    // bonds with j == e (ascending bond id)
+    for (int64_t k = S.jslice_base[sl] + lane; k < S.jslice_base[sl + 1]; k += 32) {
+      const int64_t b = S.jpos[k];
+      if (b < 0) continue;
 #pragma unroll
       for (int c = 0; c < 3; ++c) gp[c] += st[(BDEM_ST_GPJ + c) * nb + b];
 #pragma unroll
@@ -212,10 +214,11 @@ __global__ void __launch_bounds__(kThreads) k_element_assemble(bdem_system_t S, 
 #pragma unroll
       for (int t = 0; t < 6; ++t) P[t] += Ep[t];
       R[0] += erot; R[3] += erot; R[5] += erot;
-      double *dg = S.diag + 12 * (int64_t)s;
-      double *mi = S.minv + 12 * (int64_t)s;
+      const int64_t nf = S.n_free;
+      double *dg = S.diag + s;
+      double *mi = S.minv + s;
 #pragma unroll
-      for (int t = 0; t < 6; ++t) { dg[t] = P[t]; dg[6 + t] = R[t]; }
+      for (int t = 0; t < 6; ++t) { dg[t * nf] = P[t]; dg[(6 + t) * nf] = R[t]; }
       // block-Jacobi (linalg.py:100-121): singular -> identity
       double lp, ap_, lr, ar;
       eig3_minmax(P, lp, ap_);
@@ -224,14 +227,14 @@ __global__ void __launch_bounds__(kThreads) k_element_assemble(bdem_system_t S, 
       if (fmin(lp, lr) <= 1e-12 * scale) {
         const double I6[6] = {1, 0, 0, 1, 0, 1};
 #pragma unroll
-        for (int t = 0; t < 6; ++t) { mi[t] = I6[t]; mi[6 + t] = I6[t]; }
+        for (int t = 0; t < 6; ++t) { mi[t * nf] = I6[t]; mi[(6 + t) * nf] = I6[t]; }
         acc_sing += 1.0;
       } else {
         double Pi[6], Ri[6];
         inv3_sym(P, Pi);
         inv3_sym(R, Ri);
 #pragma unroll
-        for (int t = 0; t < 6; ++t) { mi[t] = Pi[t]; mi[6 + t] = Ri[t]; }
+        for (int t = 0; t < 6; ++t) { mi[t * nf] = Pi[t]; mi[(6 + t) * nf] = Ri[t]; }
       }
     }
     acc_f += fe;

@@ -29,6 +29,11 @@ __device__ __forceinline__ void load6(const double *x, int64_t s, double v[6]) {
   const double2 a = x2[0], b = x2[1], c = x2[2];
   v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = c.x; v[5] = c.y;
 }
+__device__ __forceinline__ void load6_ro(const double *x, int64_t s, double v[6]) {
+  const double2 *x2 = reinterpret_cast<const double2 *>(x + 6 * s);
+  const double2 a = __ldg(x2), b = __ldg(x2 + 1), c = __ldg(x2 + 2);
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = c.x; v[5] = c.y;
+}
 __device__ __forceinline__ void store6(double *x, int64_t s, const double v[6]) {
   double2 *x2 = reinterpret_cast<double2 *>(x + 6 * s);
   x2[0] = make_double2(v[0], v[1]);
@@ -36,111 +41,212 @@ __device__ __forceinline__ void store6(double *x, int64_t s, const double v[6]) 
   x2[2] = make_double2(v[4], v[5]);
 }
 
-// y_s = (A x)_s for one free slot s
-__device__ __forceinline__ void spmv_row(const bdem_system_t &S, const double *x, int64_t s,
-                                         const double xs[6], double y[6]) {
-  const int64_t nb = S.n_bond;
-  const double *st = S.stage;
-  const double *dg = S.diag + 12 * s;
-  symv3(dg, xs, y);
-  symv3(dg + 6, xs + 3, y + 3);
-  const int64_t e = S.free_elem[s];
-  const int a0 = S.adj_ptr[e], am = S.adj_mid[e], a1 = S.adj_ptr[e + 1];
-  for (int k = a0; k < a1; ++k) {
-    const int o = S.adj_oslot[k];
-    if (o < 0) continue;
-    const int64_t b = S.adj_bond[k];
-    double xo[6];
-    load6(x, o, xo);
-    double a[6];
+__device__ __forceinline__ void load_sym(const double *planes, int64_t s, int64_t nf, double v[6]) {
 #pragma unroll
-    for (int t = 0; t < 6; ++t) a[t] = st[(BDEM_ST_APOS + t) * nb + b];
-    double ap[3];
-    symv3(a, xo, ap);
-    y[0] -= ap[0]; y[1] -= ap[1]; y[2] -= ap[2];
-    double C[9];
-#pragma unroll
-    for (int t = 0; t < 9; ++t) C[t] = st[(BDEM_ST_C + t) * nb + b];
-    if (k < am) {  // row i: C x_j
-#pragma unroll
-      for (int r = 0; r < 3; ++r)
-        y[3 + r] += (C[3 * r] * xo[3] + C[3 * r + 1] * xo[4]) + C[3 * r + 2] * xo[5];
-    } else {       // row j: C^T x_i
-#pragma unroll
-      for (int r = 0; r < 3; ++r)
-        y[3 + r] += (C[r] * xo[3] + C[3 + r] * xo[4]) + C[6 + r] * xo[5];
-    }
-  }
-  if (S.n_pair > 0) {
-    const int64_t pc = S.pair_cap;
-    const double *ps = S.pstage;
-    for (int k = S.pi_ptr[e]; k < S.pi_ptr[e + 1]; ++k) {
-      const int o = S.slot[S.pair_j[k]];
-      if (o < 0) continue;
-      double xo[6], a[6], ap[3];
-      load6(x, o, xo);
-#pragma unroll
-      for (int t = 0; t < 6; ++t) a[t] = ps[(BDEM_PS_A + t) * pc + k];
-      symv3(a, xo, ap);
-      y[0] -= ap[0]; y[1] -= ap[1]; y[2] -= ap[2];
-    }
-    for (int kk = S.pj_ptr[e]; kk < S.pj_ptr[e + 1]; ++kk) {
-      const int64_t k = S.pj_idx[kk];
-      const int o = S.slot[S.pair_i[k]];
-      if (o < 0) continue;
-      double xo[6], a[6], ap[3];
-      load6(x, o, xo);
-#pragma unroll
-      for (int t = 0; t < 6; ++t) a[t] = ps[(BDEM_PS_A + t) * pc + k];
-      symv3(a, xo, ap);
-      y[0] -= ap[0]; y[1] -= ap[1]; y[2] -= ap[2];
-    }
-  }
+  for (int t = 0; t < 6; ++t) v[t] = planes[t * nf + s];
 }
 
 __device__ __forceinline__ void precond_row(const bdem_system_t &S, int64_t s, const double r[6],
                                             double z[6]) {
-  const double *mi = S.minv + 12 * s;
-  symv3(mi, r, z);
-  symv3(mi + 6, r + 3, z + 3);
+  const int64_t nf = S.n_free;
+  double mp[6], mr[6];
+  load_sym(S.minv, s, nf, mp);
+  load_sym(S.minv + 6 * nf, s, nf, mr);
+  symv3(mp, r, z);
+  symv3(mr, r + 3, z + 3);
 }
 
-// mode 0: plain y = A x; mode 1: PCG step (y = A p + boost p, p.Ap, |Ap|^2, |p|^2)
-__global__ void __launch_bounds__(kThreads) k_spmv(bdem_system_t S, const double *x, double *y,
-                                                   int mode) {
-  __shared__ double sh[kThreads / 32];
+// ---------------------------------------------------------------------------
+// SpMV, slot-parallel form.  One CTA works on one 32-element slice at a time:
+// warp w takes slots w, w+8, ... of the slice's i-role and j-role lists
+// (lane = element), so every thread issues one independent set of loads
+// (index -> 15 coefficient planes + the neighbour's x block) and the
+// coefficient loads of a warp are contiguous 256-byte segments.  Partial
+// products go to shared memory; warps 0..5 then form component c of
+// y = D x + sum_slots in a fixed order (deterministic).
+// mode 0: plain y = A x;  mode 1: PCG step (y = A p + boost p, p.Ap, |Ap|^2,
+// |p|^2 and the breakdown test, linalg.py:69-77).
+// ---------------------------------------------------------------------------
+#ifndef BDEM_SPMV_WARPS
+#define BDEM_SPMV_WARPS 4
+#endif
+#ifndef BDEM_SPMV_BLOCKED
+#define BDEM_SPMV_BLOCKED 0
+#endif
+#ifndef BDEM_SPMV_MINB
+#define BDEM_SPMV_MINB 8
+#endif
+constexpr int kSpmvWarps = BDEM_SPMV_WARPS;
+constexpr int kSpmvThreads = 32 * kSpmvWarps;
+
+// where slot k of a slice lives: i-role (coefficients at b, neighbour slot o,
+// C applied as is) or j-role (C^T); o < 0 = nothing to do
+struct SlotRef {
+  int64_t b;
+  int o;
+  bool tr;
+};
+
+__device__ __forceinline__ SlotRef slot_ref(const bdem_system_t &S, int64_t i0, int ki,
+                                            int64_t j0, int kj, int lane, int k) {
+  SlotRef r{0, -1, false};
+  if (k < ki) {
+    r.b = i0 + 32 * k + lane;
+    r.o = __ldg(S.pos_oslot + r.b);
+  } else if (k < ki + kj) {
+    const int64_t jk = j0 + 32 * (k - ki) + lane;
+    r.o = __ldg(S.jslot + jk);
+    r.b = __ldg(S.jpos + jk);
+    r.tr = true;
+  }
+  return r;
+}
+
+__device__ __forceinline__ void slot_apply(const bdem_system_t &S, const double *x,
+                                           const SlotRef &r, double acc[6]) {
+  if (r.o < 0) return;
+  const int64_t nb = S.n_bond;
+  const double *st = S.stage;
+  double xo[6], a[6], C[9];
+  load6_ro(x, r.o, xo);
+#pragma unroll
+  for (int t = 0; t < 6; ++t) a[t] = __ldg(st + (BDEM_ST_APOS + t) * nb + r.b);
+#pragma unroll
+  for (int t = 0; t < 9; ++t) C[t] = __ldg(st + (BDEM_ST_C + t) * nb + r.b);
+  double ap[3];
+  symv3(a, xo, ap);
+  acc[0] -= ap[0]; acc[1] -= ap[1]; acc[2] -= ap[2];
+  if (!r.tr) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+      acc[3 + q] += (C[3 * q] * xo[3] + C[3 * q + 1] * xo[4]) + C[3 * q + 2] * xo[5];
+  } else {
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+      acc[3 + q] += (C[q] * xo[3] + C[3 + q] * xo[4]) + C[6 + q] * xo[5];
+  }
+}
+
+struct SliceBounds {
+  int64_t i0, j0;
+  int ki, kj;
+};
+
+__device__ __forceinline__ SliceBounds slice_bounds(const bdem_system_t &S, int sl, int ns) {
+  SliceBounds sb{0, 0, 0, 0};
+  if (sl < ns) {
+    const int a0 = __ldg(S.slice_base + sl), a1 = __ldg(S.slice_base + sl + 1);
+    const int c0 = __ldg(S.jslice_base + sl), c1 = __ldg(S.jslice_base + sl + 1);
+    sb.i0 = a0; sb.ki = (a1 - a0) >> 5;
+    sb.j0 = c0; sb.kj = (c1 - c0) >> 5;
+  }
+  return sb;
+}
+
+// ---------------------------------------------------------------------------
+// SpMV, slot-parallel form.  One CTA walks 32-element slices; in each slice
+// warp w handles slot w of the slice's i-role then j-role lists (lane =
+// element), so each thread issues one independent set of loads: 15
+// coefficient planes (contiguous 256-byte warp segments) and the
+// neighbour's x block.  The next slice's bounds and slot indices are
+// prefetched while the current slice's data is in flight, and warps 0..5
+// prefetch their diagonal row and x before the barrier, so a slice costs
+// about one memory latency.  Partial products meet in shared memory; warp c
+// forms component c of y = D x + sum_slots in a fixed order (deterministic).
+// mode 0: plain y = A x;  mode 1: PCG step (y = A p + boost p, p.Ap, |Ap|^2,
+// |p|^2 and the breakdown test, linalg.py:69-77).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSpmvThreads, BDEM_SPMV_MINB) k_spmv(bdem_system_t S, const double *x, double *y,
+                                                       int mode) {
+  __shared__ double part[kSpmvWarps][6][32];
+  __shared__ double sh[kSpmvThreads / 32];
   double *pcg = S.pcg;
   if (mode == 1 && pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
   const double boost = mode == 1 ? pcg[BDEM_PCG_BOOST] : 0.0;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nf = S.n_free;
+  const int ns = (int)((S.n_elem + 31) >> 5);
   double acc_xy = 0.0, acc_yy = 0.0, acc_xx = 0.0;
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < S.n_free;
-       s += (int64_t)gridDim.x * blockDim.x) {
-    double xs[6], ys[6];
-    load6(x, s, xs);
-    spmv_row(S, x, s, xs, ys);
-    if (boost != 0.0) {
+#if BDEM_SPMV_BLOCKED
+  // contiguous slice ranges per CTA: neighbouring rows (and their x blocks)
+  // are processed by the same SM, so gathers reuse L1/L2 lines
+  const int per = (ns + gridDim.x - 1) / gridDim.x;
+  const int s_begin = blockIdx.x * per;
+  const int s_end = min(ns, s_begin + per);
+  const int step = 1;
+#else
+  const int s_begin = blockIdx.x, s_end = ns, step = gridDim.x;
+#endif
+#pragma unroll 1
+  for (int sl = s_begin; sl < s_end; sl += step) {
+    const SliceBounds cb = slice_bounds(S, sl, ns);
+    // tail operands (component c = w of this slice's rows), issued before the
+    // slot loads so their latency overlaps
+    const int64_t e = (int64_t)sl * 32 + lane;
+    int s = -1;
+    double dgr[3] = {0.0, 0.0, 0.0}, xs[3] = {0.0, 0.0, 0.0};
+    const int c = w, base = c < 3 ? 0 : 3, rr = c - base;
+    if (w < 6 && e < S.n_elem) {
+      s = __ldg(S.slot + e);
+      if (s >= 0) {
+        const double *dg = S.diag + (c < 3 ? 0 : 6 * nf);
 #pragma unroll
-      for (int c = 0; c < 6; ++c) ys[c] = ys[c] + boost * xs[c];
+        for (int t = 0; t < 3; ++t) {
+          xs[t] = __ldg(x + 6 * (int64_t)s + base + t);
+          dgr[t] = __ldg(dg + sidx<3>(rr, t) * nf + s);
+        }
+      }
     }
-    store6(y, s, ys);
+    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
+    for (int k = w; k < cb.ki + cb.kj; k += kSpmvWarps)
+      slot_apply(S, x, slot_ref(S, cb.i0, cb.ki, cb.j0, cb.kj, lane, k), acc);
 #pragma unroll
-    for (int c = 0; c < 6; ++c) {
-      acc_xy += xs[c] * ys[c];
-      acc_yy += ys[c] * ys[c];
-      acc_xx += xs[c] * xs[c];
+    for (int q = 0; q < 6; ++q) part[w][q][lane] = acc[q];
+    __syncthreads();
+    if (s >= 0) {
+      double yc = (dgr[0] * xs[0] + dgr[1] * xs[1]) + dgr[2] * xs[2];
+#pragma unroll
+      for (int ww = 0; ww < kSpmvWarps; ++ww) yc += part[ww][c][lane];
+      if (c < 3 && S.n_pair > 0) {
+        const int64_t pc = S.pair_cap;
+        const double *ps = S.pstage;
+        for (int k = S.pi_ptr[e]; k < S.pi_ptr[e + 1]; ++k) {
+          const int o = S.slot[S.pair_j[k]];
+          if (o < 0) continue;
+          yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[6 * (int64_t)o] +
+                 ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[6 * (int64_t)o + 1]) +
+                ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[6 * (int64_t)o + 2];
+        }
+        for (int kk = S.pj_ptr[e]; kk < S.pj_ptr[e + 1]; ++kk) {
+          const int64_t k = S.pj_idx[kk];
+          const int o = S.slot[S.pair_i[k]];
+          if (o < 0) continue;
+          yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[6 * (int64_t)o] +
+                 ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[6 * (int64_t)o + 1]) +
+                ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[6 * (int64_t)o + 2];
+        }
+      }
+      const double xc = xs[rr];
+      if (boost != 0.0) yc = yc + boost * xc;
+      y[6 * (int64_t)s + c] = yc;
+      acc_xy += xc * yc;
+      acc_yy += yc * yc;
+      acc_xx += xc * xc;
     }
+    __syncthreads();
   }
   if (mode == 0) return;
-  double v = block_sum<kThreads>(acc_xy, sh);
+  double v = block_sum<kSpmvThreads>(acc_xy, sh);
   if (threadIdx.x == 0) *red_slot(S.red, RC_PAP, blockIdx.x) = v;
-  v = block_sum<kThreads>(acc_yy, sh);
+  v = block_sum<kSpmvThreads>(acc_yy, sh);
   if (threadIdx.x == 0) *red_slot(S.red, RC_AP2, blockIdx.x) = v;
-  v = block_sum<kThreads>(acc_xx, sh);
+  v = block_sum<kSpmvThreads>(acc_xx, sh);
   if (threadIdx.x == 0) *red_slot(S.red, RC_PP2, blockIdx.x) = v;
   if (!last_block(S.counter + CNT_SPMV)) return;
-  const double pap = sum_partials<kThreads>(S.red, RC_PAP, gridDim.x, sh);
-  const double ap2 = sum_partials<kThreads>(S.red, RC_AP2, gridDim.x, sh);
-  const double pp2 = sum_partials<kThreads>(S.red, RC_PP2, gridDim.x, sh);
+  const double pap = sum_partials<kSpmvThreads>(S.red, RC_PAP, gridDim.x, sh);
+  const double ap2 = sum_partials<kSpmvThreads>(S.red, RC_AP2, gridDim.x, sh);
+  const double pp2 = sum_partials<kSpmvThreads>(S.red, RC_PP2, gridDim.x, sh);
   if (threadIdx.x == 0) {
     pcg[BDEM_PCG_PAP] = pap;
     pcg[BDEM_PCG_APNORM2] = ap2;
@@ -317,6 +423,20 @@ __global__ void __launch_bounds__(kThreads) k_pair(bdem_system_t S, const double
   if (threadIdx.x == 0) *red_slot(S.red, BDEM_SC_EPAIR, blockIdx.x) = s;
 }
 
+// resident-grid size of k_spmv (one wave), capped by the partial-sum slots
+static unsigned int spmv_grid() {
+  static unsigned int g = 0;
+  if (g == 0) {
+    int dev = 0, sms = 148, per_sm = 4;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv, kSpmvThreads, 0);
+    long long want = (long long)sms * (per_sm > 0 ? per_sm : 1);
+    g = (unsigned int)(want < kRedBlocks ? want : kRedBlocks);
+  }
+  return g;
+}
+
 }  // namespace bdem
 
 using namespace bdem;
@@ -325,7 +445,7 @@ extern "C" {
 
 int bdem_spmv(const bdem_system_t *sys, const double *x, double *y, void *stream) {
   if (!sys) return BDEM_ERR_ARG;
-  k_spmv<<<kRedBlocks, kThreads, 0, as_stream(stream)>>>(*sys, x, y, 0);
+  k_spmv<<<spmv_grid(), kSpmvThreads, 0, as_stream(stream)>>>(*sys, x, y, 0);
   return launch_status();
 }
 
@@ -350,7 +470,7 @@ int bdem_pcg_iterate(const bdem_system_t *sys, double *x, double *r, double *zv,
   if (!sys || n_iter < 0) return BDEM_ERR_ARG;
   cudaStream_t st = as_stream(stream);
   for (int it = 0; it < n_iter; ++it) {
-    k_spmv<<<kRedBlocks, kThreads, 0, st>>>(*sys, pv, ap, 1);
+    k_spmv<<<spmv_grid(), kSpmvThreads, 0, st>>>(*sys, pv, ap, 1);
     k_pcg_update<<<kRedBlocks, kThreads, 0, st>>>(*sys, x, r, zv, pv, ap);
     k_pcg_pupdate<<<kRedBlocks, kThreads, 0, st>>>(*sys, pv, zv);
   }
@@ -359,7 +479,7 @@ int bdem_pcg_iterate(const bdem_system_t *sys, double *x, double *r, double *zv,
 
 int bdem_pcg_spmv(const bdem_system_t *sys, const double *pv, double *ap, void *stream) {
   if (!sys) return BDEM_ERR_ARG;
-  k_spmv<<<kRedBlocks, kThreads, 0, as_stream(stream)>>>(*sys, pv, ap, 1);
+  k_spmv<<<spmv_grid(), kSpmvThreads, 0, as_stream(stream)>>>(*sys, pv, ap, 1);
   return launch_status();
 }
 

@@ -38,34 +38,63 @@ def _ptr(t) -> int:
     return 0 if t is None else t.data_ptr()
 
 
-def build_adjacency(bi: np.ndarray, bj: np.ndarray, n: int, slot: np.ndarray):
-    """Element -> bond lists in np.add.at order (integrator.py:100-103):
-    for element e, bonds with i == e ascending, then bonds with j == e
-    ascending.  Returns adj_ptr (n+1), adj_mid (n), adj_bond, adj_oslot."""
-    nb = bi.shape[0]
-    ci = np.bincount(bi, minlength=n)
-    cj = np.bincount(bj, minlength=n)
-    adj_ptr = np.zeros(n + 1, dtype=np.int64)
-    np.cumsum(ci + cj, out=adj_ptr[1:])
-    adj_mid = adj_ptr[:-1] + ci
-    bonds = np.arange(nb, dtype=np.int64)
-    oi = np.argsort(bi, kind="stable")
-    oj = np.argsort(bj, kind="stable")
-    si = np.cumsum(ci) - ci
-    sj = np.cumsum(cj) - cj
-    rank_i = np.empty(nb, dtype=np.int64)
-    rank_i[oi] = bonds - si[bi[oi]]
-    rank_j = np.empty(nb, dtype=np.int64)
-    rank_j[oj] = bonds - sj[bj[oj]]
-    pos_i = adj_ptr[bi] + rank_i
-    pos_j = adj_mid[bj] + rank_j
-    adj_bond = np.empty(2 * nb, dtype=np.int32)
-    adj_oslot = np.empty(2 * nb, dtype=np.int32)
-    adj_bond[pos_i] = bonds
-    adj_bond[pos_j] = bonds
-    adj_oslot[pos_i] = slot[bj]
-    adj_oslot[pos_j] = slot[bi]
-    return (adj_ptr.astype(np.int32), adj_mid.astype(np.int32), adj_bond, adj_oslot)
+class SellLayout:
+    """SELL-32 placement of the bonds (see bdem_system_t in the header).
+
+    Elements are cut into slices of 32 consecutive ids.  Each slice owns a
+    slot-major block of positions: slot k of lane l holds the k-th bond with
+    i == 32 s + l in ascending bond id (the order np.add.at accumulates in,
+    integrator.py:100-103).  A warp that owns a slice therefore reads slot k
+    of 32 consecutive rows as one contiguous 256-byte segment per plane.  The
+    j-role lists (bonds with j == e, ascending id) use the same shape and hold
+    positions.  Padding positions carry status BROKEN and zero data.
+    """
+
+    def __init__(self, bi: np.ndarray, bj: np.ndarray, n: int, slot: np.ndarray):
+        nb = bi.shape[0]
+        self.n_slices = ns = max((n + 31) // 32, 1)
+        self.slice_base, rank_i = self._slices(bi, n, ns)
+        self.n_pos = int(self.slice_base[-1])
+        self.pos_of_bond = self.slice_base[bi // 32] + 32 * rank_i + (bi % 32)
+        self.bond_of_pos = np.full(self.n_pos, -1, dtype=np.int64)
+        self.bond_of_pos[self.pos_of_bond] = np.arange(nb)
+        self.pos_oslot = np.full(self.n_pos, -1, dtype=np.int32)
+        self.pos_oslot[self.pos_of_bond] = slot[bj]
+        self.jslice_base, rank_j = self._slices(bj, n, ns)
+        self.n_jpos = int(self.jslice_base[-1])
+        jidx = self.jslice_base[bj // 32] + 32 * rank_j + (bj % 32)
+        self.jpos = np.full(self.n_jpos, -1, dtype=np.int32)
+        self.jpos[jidx] = self.pos_of_bond
+        self.jslot = np.full(self.n_jpos, -1, dtype=np.int32)
+        self.jslot[jidx] = slot[bi]
+
+    @staticmethod
+    def _slices(key, n, ns):
+        """Slot rank of every bond within its element (ascending id) and the
+        slice base offsets (32 x max slots per slice)."""
+        nb = key.shape[0]
+        cnt = np.bincount(key, minlength=n)
+        order = np.argsort(key, kind="stable")
+        start = np.cumsum(cnt) - cnt
+        rank = np.empty(nb, dtype=np.int64)
+        rank[order] = np.arange(nb) - start[key[order]]
+        padded = np.zeros(ns * 32, dtype=np.int64)
+        padded[:n] = cnt
+        kmax = padded.reshape(ns, 32).max(axis=1)
+        base = np.zeros(ns + 1, dtype=np.int64)
+        np.cumsum(32 * kmax, out=base[1:])
+        return base, rank
+
+    def to_positions(self, arr, fill=0):
+        """Scatter a per-bond array (..., nb) into positions (..., n_pos)."""
+        arr = np.asarray(arr)
+        out = np.full(arr.shape[:-1] + (max(self.n_pos, 1),), fill, dtype=arr.dtype)
+        out[..., self.pos_of_bond] = arr
+        return out
+
+    def to_bonds(self, arr):
+        """Gather a per-position array back into caller bond order."""
+        return np.asarray(arr)[..., self.pos_of_bond]
 
 
 def bond_geometry_planes(b) -> np.ndarray:
@@ -124,20 +153,27 @@ class DeviceSystem:
         # Newton iterate, trial point, direction (pinned rows of dp/dq stay 0)
         self.xp, self.xq, self.tp, self.tq = z3(), z4(), z3(), z4()
         self.dp, self.dq = z3(), z4()
-        # bonds
-        self.bond_i = _t(b.i.astype(np.int32), I32, dev)
-        self.bond_j = _t(b.j.astype(np.int32), I32, dev)
-        self.status = _t(np.asarray(b.status, dtype=np.int8), torch.int8, dev)
-        self.geom = _t(bond_geometry_planes(b), device=dev)
-        self.bstate = torch.zeros((L.BS["COUNT"], max(nb, 1)), dtype=F64, device=dev)
-        adj = build_adjacency(np.asarray(b.i, dtype=np.int64), np.asarray(b.j, dtype=np.int64), n,
-                              slot)
-        self.adj_ptr, self.adj_mid, self.adj_bond, self.adj_oslot = (
-            _t(a, I32, dev) for a in adj)
+        # bonds, placed by SELL-32 position
+        bi64 = np.asarray(b.i, dtype=np.int64)
+        bj64 = np.asarray(b.j, dtype=np.int64)
+        self.sell = sell = SellLayout(bi64, bj64, n, slot)
+        self.npos = npos = max(sell.n_pos, 1)
+        self.bond_i = _t(sell.to_positions(bi64.astype(np.int32)), I32, dev)
+        self.bond_j = _t(sell.to_positions(bj64.astype(np.int32)), I32, dev)
+        self.status = _t(sell.to_positions(np.asarray(b.status, dtype=np.int8), fill=2),
+                         torch.int8, dev)
+        self.geom = _t(sell.to_positions(bond_geometry_planes(b)), device=dev)
+        self.bstate = torch.zeros((L.BS["COUNT"], npos), dtype=F64, device=dev)
+        self.slice_base = _t(sell.slice_base.astype(np.int32), I32, dev)
+        self.pos_oslot = _t(np.append(sell.pos_oslot, -1).astype(np.int32), I32, dev)
+        self.jslice_base = _t(sell.jslice_base.astype(np.int32), I32, dev)
+        self.jpos = _t(np.append(sell.jpos, -1).astype(np.int32), I32, dev)
+        self.jslot = _t(np.append(sell.jslot, -1).astype(np.int32), I32, dev)
+        self.pos_of_bond_d = torch.as_tensor(sell.pos_of_bond).to(dev)
         # staging / reduced system
-        self.stage = torch.zeros((L.ST["COUNT"], max(nb, 1)), dtype=F64, device=dev)
-        self.diag = torch.zeros((max(nf, 1), 12), dtype=F64, device=dev)
-        self.minv = torch.zeros((max(nf, 1), 12), dtype=F64, device=dev)
+        self.stage = torch.zeros((L.ST["COUNT"], npos), dtype=F64, device=dev)
+        self.diag = torch.zeros((12, max(nf, 1)), dtype=F64, device=dev)
+        self.minv = torch.zeros((12, max(nf, 1)), dtype=F64, device=dev)
         v6 = lambda: torch.zeros(max(6 * nf, 6), dtype=F64, device=dev)  # noqa: E731
         self.z, self.y, self.r, self.zv, self.pv, self.ap = v6(), v6(), v6(), v6(), v6(), v6()
         self.red = torch.zeros((L.SC["COUNT"], L.RED_BLOCKS), dtype=F64, device=dev)
@@ -155,18 +191,20 @@ class DeviceSystem:
         self.launches = 0
         self.labels = None
         self.timer = None   # optional timing.KernelTimer picked up by GPUProblem
+        self._pins = {}
 
         self.sys = L.System()
         s = self.sys
-        s.n_elem, s.n_free, s.n_bond = n, nf, nb
+        s.n_elem, s.n_free, s.n_bond = n, nf, (sell.n_pos if nb else 0)
         s.mass, s.radius = _ptr(self.mass), _ptr(self.radius)
         s.mp_dt2, s.mq_dt2 = _ptr(self.mp_dt2), _ptr(self.mq_dt2)
         s.p_hat, s.q_hat = _ptr(self.p_hat), _ptr(self.q_hat)
         s.slot, s.free_elem = _ptr(self.slot), _ptr(self.free_elem)
         s.bond_i, s.bond_j, s.status = _ptr(self.bond_i), _ptr(self.bond_j), _ptr(self.status)
         s.geom, s.bstate = _ptr(self.geom), _ptr(self.bstate)
-        s.adj_ptr, s.adj_mid = _ptr(self.adj_ptr), _ptr(self.adj_mid)
-        s.adj_bond, s.adj_oslot = _ptr(self.adj_bond), _ptr(self.adj_oslot)
+        s.slice_base, s.pos_oslot = _ptr(self.slice_base), _ptr(self.pos_oslot)
+        s.jslice_base, s.jpos, s.jslot = (_ptr(self.jslice_base), _ptr(self.jpos),
+                                          _ptr(self.jslot))
         s.stage, s.diag, s.minv = _ptr(self.stage), _ptr(self.diag), _ptr(self.minv)
         s.red, s.scalars, s.pcg = _ptr(self.red), _ptr(self.scalars), _ptr(self.pcg_state)
         s.err, s.counter = _ptr(self.err), _ptr(self.counter)
@@ -205,42 +243,67 @@ class DeviceSystem:
             for t in range(6):
                 s.colliders[k].a[t] = a[t]
 
+    def _pinned(self, key, shape, dtype=F64):
+        """Reusable page-locked host staging buffer."""
+        buf = self._pins.get(key)
+        if buf is None or tuple(buf.shape) != tuple(shape):
+            buf = torch.empty(shape, dtype=dtype).pin_memory()
+            self._pins[key] = buf
+        return buf
+
+    def _h2d(self, dst, src_np, key):
+        st = self._pinned(key, dst.shape, dst.dtype)
+        st.numpy()[...] = src_np
+        dst.copy_(st, non_blocking=True)
+
+    def _d2h(self, src, key):
+        st = self._pinned(key, src.shape, src.dtype)
+        st.copy_(src, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return st.numpy()
+
     def upload_elements(self, el, p_prev=None, q_prev=None):
+        """Host -> HBM copy of the element state through pinned staging."""
         for name in ("p", "q", "v", "qdot"):
-            getattr(self, name).copy_(_host(getattr(el, name)), non_blocking=True)
+            self._h2d(getattr(self, name), getattr(el, name), name)
         if p_prev is not None:
-            self.p_prev.copy_(_host(p_prev), non_blocking=True)
-            self.q_prev.copy_(_host(q_prev), non_blocking=True)
+            self._h2d(self.p_prev, p_prev, "p_prev")
+            self._h2d(self.q_prev, q_prev, "q_prev")
 
     def upload_bond_state(self, b):
         if self.nb == 0:
             return
-        st = np.empty((L.BS["COUNT"], self.nb))
-        st[L.BS["SCALE"]] = b.stiffness_scale
-        st[L.BS["DAMAGE"]] = b.damage
-        st[L.BS["PLASTIC"]] = b.plastic_strain
-        st[L.BS["SIGMA"]] = b.sigma
-        st[L.BS["TAU"]] = b.tau
-        self.bstate.copy_(torch.from_numpy(st))
-        self.status.copy_(torch.from_numpy(np.asarray(b.status, dtype=np.int8)))
+        st = self._pinned("bstate", (L.BS["COUNT"], self.nb))
+        h = st.numpy()
+        h[L.BS["SCALE"]] = b.stiffness_scale
+        h[L.BS["DAMAGE"]] = b.damage
+        h[L.BS["PLASTIC"]] = b.plastic_strain
+        h[L.BS["SIGMA"]] = b.sigma
+        h[L.BS["TAU"]] = b.tau
+        pos = self.pos_of_bond_d
+        self.bstate[:, pos] = st.to(self.device, non_blocking=True)
+        stt = self._pinned("status", (self.nb,), torch.int8)
+        stt.numpy()[...] = b.status
+        self.status[pos] = stt.to(self.device, non_blocking=True)
 
     def download_bond_state(self, b):
         if self.nb == 0:
             return
-        st = self.bstate.cpu().numpy()
-        b.stiffness_scale[:] = st[L.BS["SCALE"]]
-        b.damage[:] = st[L.BS["DAMAGE"]]
-        b.plastic_strain[:] = st[L.BS["PLASTIC"]]
-        b.sigma[:] = st[L.BS["SIGMA"]]
-        b.tau[:] = st[L.BS["TAU"]]
-        b.status[:] = self.status.cpu().numpy()
+        pos = self.pos_of_bond_d
+        h = self._d2h(self.bstate[:, pos], "bstate_out")
+        b.stiffness_scale[:] = h[L.BS["SCALE"]]
+        b.damage[:] = h[L.BS["DAMAGE"]]
+        b.plastic_strain[:] = h[L.BS["PLASTIC"]]
+        b.sigma[:] = h[L.BS["SIGMA"]]
+        b.tau[:] = h[L.BS["TAU"]]
+        b.status[:] = self._d2h(self.status[pos], "status_out")
 
     def download_state(self, scene):
         el = scene.elements
         for name in ("p", "q", "v", "qdot"):
-            getattr(el, name)[:] = getattr(self, name).cpu().numpy()
-        scene.p_prev = self.p_prev.cpu().numpy()
-        scene.q_prev = self.q_prev.cpu().numpy()
+            getattr(el, name)[:] = self._d2h(getattr(self, name), name + "_out")
+        scene.p_prev = self._d2h(self.p_prev, "p_prev_out").copy()
+        scene.q_prev = self._d2h(self.q_prev, "q_prev_out").copy()
         self.download_bond_state(scene.bonds)
 
     def bootstrap_history(self, dt):
@@ -301,14 +364,18 @@ class DeviceSystem:
     def reset_errors(self):
         self.err.copy_(torch.tensor([0, 2**31 - 1, 0, 2**31 - 1, 0, 0, 0, 0], dtype=I32))
 
+    def bond_id(self, pos: int) -> int:
+        """Caller bond index of a SELL position."""
+        return int(self.sell.bond_of_pos[pos]) if 0 <= pos < self.sell.n_pos else -1
+
     def raise_errors(self, host_err):
         if host_err[L.ERRSLOT_DEG_COUNT] > 0:
-            first = int(host_err[L.ERRSLOT_DEG_FIRST])
+            first = self.bond_id(int(host_err[L.ERRSLOT_DEG_FIRST]))
             self.reset_errors()
             raise DegenerateBondError(f"coincident bond endpoints at bond indices [{first}] "
                                       f"({int(host_err[L.ERRSLOT_DEG_COUNT])} total)")
         if host_err[L.ERRSLOT_ANTI_COUNT] > 0:
-            first = int(host_err[L.ERRSLOT_ANTI_FIRST])
+            first = self.bond_id(int(host_err[L.ERRSLOT_ANTI_FIRST]))
             self.reset_errors()
             raise DegenerateShearError(f"antipodal quaternion pairs at bond indices [{first}] "
                                        f"({int(host_err[L.ERRSLOT_ANTI_COUNT])} total)")

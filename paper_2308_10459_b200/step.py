@@ -143,10 +143,10 @@ def _device_bond_update(dev, youngs, plastic):
         return []
     st = dev.stream
     if getattr(dev, "_flags", None) is None:
-        dev._flags = torch.zeros(dev.nb, dtype=torch.uint8, device=dev.device)
-        dev._ev_idx = torch.zeros(dev.nb, dtype=torch.int32, device=dev.device)
-        dev._sel_work = torch.empty(int(dev.lib.bdem_select_workspace(dev.nb)), dtype=torch.uint8,
-                                    device=dev.device)
+        dev._flags = torch.zeros(dev.npos, dtype=torch.uint8, device=dev.device)
+        dev._ev_idx = torch.zeros(dev.npos, dtype=torch.int32, device=dev.device)
+        dev._sel_work = torch.empty(int(dev.lib.bdem_select_workspace(dev.npos)),
+                                    dtype=torch.uint8, device=dev.device)
     pl = None
     if plastic is not None:
         arr = (C.c_double * 4)(plastic.fracture_strain, plastic.yield_strain, plastic.weakening,
@@ -155,17 +155,19 @@ def _device_bond_update(dev, youngs, plastic):
     dev.call("bdem_bond_update", dev.sysp, dev.p.data_ptr(), dev.q.data_ptr(), float(youngs), pl,
              dev._flags.data_ptr(), st)
     cnt = C.c_int64(0)
-    L.check(dev.lib.bdem_select_flagged(dev._flags.data_ptr(), dev.nb, dev._ev_idx.data_ptr(),
+    L.check(dev.lib.bdem_select_flagged(dev._flags.data_ptr(), dev.npos, dev._ev_idx.data_ptr(),
                                         dev._sel_work.data_ptr(), C.byref(cnt), st),
             "bdem_select_flagged")
     dev.launches += 1
     m = int(cnt.value)
     if m == 0:
         return []
-    idx = dev._ev_idx[:m].long()
-    sig = dev.bstate[L.BS["SIGMA"]][idx].cpu().numpy()
-    tau = dev.bstate[L.BS["TAU"]][idx].cpu().numpy()
-    return [(int(b), float(s), float(t)) for b, s, t in zip(idx.cpu().numpy(), sig, tau)]
+    pos = dev._ev_idx[:m].long()
+    sig = dev.bstate[L.BS["SIGMA"]][pos].cpu().numpy()
+    tau = dev.bstate[L.BS["TAU"]][pos].cpu().numpy()
+    ids = dev.sell.bond_of_pos[pos.cpu().numpy()]
+    order = np.argsort(ids, kind="stable")       # ascending bond id (bonds.py:564-569)
+    return [(int(ids[k]), float(sig[k]), float(tau[k])) for k in order]
 
 
 def update_bond_states(bonds, p, q, youngs, plastic=None, scene=None):

@@ -166,7 +166,7 @@ def test_assembly_vs_golden(cuda_ok, tag):
     # clamped bond blocks against build_clamped_pieces (active bonds)
     b = bonds_from(d, f"{tag}_b_")
     act = np.nonzero(b.status != 2)[0]
-    st = dev.stage.cpu().numpy()
+    st = dev.stage.cpu().numpy()[:, dev.sell.pos_of_bond]
     apos = _sym6_to_mat(st[L.ST["APOS"]:L.ST["APOS"] + 6].T[act])
     want_pp = d[f"{tag}_bond_pp"]
     hs = np.abs(want_pp).max()
@@ -181,13 +181,13 @@ def test_assembly_vs_golden(cuda_ok, tag):
     _assert_close(D, rot[:, 3:, 3:], 1e-9, 1e-11 * hr, "rot (jj)")
     _assert_close(Cb, rot[:, :3, 3:], 1e-9, 1e-11 * hr, "rot (ij)")
     # diagonal blocks and block-Jacobi inverses
-    diag = dev.diag[:dev.nf].cpu().numpy()
+    diag = dev.diag[:, :dev.nf].cpu().numpy().T
     P, R = _sym6_to_mat(diag[:, :6]), _sym6_to_mat(diag[:, 6:])
     want = d[f"{tag}_diag"]
     sc = np.abs(want).max()
     _assert_close(P, want[:, :3, :3], 1e-9, 1e-11 * sc, "diag pos")
     _assert_close(R, want[:, 3:, 3:], 1e-9, 1e-11 * sc, "diag rot")
-    minv = dev.minv[:dev.nf].cpu().numpy()
+    minv = dev.minv[:, :dev.nf].cpu().numpy().T
     wm = d[f"{tag}_minv"]
     _assert_close(_sym6_to_mat(minv[:, :6]), wm[:, :3, :3], 1e-7, 1e-9 * np.abs(wm).max(), "Pinv")
     _assert_close(_sym6_to_mat(minv[:, 6:]), wm[:, 3:, 3:], 1e-7, 1e-9 * np.abs(wm).max(), "Rinv")
