@@ -180,23 +180,6 @@ __global__ void __launch_bounds__(kSpmvThreads, BDEM_SPMV_MINB) k_spmv(bdem_syst
 #pragma unroll 1
   for (int sl = s_begin; sl < s_end; sl += step) {
     const SliceBounds cb = slice_bounds(S, sl, ns);
-    // tail operands (component c = w of this slice's rows), issued before the
-    // slot loads so their latency overlaps
-    const int64_t e = (int64_t)sl * 32 + lane;
-    int s = -1;
-    double dgr[3] = {0.0, 0.0, 0.0}, xs[3] = {0.0, 0.0, 0.0};
-    const int c = w, base = c < 3 ? 0 : 3, rr = c - base;
-    if (w < 6 && e < S.n_elem) {
-      s = __ldg(S.slot + e);
-      if (s >= 0) {
-        const double *dg = S.diag + (c < 3 ? 0 : 6 * nf);
-#pragma unroll
-        for (int t = 0; t < 3; ++t) {
-          xs[t] = __ldg(x + 6 * (int64_t)s + base + t);
-          dgr[t] = __ldg(dg + sidx<3>(rr, t) * nf + s);
-        }
-      }
-    }
     double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll 1
     for (int k = w; k < cb.ki + cb.kj; k += kSpmvWarps)
@@ -204,35 +187,48 @@ __global__ void __launch_bounds__(kSpmvThreads, BDEM_SPMV_MINB) k_spmv(bdem_syst
 #pragma unroll
     for (int q = 0; q < 6; ++q) part[w][q][lane] = acc[q];
     __syncthreads();
+    // component c of y for the 32 rows of this slice (c = w, w + W, ...)
+    const int64_t e = (int64_t)sl * 32 + lane;
+    const int s = e < S.n_elem ? __ldg(S.slot + e) : -1;
     if (s >= 0) {
-      double yc = (dgr[0] * xs[0] + dgr[1] * xs[1]) + dgr[2] * xs[2];
+      for (int c = w; c < 6; c += kSpmvWarps) {
+        const int base = c < 3 ? 0 : 3, rr = c - base;
+        const double *dg = S.diag + (c < 3 ? 0 : 6 * nf);
+        double xs[3], dgr[3];
 #pragma unroll
-      for (int ww = 0; ww < kSpmvWarps; ++ww) yc += part[ww][c][lane];
-      if (c < 3 && S.n_pair > 0) {
-        const int64_t pc = S.pair_cap;
-        const double *ps = S.pstage;
-        for (int k = S.pi_ptr[e]; k < S.pi_ptr[e + 1]; ++k) {
-          const int o = S.slot[S.pair_j[k]];
-          if (o < 0) continue;
-          yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[6 * (int64_t)o] +
-                 ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[6 * (int64_t)o + 1]) +
-                ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[6 * (int64_t)o + 2];
+        for (int t = 0; t < 3; ++t) {
+          xs[t] = __ldg(x + 6 * (int64_t)s + base + t);
+          dgr[t] = __ldg(dg + sidx<3>(rr, t) * nf + s);
         }
-        for (int kk = S.pj_ptr[e]; kk < S.pj_ptr[e + 1]; ++kk) {
-          const int64_t k = S.pj_idx[kk];
-          const int o = S.slot[S.pair_i[k]];
-          if (o < 0) continue;
-          yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[6 * (int64_t)o] +
-                 ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[6 * (int64_t)o + 1]) +
-                ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[6 * (int64_t)o + 2];
+        double yc = (dgr[0] * xs[0] + dgr[1] * xs[1]) + dgr[2] * xs[2];
+#pragma unroll
+        for (int ww = 0; ww < kSpmvWarps; ++ww) yc += part[ww][c][lane];
+        if (c < 3 && S.n_pair > 0) {
+          const int64_t pc = S.pair_cap;
+          const double *ps = S.pstage;
+          for (int k = S.pi_ptr[e]; k < S.pi_ptr[e + 1]; ++k) {
+            const int o = S.slot[S.pair_j[k]];
+            if (o < 0) continue;
+            yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[6 * (int64_t)o] +
+                   ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[6 * (int64_t)o + 1]) +
+                  ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[6 * (int64_t)o + 2];
+          }
+          for (int kk = S.pj_ptr[e]; kk < S.pj_ptr[e + 1]; ++kk) {
+            const int64_t k = S.pj_idx[kk];
+            const int o = S.slot[S.pair_i[k]];
+            if (o < 0) continue;
+            yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[6 * (int64_t)o] +
+                   ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[6 * (int64_t)o + 1]) +
+                  ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[6 * (int64_t)o + 2];
+          }
         }
+        const double xc = xs[rr];
+        if (boost != 0.0) yc = yc + boost * xc;
+        y[6 * (int64_t)s + c] = yc;
+        acc_xy += xc * yc;
+        acc_yy += yc * yc;
+        acc_xx += xc * xc;
       }
-      const double xc = xs[rr];
-      if (boost != 0.0) yc = yc + boost * xc;
-      y[6 * (int64_t)s + c] = yc;
-      acc_xy += xc * yc;
-      acc_yy += yc * yc;
-      acc_xx += xc * xc;
     }
     __syncthreads();
   }
