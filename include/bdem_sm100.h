@@ -20,8 +20,9 @@
  *  - Layouts: p (n,3), q (n,4) scalar-last row-major like the reference;
  *    per-bond data in structure-of-arrays planes of length n_bond, indexed
  *    by SELL-32 position (see bdem_system_t); per-free-element blocks in
- *    planes of length n_free.
- *    Reduced vectors hold 6 doubles per free element [pos(3), rot(3)].
+ *    planes of stride vstride.  Reduced vectors (z, y, PCG x/r/z/p/Ap) are
+ *    6 planes [pos x,y,z, rot x,y,z] of stride vstride: component c of free
+ *    slot s is v[c * vstride + s].
  */
 #ifndef BDEM_SM100_H
 #define BDEM_SM100_H
@@ -144,6 +145,8 @@ enum {
 typedef struct {
   /* sizes */
   int64_t n_elem, n_free, n_bond, n_pair, pair_cap;
+  int64_t vstride;               /* plane stride of reduced vectors and diag/minv:
+                                    n_free rounded up to 32 (256-B aligned planes) */
   /* element data (device) */
   const double *mass, *radius;
   const double *mp_dt2, *mq_dt2; /* m/dt^2, 1.6 m r^2/dt^2; 0 when pinned */

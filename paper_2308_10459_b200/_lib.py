@@ -41,7 +41,7 @@ class Collider(C.Structure):
 class System(C.Structure):
     _fields_ = [
         ("n_elem", C.c_int64), ("n_free", C.c_int64), ("n_bond", C.c_int64),
-        ("n_pair", C.c_int64), ("pair_cap", C.c_int64),
+        ("n_pair", C.c_int64), ("pair_cap", C.c_int64), ("vstride", C.c_int64),
         ("mass", _p), ("radius", _p), ("mp_dt2", _p), ("mq_dt2", _p), ("p_hat", _p),
         ("q_hat", _p), ("slot", _p), ("free_elem", _p),
         ("bond_i", _p), ("bond_j", _p), ("status", _p), ("geom", _p), ("bstate", _p),

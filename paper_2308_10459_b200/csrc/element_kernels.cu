@@ -193,9 +193,9 @@ __global__ void __launch_bounds__(kThreads) k_element_assemble(bdem_system_t S, 
       // reduced gradient (solver.py:116-123)
       double zr[3];
       gl_apply(qe, gq, zr);
-      double *zs = z + 6 * (int64_t)s;
-      zs[0] = gp[0]; zs[1] = gp[1]; zs[2] = gp[2];
-      zs[3] = zr[0]; zs[4] = zr[1]; zs[5] = zr[2];
+      const int64_t nf6 = S.vstride;
+      z[0 * nf6 + s] = gp[0]; z[1 * nf6 + s] = gp[1]; z[2 * nf6 + s] = gp[2];
+      z[3 * nf6 + s] = zr[0]; z[4 * nf6 + s] = zr[1]; z[5 * nf6 + s] = zr[2];
       acc_g2 += (((gp[0] * gp[0] + gp[1] * gp[1]) + gp[2] * gp[2]) +
                  ((zr[0] * zr[0] + zr[1] * zr[1]) + zr[2] * zr[2]));
       const double qq = ((qe[0] * qe[0] + qe[1] * qe[1]) + qe[2] * qe[2]) + qe[3] * qe[3];
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kThreads) k_element_assemble(bdem_system_t S, 
 #pragma unroll
       for (int t = 0; t < 6; ++t) P[t] += Ep[t];
       R[0] += erot; R[3] += erot; R[5] += erot;
-      const int64_t nf = S.n_free;
+      const int64_t nf = S.vstride;
       double *dg = S.diag + s;
       double *mi = S.minv + s;
 #pragma unroll
@@ -357,13 +357,13 @@ __global__ void k_direction(bdem_system_t S, const double *q, const double *y, d
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= S.n_free) return;
   const int64_t e = S.free_elem[s];
-  const double *ys = y + 6 * s;
+  const int64_t nf = S.vstride;
   double qe[4], yr[3], w[4];
   load_q(q, e, qe);
 #pragma unroll
-  for (int c = 0; c < 3; ++c) dp[3 * e + c] = sign * ys[c];
+  for (int c = 0; c < 3; ++c) dp[3 * e + c] = sign * y[c * nf + s];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) yr[c] = sign * ys[3 + c];
+  for (int c = 0; c < 3; ++c) yr[c] = sign * y[(3 + c) * nf + s];
   glt_apply(qe, yr, w);
   store_q(dq, e, w);
 }

@@ -24,21 +24,20 @@ enum { CNT_SPMV = 2, CNT_UPDATE = 3, CNT_INIT = 4 };
 // partial-sum columns of sys->red owned by PCG (disjoint from BDEM_SC_*)
 enum { RC_PAP = 20, RC_AP2 = 21, RC_PP2 = 22, RC_RR = 23, RC_RZ = 24, RC_IRR = 25, RC_IRZ = 26 };
 
-__device__ __forceinline__ void load6(const double *x, int64_t s, double v[6]) {
-  const double2 *x2 = reinterpret_cast<const double2 *>(x + 6 * s);
-  const double2 a = x2[0], b = x2[1], c = x2[2];
-  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = c.x; v[5] = c.y;
+// reduced vectors are 6 planes of stride vstride: component c of slot s at
+// x[c * vstride + s], so a warp touching 32 consecutive slots reads 256 contiguous
+// bytes per component
+__device__ __forceinline__ void load6(const double *x, int64_t s, int64_t nf, double v[6]) {
+#pragma unroll
+  for (int c = 0; c < 6; ++c) v[c] = x[c * nf + s];
 }
-__device__ __forceinline__ void load6_ro(const double *x, int64_t s, double v[6]) {
-  const double2 *x2 = reinterpret_cast<const double2 *>(x + 6 * s);
-  const double2 a = __ldg(x2), b = __ldg(x2 + 1), c = __ldg(x2 + 2);
-  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = c.x; v[5] = c.y;
+__device__ __forceinline__ void load6_ro(const double *x, int64_t s, int64_t nf, double v[6]) {
+#pragma unroll
+  for (int c = 0; c < 6; ++c) v[c] = __ldg(x + c * nf + s);
 }
-__device__ __forceinline__ void store6(double *x, int64_t s, const double v[6]) {
-  double2 *x2 = reinterpret_cast<double2 *>(x + 6 * s);
-  x2[0] = make_double2(v[0], v[1]);
-  x2[1] = make_double2(v[2], v[3]);
-  x2[2] = make_double2(v[4], v[5]);
+__device__ __forceinline__ void store6(double *x, int64_t s, int64_t nf, const double v[6]) {
+#pragma unroll
+  for (int c = 0; c < 6; ++c) x[c * nf + s] = v[c];
 }
 
 __device__ __forceinline__ void load_sym(const double *planes, int64_t s, int64_t nf, double v[6]) {
@@ -48,7 +47,7 @@ __device__ __forceinline__ void load_sym(const double *planes, int64_t s, int64_
 
 __device__ __forceinline__ void precond_row(const bdem_system_t &S, int64_t s, const double r[6],
                                             double z[6]) {
-  const int64_t nf = S.n_free;
+  const int64_t nf = S.vstride;
   double mp[6], mr[6];
   load_sym(S.minv, s, nf, mp);
   load_sym(S.minv + 6 * nf, s, nf, mr);
@@ -108,7 +107,7 @@ __device__ __forceinline__ void slot_apply(const bdem_system_t &S, const double 
   const int64_t nb = S.n_bond;
   const double *st = S.stage;
   double xo[6], a[6], C[9];
-  load6_ro(x, r.o, xo);
+  load6_ro(x, r.o, S.vstride, xo);
 #pragma unroll
   for (int t = 0; t < 6; ++t) a[t] = __ldg(st + (BDEM_ST_APOS + t) * nb + r.b);
 #pragma unroll
@@ -164,7 +163,7 @@ __global__ void __launch_bounds__(kSpmvThreads, BDEM_SPMV_MINB) k_spmv(bdem_syst
   if (mode == 1 && pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
   const double boost = mode == 1 ? pcg[BDEM_PCG_BOOST] : 0.0;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t nf = S.n_free;
+  const int64_t nf = S.vstride;
   const int ns = (int)((S.n_elem + 31) >> 5);
   double acc_xy = 0.0, acc_yy = 0.0, acc_xx = 0.0;
 #if BDEM_SPMV_BLOCKED
@@ -197,7 +196,7 @@ __global__ void __launch_bounds__(kSpmvThreads, BDEM_SPMV_MINB) k_spmv(bdem_syst
         double xs[3], dgr[3];
 #pragma unroll
         for (int t = 0; t < 3; ++t) {
-          xs[t] = __ldg(x + 6 * (int64_t)s + base + t);
+          xs[t] = __ldg(x + (base + t) * nf + s);
           dgr[t] = __ldg(dg + sidx<3>(rr, t) * nf + s);
         }
         double yc = (dgr[0] * xs[0] + dgr[1] * xs[1]) + dgr[2] * xs[2];
@@ -209,22 +208,22 @@ __global__ void __launch_bounds__(kSpmvThreads, BDEM_SPMV_MINB) k_spmv(bdem_syst
           for (int k = S.pi_ptr[e]; k < S.pi_ptr[e + 1]; ++k) {
             const int o = S.slot[S.pair_j[k]];
             if (o < 0) continue;
-            yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[6 * (int64_t)o] +
-                   ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[6 * (int64_t)o + 1]) +
-                  ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[6 * (int64_t)o + 2];
+            yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[0 * nf + o] +
+                   ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[1 * nf + o]) +
+                  ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[2 * nf + o];
           }
           for (int kk = S.pj_ptr[e]; kk < S.pj_ptr[e + 1]; ++kk) {
             const int64_t k = S.pj_idx[kk];
             const int o = S.slot[S.pair_i[k]];
             if (o < 0) continue;
-            yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[6 * (int64_t)o] +
-                   ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[6 * (int64_t)o + 1]) +
-                  ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[6 * (int64_t)o + 2];
+            yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[0 * nf + o] +
+                   ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[1 * nf + o]) +
+                  ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[2 * nf + o];
           }
         }
         const double xc = xs[rr];
         if (boost != 0.0) yc = yc + boost * xc;
-        y[6 * (int64_t)s + c] = yc;
+        y[c * nf + s] = yc;
         acc_xy += xc * yc;
         acc_yy += yc * yc;
         acc_xx += xc * xc;
@@ -258,7 +257,10 @@ __global__ void __launch_bounds__(kSpmvThreads, BDEM_SPMV_MINB) k_spmv(bdem_syst
 }
 
 // x += alpha p; r -= alpha Ap; z = M^-1 r; r.r, r.z (linalg.py:79-89)
-__global__ void __launch_bounds__(kThreads) k_pcg_update(bdem_system_t S, double *x, double *r,
+#ifndef BDEM_UPD_MINB
+#define BDEM_UPD_MINB 4
+#endif
+__global__ void __launch_bounds__(kThreads, BDEM_UPD_MINB) k_pcg_update(bdem_system_t S, double *x, double *r,
                                                          double *zv, const double *p,
                                                          const double *ap) {
   __shared__ double sh[kThreads / 32];
@@ -266,25 +268,51 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(bdem_system_t S, double
   if (pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
   const double alpha = pcg[BDEM_PCG_ALPHA];
   double acc_rr = 0.0, acc_rz = 0.0;
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < S.n_free;
-       s += (int64_t)gridDim.x * blockDim.x) {
-    double xs[6], rs[6], ps[6], aps[6], zs[6];
-    load6(x, s, xs);
-    load6(r, s, rs);
-    load6(p, s, ps);
-    load6(ap, s, aps);
+  // two consecutive slots per thread with 16-byte loads (planes are 256-B
+  // aligned, stride vstride); padding slots carry zeros and stay zero
+  const int64_t nf = S.vstride;
+  const double2 *p2 = reinterpret_cast<const double2 *>(p);
+  const double2 *ap2 = reinterpret_cast<const double2 *>(ap);
+  double2 *x2 = reinterpret_cast<double2 *>(x);
+  double2 *r2 = reinterpret_cast<double2 *>(r);
+  double2 *z2 = reinterpret_cast<double2 *>(zv);
+  const double2 *mi2 = reinterpret_cast<const double2 *>(S.minv);
+  const int64_t h2 = nf >> 1;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < h2;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    // position half (components 0..2, P^-1) then rotation half (3..5, R^-1)
 #pragma unroll
-    for (int c = 0; c < 6; ++c) {
-      xs[c] = xs[c] + alpha * ps[c];
-      rs[c] = rs[c] - alpha * aps[c];
-      acc_rr += rs[c] * rs[c];
+    for (int h = 0; h < 2; ++h) {
+      double ra[3], rb[3], ma[6], mb[6], za[3], zb[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int64_t k = (3 * h + c) * h2 + t;
+        const double2 xv = x2[k], rv = r2[k], pv = p2[k], av = ap2[k];
+        x2[k] = make_double2(xv.x + alpha * pv.x, xv.y + alpha * pv.y);
+        ra[c] = rv.x - alpha * av.x;
+        rb[c] = rv.y - alpha * av.y;
+        r2[k] = make_double2(ra[c], rb[c]);
+      }
+#pragma unroll
+      for (int tt = 0; tt < 6; ++tt) {
+        const double2 m = mi2[(6 * h + tt) * h2 + t];
+        ma[tt] = m.x;
+        mb[tt] = m.y;
+      }
+      symv3(ma, ra, za);
+      symv3(mb, rb, zb);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        z2[(3 * h + c) * h2 + t] = make_double2(za[c], zb[c]);
+        acc_rr += ra[c] * ra[c];
+        acc_rz += ra[c] * za[c];
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        acc_rr += rb[c] * rb[c];
+        acc_rz += rb[c] * zb[c];
+      }
     }
-    store6(x, s, xs);
-    store6(r, s, rs);
-    precond_row(S, s, rs, zs);
-    store6(zv, s, zs);
-#pragma unroll
-    for (int c = 0; c < 6; ++c) acc_rz += rs[c] * zs[c];
   }
   double v = block_sum<kThreads>(acc_rr, sh);
   if (threadIdx.x == 0) *red_slot(S.red, RC_RR, blockIdx.x) = v;
@@ -315,10 +343,14 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(bdem_system_t S, doubl
   const double *pcg = S.pcg;
   if (pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
   const double beta = pcg[BDEM_PCG_BETA];
-  const int64_t n6 = 6 * S.n_free;
+  const int64_t n6 = 3 * S.vstride;  // double2 units over 6 planes
+  double2 *p2 = reinterpret_cast<double2 *>(p);
+  const double2 *z2 = reinterpret_cast<const double2 *>(zv);
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n6;
-       k += (int64_t)gridDim.x * blockDim.x)
-    p[k] = zv[k] + beta * p[k];
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const double2 zz = z2[k], pp = p2[k];
+    p2[k] = make_double2(zz.x + beta * pp.x, zz.y + beta * pp.y);
+  }
 }
 
 // x = 0, r = sign b, z = M^-1 r, p = z, r.z, |b| (linalg.py:52-68)
@@ -332,17 +364,17 @@ __global__ void __launch_bounds__(kThreads) k_pcg_init(bdem_system_t S, const do
        s += (int64_t)gridDim.x * blockDim.x) {
     double bs[6], zs[6];
     const double zero[6] = {0, 0, 0, 0, 0, 0};
-    load6(b, s, bs);
+    load6(b, s, S.vstride, bs);
 #pragma unroll
     for (int c = 0; c < 6; ++c) {
       bs[c] = sign * bs[c];
       acc_rr += bs[c] * bs[c];
     }
-    store6(x, s, zero);
-    store6(r, s, bs);
+    store6(x, s, S.vstride, zero);
+    store6(r, s, S.vstride, bs);
     precond_row(S, s, bs, zs);
-    store6(zv, s, zs);
-    store6(p, s, zs);
+    store6(zv, s, S.vstride, zs);
+    store6(p, s, S.vstride, zs);
 #pragma unroll
     for (int c = 0; c < 6; ++c) acc_rz += bs[c] * zs[c];
   }
@@ -372,9 +404,9 @@ __global__ void k_precond(bdem_system_t S, const double *r, double *zv) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= S.n_free) return;
   double rs[6], zs[6];
-  load6(r, s, rs);
+  load6(r, s, S.vstride, rs);
   precond_row(S, s, rs, zs);
-  store6(zv, s, zs);
+  store6(zv, s, S.vstride, zs);
 }
 
 // self_repulsion_terms + clamp of the pair block (contact.py:180-224, solver.py:162)

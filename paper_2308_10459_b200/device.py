@@ -172,9 +172,12 @@ class DeviceSystem:
         self.pos_of_bond_d = torch.as_tensor(sell.pos_of_bond).to(dev)
         # staging / reduced system
         self.stage = torch.zeros((L.ST["COUNT"], npos), dtype=F64, device=dev)
-        self.diag = torch.zeros((12, max(nf, 1)), dtype=F64, device=dev)
-        self.minv = torch.zeros((12, max(nf, 1)), dtype=F64, device=dev)
-        v6 = lambda: torch.zeros(max(6 * nf, 6), dtype=F64, device=dev)  # noqa: E731
+        # reduced vectors / diagonal blocks: planes of stride vstride (n_free
+        # rounded up to 32 -> 256-byte aligned planes, zero padding)
+        self.vstride = vs = max(32, (nf + 31) // 32 * 32)
+        self.diag = torch.zeros((12, vs), dtype=F64, device=dev)
+        self.minv = torch.zeros((12, vs), dtype=F64, device=dev)
+        v6 = lambda: torch.zeros(6 * vs, dtype=F64, device=dev)  # noqa: E731
         self.z, self.y, self.r, self.zv, self.pv, self.ap = v6(), v6(), v6(), v6(), v6(), v6()
         self.red = torch.zeros((L.SC["COUNT"], L.RED_BLOCKS), dtype=F64, device=dev)
         self.scalars = torch.zeros(L.SC["COUNT"], dtype=F64, device=dev)
@@ -196,6 +199,7 @@ class DeviceSystem:
         self.sys = L.System()
         s = self.sys
         s.n_elem, s.n_free, s.n_bond = n, nf, (sell.n_pos if nb else 0)
+        s.vstride = self.vstride
         s.mass, s.radius = _ptr(self.mass), _ptr(self.radius)
         s.mp_dt2, s.mq_dt2 = _ptr(self.mp_dt2), _ptr(self.mq_dt2)
         s.p_hat, s.q_hat = _ptr(self.p_hat), _ptr(self.q_hat)

@@ -239,7 +239,7 @@ def minimize_second_order(problem: GPUProblem, p0, q0, cfg: SolverConfig) -> Sol
     pcg_total = 0
     gnorm = math.inf
     max_dev = 0.0
-    nf6 = 6 * d.nf
+    nf6 = 6 * d.vstride
     last_checked = True
     for it in range(cfg.max_iterations):
         f, gnorm, cnorm, dev_it = problem.assemble(p, q)

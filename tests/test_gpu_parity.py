@@ -143,6 +143,20 @@ def _gpu_problem(d, tag):
     return dev, GPUProblem(dev)
 
 
+def _aos(t, dev):
+    """Reduced device vector (6 planes of stride vstride) -> 6 per slot."""
+    vs, nf = dev.vstride, dev.nf
+    return t[:6 * vs].reshape(6, vs)[:, :nf].T.reshape(-1).cpu().numpy()
+
+
+def _soa(a, dev):
+    import torch
+    vs, nf = dev.vstride, dev.nf
+    out = np.zeros((6, vs))
+    out[:, :nf] = a.reshape(nf, 6).T
+    return torch.from_numpy(out).reshape(-1).cuda()
+
+
 def _sym6_to_mat(s):
     m = np.empty(s.shape[:-1] + (3, 3))
     idx = [(0, 0, 0), (1, 0, 1), (2, 0, 2), (3, 1, 1), (4, 1, 2), (5, 2, 2)]
@@ -161,7 +175,7 @@ def test_assembly_vs_golden(cuda_ok, tag):
     f, gnorm, cnorm, _ = prob.assemble(dev.xp, dev.xq)
     assert f == pytest.approx(float(d[f"{tag}_f"]), rel=1e-12)
     assert gnorm == pytest.approx(float(d[f"{tag}_gnorm"]), rel=1e-10)
-    z = dev.z[:6 * dev.nf].cpu().numpy()
+    z = _aos(dev.z, dev)
     _assert_close(z, d[f"{tag}_z"], 1e-9, 1e-11 * np.abs(z).max(), "z")
     # clamped bond blocks against build_clamped_pieces (active bonds)
     b = bonds_from(d, f"{tag}_b_")
@@ -195,20 +209,20 @@ def test_assembly_vs_golden(cuda_ok, tag):
     Adense = d[f"{tag}_A"]
     rng = np.random.default_rng(3)
     x = rng.normal(size=Adense.shape[0])
-    xd = torch.from_numpy(x).cuda()
+    xd = _soa(x, dev)
     yd = torch.zeros_like(xd)
     dev.call("bdem_spmv", dev.sysp, xd.data_ptr(), yd.data_ptr(), dev.stream)
     want_y = Adense @ x
-    _assert_close(yd.cpu().numpy(), want_y, 1e-9, 1e-11 * np.abs(want_y).max(), "A x")
+    _assert_close(_aos(yd, dev), want_y, 1e-9, 1e-11 * np.abs(want_y).max(), "A x")
     # PCG at the reference's inner tolerance
     res = prob.solve_pcg(float(d[f"{tag}_pcg_tol"]), 2000)
     assert abs(res.iterations - int(d[f"{tag}_pcg_it"])) <= 1
-    y = dev.y[:6 * dev.nf].cpu().numpy()
+    y = _aos(dev.y, dev)
     if res.iterations == int(d[f"{tag}_pcg_it"]):
         _assert_close(y, d[f"{tag}_pcg_x"], 1e-6, 1e-8 * np.abs(y).max(), "pcg x")
     # tight solve is path independent: compare to the exact solution
     res = prob.solve_pcg(1e-10, 2000)
-    y = dev.y[:6 * dev.nf].cpu().numpy()
+    y = _aos(dev.y, dev)
     _assert_close(y, d[f"{tag}_pcg_tight_x"], 1e-7, 1e-9 * np.abs(y).max(), "tight pcg x")
     # objective value at the iterate
     val = prob.value(dev.xp, dev.xq)
