@@ -192,6 +192,18 @@ class ClockSampler:
 # GPU arm
 # ---------------------------------------------------------------------------
 
+def reduce_across_ranks(times_ms, counts, world, device):
+    """Replica aggregation: device times -> max over ranks, work -> sum."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(times_ms, dtype=torch.float64, device=device)
+    c = torch.tensor(counts, dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+    return [float(v) for v in t], [float(v) for v in c]
+
+
 def spmv_bytes(dev):
     """Algorithmic bytes of one SpMV in this library's format:
     per bond with both ends free: a+ (6) + C (9) fp64 read once = 120 B, plus
@@ -291,13 +303,8 @@ def run_ours(args):
     h2d = dev.n * (3 + 4 + 3 + 4 + 3 + 4) * 8 + dev.nb * (5 * 8 + 1)
     d2h = h2d
 
-    ms_t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device="cuda")
-    cnt_t = torch.tensor([stats["newton"], e2e_newton], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(cnt_t, op=dist.ReduceOp.SUM)
-    ms_max, e2e_ms_max = float(ms_t[0]), float(ms_t[1])
-    newton_all, e2e_newton_all = float(cnt_t[0]), float(cnt_t[1])
+    (ms_max, e2e_ms_max), (newton_all, e2e_newton_all) = reduce_across_ranks(
+        [ms, e2e_ms], [stats["newton"], e2e_newton], world, "cuda")
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()

@@ -342,3 +342,83 @@ def test_broadphase_and_components_vs_golden(cuda_ok):
     b.i, b.j, b.status = d["lab_i"], d["lab_j"], d["lab_status"]
     lab = label_components(int(d["lab_n"]), b)
     assert np.array_equal(lab.labels, d["lab_labels"])
+
+
+def test_reference_minimizers_adapter(cuda_ok):
+    """integration.minimize_reference_problem accepts the reference's
+    ImplicitProblem shape (solver.py:834-840 MINIMIZERS seam) and reproduces
+    the reference's solution of the golden solve."""
+    from paper_2308_10459_b200 import HalfSpace, SolverConfig
+    from paper_2308_10459_b200.integration import minimize_reference_problem
+    d = load("newton_solve.npz")
+    el = elements_from(d, "el_")
+    b = bonds_from(d, "b_")
+    hs = d["hs"]
+    dt = float(d["dt"])
+
+    class Model:                      # PotentialModel fields (integrator.py:46-54)
+        pass
+    model = Model()
+    model.elements, model.bonds, model.pairs = el, b, d["pairs"]
+    model.colliders = [HalfSpace(tuple(hs[:3]), hs[3])]
+    model.gravity, model.k_contact, model.k_element = d["gravity"], float(d["kc"]), float(d["ke"])
+
+    class Ctx:                        # StepContext (integrator.py:141-161)
+        pass
+    ctx = Ctx()
+    ctx.p_hat = 2.0 * el.p - d["p_prev"]
+    ctx.q_hat = 2.0 * el.q - d["q_prev"]
+
+    class Problem:                    # ImplicitProblem (integrator.py:164-210)
+        free = ~el.pinned
+
+        def inertia_diag(self):
+            mp = np.where(self.free, el.mass / dt**2, 0.0)
+            mq = np.where(self.free, 1.6 * el.mass * el.radius**2 / dt**2, 0.0)
+            return mp, mq
+    prob = Problem()
+    prob.model, prob.ctx = model, ctx
+    res = minimize_reference_problem(prob, d["p0"], d["q0"],
+                                     SolverConfig(epsilon=float(d["epsilon"]),
+                                                  max_iterations=200))
+    assert res.converged and isinstance(res.p, np.ndarray)
+    atol = 10 * float(d["epsilon"]) / (el.mass / dt**2).min()
+    _assert_close(res.p, d["solve_p"], 1e-8, atol, "p")
+
+
+def test_spmv_matches_oracle_csr_random_q(cuda_ok):
+    """Reduced matrix-vector product on a 22^3 random-q cube (every rotation
+    block indefinite -> Jacobi clamp) against the oracle's assembled CSR."""
+    import torch
+    from oracle import cpu_oracle as O
+    from paper_2308_10459_b200 import configs as C
+    from paper_2308_10459_b200.device import DeviceSystem
+    from paper_2308_10459_b200.newton import GPUProblem
+    spec = C.cube(seed=13, random_q=True)
+    el, b = spec.elements, spec.bonds
+    rng = np.random.default_rng(13)
+    el.v[:] = 0.05 * rng.normal(size=el.v.shape)
+    dev = DeviceSystem(elements=el, bonds=b)
+    dev.set_physics(spec.gravity, spec.k_contact, 0.0, spec.colliders)
+    p_prev = el.p - spec.dt * el.v
+    dev.p_prev.copy_(torch.from_numpy(p_prev))
+    dev.q_prev.copy_(torch.from_numpy(el.q))
+    dev.call("bdem_predict", dev.sysp, dev.p.data_ptr(), dev.q.data_ptr(), dev.v.data_ptr(),
+             dev.qdot.data_ptr(), dev.p_prev.data_ptr(), dev.q_prev.data_ptr(), spec.dt,
+             dev.p_hat.data_ptr(), dev.q_hat.data_ptr(), dev.mp_dt2.data_ptr(),
+             dev.mq_dt2.data_ptr(), dev.xp.data_ptr(), dev.xq.data_ptr(), dev.stream)
+    prob = GPUProblem(dev)
+    f, gnorm, _, _ = prob.assemble(dev.xp, dev.xq)
+    obj = O.Objective(el, b, np.zeros((0, 2), dtype=np.int64), spec.colliders, spec.gravity,
+                      spec.k_contact, 0.0, spec.dt, p_prev, el.q.copy(), el.p.copy(), el.q.copy())
+    p, q = dev.xp.cpu().numpy(), dev.xq.cpu().numpy()
+    fo, gp, gq = obj.value_and_gradient(p, q)
+    assert f == pytest.approx(fo, rel=1e-11)
+    pc = O.clamped_pieces(obj, p, q, gq)
+    mat, _ = O.reduced_system(pc, obj.free)
+    x = rng.normal(size=mat.shape[0])
+    xd = _soa(x, dev)
+    yd = torch.zeros_like(xd)
+    dev.call("bdem_spmv", dev.sysp, xd.data_ptr(), yd.data_ptr(), dev.stream)
+    want = mat @ x
+    _assert_close(_aos(yd, dev), want, 1e-9, 1e-10 * np.abs(want).max(), "A x (random q)")
