@@ -55,6 +55,88 @@ __device__ __forceinline__ void precond_row(const bdem_system_t &S, int64_t s, c
   symv3(mr, r + 3, z + 3);
 }
 
+// component c (= w, w + W, ...) of y for the 32 rows of slice sl:
+// y = D x + sum of the staged slot partials (fixed order) - pair couplings
+template <int W>
+__device__ __forceinline__ void spmv_tail(const bdem_system_t &S, const double *x, double *y,
+                                          int sl, int w, int lane, const double (*part)[6][32],
+                                          double boost, double &acc_xy, double &acc_yy,
+                                          double &acc_xx) {
+  const int64_t nf = S.vstride;
+  const int64_t e = (int64_t)sl * 32 + lane;
+  const int s = e < S.n_elem ? __ldg(S.slot + e) : -1;
+  if (s < 0) return;
+  for (int c = w; c < 6; c += W) {
+    const int base = c < 3 ? 0 : 3, rr = c - base;
+    const double *dg = S.diag + (c < 3 ? 0 : 6 * nf);
+    double xs[3], dgr[3];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      xs[t] = __ldg(x + (base + t) * nf + s);
+      dgr[t] = __ldg(dg + sidx<3>(rr, t) * nf + s);
+    }
+    double yc = (dgr[0] * xs[0] + dgr[1] * xs[1]) + dgr[2] * xs[2];
+#pragma unroll
+    for (int ww = 0; ww < W; ++ww) yc += part[ww][c][lane];
+    if (c < 3 && S.n_pair > 0) {
+      const int64_t pc = S.pair_cap;
+      const double *ps = S.pstage;
+      for (int k = S.pi_ptr[e]; k < S.pi_ptr[e + 1]; ++k) {
+        const int o = S.slot[S.pair_j[k]];
+        if (o < 0) continue;
+        yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[0 * nf + o] +
+               ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[1 * nf + o]) +
+              ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[2 * nf + o];
+      }
+      for (int kk = S.pj_ptr[e]; kk < S.pj_ptr[e + 1]; ++kk) {
+        const int64_t k = S.pj_idx[kk];
+        const int o = S.slot[S.pair_i[k]];
+        if (o < 0) continue;
+        yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[0 * nf + o] +
+               ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[1 * nf + o]) +
+              ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[2 * nf + o];
+      }
+    }
+    const double xc = xs[rr];
+    if (boost != 0.0) yc = yc + boost * xc;
+    y[c * nf + s] = yc;
+    acc_xy += xc * yc;
+    acc_yy += yc * yc;
+    acc_xx += xc * xc;
+  }
+}
+
+// PCG-mode epilogue shared by the SpMV kernels: per-block partials of p.Ap,
+// |Ap|^2, |p|^2; the last block sets alpha or flags breakdown (linalg.py:69-77)
+template <int NT>
+__device__ __forceinline__ void spmv_pcg_epilogue(const bdem_system_t &S, double boost,
+                                                  double acc_xy, double acc_yy, double acc_xx,
+                                                  double *sh) {
+  double *pcg = S.pcg;
+  double v = block_sum<NT>(acc_xy, sh);
+  if (threadIdx.x == 0) *red_slot(S.red, RC_PAP, blockIdx.x) = v;
+  v = block_sum<NT>(acc_yy, sh);
+  if (threadIdx.x == 0) *red_slot(S.red, RC_AP2, blockIdx.x) = v;
+  v = block_sum<NT>(acc_xx, sh);
+  if (threadIdx.x == 0) *red_slot(S.red, RC_PP2, blockIdx.x) = v;
+  if (!last_block(S.counter + CNT_SPMV)) return;
+  const double pap = sum_partials<NT>(S.red, RC_PAP, gridDim.x, sh);
+  const double ap2 = sum_partials<NT>(S.red, RC_AP2, gridDim.x, sh);
+  const double pp2 = sum_partials<NT>(S.red, RC_PP2, gridDim.x, sh);
+  if (threadIdx.x == 0) {
+    pcg[BDEM_PCG_PAP] = pap;
+    pcg[BDEM_PCG_APNORM2] = ap2;
+    pcg[BDEM_PCG_PNORM2] = pp2;
+    if (pap <= 0.0) {  // breakdown: boost for the restart (linalg.py:74-77)
+      const double sc = sqrt(ap2) / fmax(sqrt(pp2), 1e-300);
+      pcg[BDEM_PCG_BOOST] = fmax(boost * 100.0, 1e-10 * fmax(sc, 1.0));
+      pcg[BDEM_PCG_STATE] = PCG_BREAKDOWN;
+    } else {
+      pcg[BDEM_PCG_ALPHA] = pcg[BDEM_PCG_RZ] / pap;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // SpMV, slot-parallel form.  One CTA works on one 32-element slice at a time:
 // warp w takes slots w, w+8, ... of the slice's i-role and j-role lists
@@ -180,80 +262,24 @@ __global__ void __launch_bounds__(kSpmvThreads, BDEM_SPMV_MINB) k_spmv(bdem_syst
   for (int sl = s_begin; sl < s_end; sl += step) {
     const SliceBounds cb = slice_bounds(S, sl, ns);
     double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    // software pipeline on the (cheap, integer) slot indices: the next slot's
+    // index loads are in flight while this slot's coefficients arrive
+    const int kt = cb.ki + cb.kj;
+    SlotRef cur = slot_ref(S, cb.i0, cb.ki, cb.j0, cb.kj, lane, w);
 #pragma unroll 1
-    for (int k = w; k < cb.ki + cb.kj; k += kSpmvWarps)
-      slot_apply(S, x, slot_ref(S, cb.i0, cb.ki, cb.j0, cb.kj, lane, k), acc);
+    for (int k = w; k < kt; k += kSpmvWarps) {
+      const SlotRef nxt = slot_ref(S, cb.i0, cb.ki, cb.j0, cb.kj, lane, k + kSpmvWarps);
+      slot_apply(S, x, cur, acc);
+      cur = nxt;
+    }
 #pragma unroll
     for (int q = 0; q < 6; ++q) part[w][q][lane] = acc[q];
     __syncthreads();
-    // component c of y for the 32 rows of this slice (c = w, w + W, ...)
-    const int64_t e = (int64_t)sl * 32 + lane;
-    const int s = e < S.n_elem ? __ldg(S.slot + e) : -1;
-    if (s >= 0) {
-      for (int c = w; c < 6; c += kSpmvWarps) {
-        const int base = c < 3 ? 0 : 3, rr = c - base;
-        const double *dg = S.diag + (c < 3 ? 0 : 6 * nf);
-        double xs[3], dgr[3];
-#pragma unroll
-        for (int t = 0; t < 3; ++t) {
-          xs[t] = __ldg(x + (base + t) * nf + s);
-          dgr[t] = __ldg(dg + sidx<3>(rr, t) * nf + s);
-        }
-        double yc = (dgr[0] * xs[0] + dgr[1] * xs[1]) + dgr[2] * xs[2];
-#pragma unroll
-        for (int ww = 0; ww < kSpmvWarps; ++ww) yc += part[ww][c][lane];
-        if (c < 3 && S.n_pair > 0) {
-          const int64_t pc = S.pair_cap;
-          const double *ps = S.pstage;
-          for (int k = S.pi_ptr[e]; k < S.pi_ptr[e + 1]; ++k) {
-            const int o = S.slot[S.pair_j[k]];
-            if (o < 0) continue;
-            yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[0 * nf + o] +
-                   ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[1 * nf + o]) +
-                  ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[2 * nf + o];
-          }
-          for (int kk = S.pj_ptr[e]; kk < S.pj_ptr[e + 1]; ++kk) {
-            const int64_t k = S.pj_idx[kk];
-            const int o = S.slot[S.pair_i[k]];
-            if (o < 0) continue;
-            yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[0 * nf + o] +
-                   ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[1 * nf + o]) +
-                  ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[2 * nf + o];
-          }
-        }
-        const double xc = xs[rr];
-        if (boost != 0.0) yc = yc + boost * xc;
-        y[c * nf + s] = yc;
-        acc_xy += xc * yc;
-        acc_yy += yc * yc;
-        acc_xx += xc * xc;
-      }
-    }
+    spmv_tail<kSpmvWarps>(S, x, y, sl, w, lane, part, boost, acc_xy, acc_yy, acc_xx);
     __syncthreads();
   }
   if (mode == 0) return;
-  double v = block_sum<kSpmvThreads>(acc_xy, sh);
-  if (threadIdx.x == 0) *red_slot(S.red, RC_PAP, blockIdx.x) = v;
-  v = block_sum<kSpmvThreads>(acc_yy, sh);
-  if (threadIdx.x == 0) *red_slot(S.red, RC_AP2, blockIdx.x) = v;
-  v = block_sum<kSpmvThreads>(acc_xx, sh);
-  if (threadIdx.x == 0) *red_slot(S.red, RC_PP2, blockIdx.x) = v;
-  if (!last_block(S.counter + CNT_SPMV)) return;
-  const double pap = sum_partials<kSpmvThreads>(S.red, RC_PAP, gridDim.x, sh);
-  const double ap2 = sum_partials<kSpmvThreads>(S.red, RC_AP2, gridDim.x, sh);
-  const double pp2 = sum_partials<kSpmvThreads>(S.red, RC_PP2, gridDim.x, sh);
-  if (threadIdx.x == 0) {
-    pcg[BDEM_PCG_PAP] = pap;
-    pcg[BDEM_PCG_APNORM2] = ap2;
-    pcg[BDEM_PCG_PNORM2] = pp2;
-    if (pap <= 0.0) {  // breakdown: boost for the restart (linalg.py:74-77)
-      const double sc = sqrt(ap2) / fmax(sqrt(pp2), 1e-300);
-      pcg[BDEM_PCG_BOOST] = fmax(boost * 100.0, 1e-10 * fmax(sc, 1.0));
-      pcg[BDEM_PCG_STATE] = PCG_BREAKDOWN;
-    } else {
-      pcg[BDEM_PCG_ALPHA] = pcg[BDEM_PCG_RZ] / pap;
-    }
-  }
+  spmv_pcg_epilogue<kSpmvThreads>(S, boost, acc_xy, acc_yy, acc_xx, sh);
 }
 
 // x += alpha p; r -= alpha Ap; z = M^-1 r; r.r, r.z (linalg.py:79-89)
@@ -465,6 +491,13 @@ static unsigned int spmv_grid() {
   return g;
 }
 
+// one SpMV launch (plain or PCG mode) with the configured kernel
+static void launch_spmv(const bdem_system_t &S, const double *x, double *y, int mode,
+                        cudaStream_t st) {
+  const unsigned int g = spmv_grid();
+  k_spmv<<<g, kSpmvThreads, 0, st>>>(S, x, y, mode);
+}
+
 }  // namespace bdem
 
 using namespace bdem;
@@ -473,7 +506,7 @@ extern "C" {
 
 int bdem_spmv(const bdem_system_t *sys, const double *x, double *y, void *stream) {
   if (!sys) return BDEM_ERR_ARG;
-  k_spmv<<<spmv_grid(), kSpmvThreads, 0, as_stream(stream)>>>(*sys, x, y, 0);
+  launch_spmv(*sys, x, y, 0, as_stream(stream));
   return launch_status();
 }
 
@@ -498,7 +531,7 @@ int bdem_pcg_iterate(const bdem_system_t *sys, double *x, double *r, double *zv,
   if (!sys || n_iter < 0) return BDEM_ERR_ARG;
   cudaStream_t st = as_stream(stream);
   for (int it = 0; it < n_iter; ++it) {
-    k_spmv<<<spmv_grid(), kSpmvThreads, 0, st>>>(*sys, pv, ap, 1);
+    launch_spmv(*sys, pv, ap, 1, st);
     k_pcg_update<<<kRedBlocks, kThreads, 0, st>>>(*sys, x, r, zv, pv, ap);
     k_pcg_pupdate<<<kRedBlocks, kThreads, 0, st>>>(*sys, pv, zv);
   }
@@ -507,7 +540,7 @@ int bdem_pcg_iterate(const bdem_system_t *sys, double *x, double *r, double *zv,
 
 int bdem_pcg_spmv(const bdem_system_t *sys, const double *pv, double *ap, void *stream) {
   if (!sys) return BDEM_ERR_ARG;
-  k_spmv<<<spmv_grid(), kSpmvThreads, 0, as_stream(stream)>>>(*sys, pv, ap, 1);
+  launch_spmv(*sys, pv, ap, 1, as_stream(stream));
   return launch_status();
 }
 
