@@ -192,6 +192,30 @@ class ClockSampler:
 # GPU arm
 # ---------------------------------------------------------------------------
 
+def snapshot(scene):
+    """Host copy of everything a step reads (element + bond state, history)."""
+    import copy
+    scene.sync_to_host()
+    return {"el": scene.elements.copy(), "b": scene.bonds.copy(), "time": scene.time,
+            "p_prev": scene.p_prev.copy(), "q_prev": scene.q_prev.copy(),
+            "labels": copy.deepcopy(scene._labels)}
+
+
+def restore(scene, snap):
+    """Write a snapshot back into the scene's host arrays (in place)."""
+    for name in ("p", "q", "v", "qdot"):
+        getattr(scene.elements, name)[...] = getattr(snap["el"], name)
+    for name in scene.bonds.STATE_FIELDS:
+        getattr(scene.bonds, name)[...] = getattr(snap["b"], name)
+    scene.p_prev[...] = snap["p_prev"]
+    scene.q_prev[...] = snap["q_prev"]
+    scene.time = snap["time"]
+    if snap["labels"] is not None:
+        scene._labels = snap["labels"]
+        scene.device.labels = __import__("torch").as_tensor(snap["labels"].labels).to(
+            scene.device.device)
+
+
 def reduce_across_ranks(times_ms, counts, world, device):
     """Replica aggregation: device times -> max over ranks, work -> sum."""
     import torch
@@ -260,6 +284,7 @@ def run_ours(args):
 
     for _ in range(args.warmup):
         stable_step(scene, cfg)
+    snap = snapshot(scene)      # the e2e leg replays exactly the timed steps
 
     timer = KernelTimer()
     dev.timer = timer
@@ -285,9 +310,10 @@ def run_ours(args):
     durations = timer.resolve()
     dev.timer = None
 
-    # e2e through the same public call with host buffers every step
+    # e2e: the same steps again, from the same state, through the same public
+    # call with host buffers every step (H2D of the state before, D2H after)
     n_e2e = args.e2e_steps if args.e2e_steps is not None else args.steps
-    scene.sync_to_host()
+    restore(scene, snap)
     scene.host_sync = True
     e2e_newton = 0
     barrier()
@@ -339,6 +365,7 @@ def run_ours(args):
                      "peak_source": peak_kind,
                      "traffic": traffic.get("k_spmv", {}).get("dram_bytes_per_launch")},
         "e2e": {"value": e2e_newton_all / (e2e_ms_max * 1e-3) if n_e2e else None, "unit": UNIT,
+                "same_steps_as_value": True, "newton_iterations": e2e_newton,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n_e2e},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),

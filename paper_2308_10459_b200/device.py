@@ -19,6 +19,7 @@ Memory layout (HBM):
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 
 import numpy as np
 import torch
@@ -255,10 +256,45 @@ class DeviceSystem:
             self._pins[key] = buf
         return buf
 
+    def _host_view(self, arr, dtype):
+        """Torch view of a caller's numpy array in page-locked memory.
+
+        The array is registered with the CUDA driver once (cudaHostRegister),
+        so host<->HBM copies run directly on the caller's memory at PCIe
+        speed with no staging memcpy; registration is dropped when the array
+        is garbage collected.  Returns None for arrays that cannot be viewed
+        (wrong dtype, non-contiguous) -- callers then stage."""
+        if not isinstance(arr, np.ndarray) or arr.dtype != dtype or \
+                not arr.flags["C_CONTIGUOUS"] or arr.nbytes == 0:
+            return None
+        key = (arr.ctypes.data, arr.nbytes)
+        if key not in _REGISTERED:
+            rt = torch.cuda.cudart()
+            if int(rt.cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)) != 0:
+                return None
+            _REGISTERED[key] = True
+            weakref.finalize(arr.base if arr.base is not None else arr, _unregister, key)
+        return torch.from_numpy(arr)
+
     def _h2d(self, dst, src_np, key):
+        src = np.asarray(src_np)
+        view = self._host_view(src, np.float64 if dst.dtype == F64 else np.int8)
+        if view is not None and tuple(view.shape) == tuple(dst.shape):
+            dst.copy_(view, non_blocking=True)
+            return
         st = self._pinned(key, dst.shape, dst.dtype)
-        st.numpy()[...] = src_np
+        st.numpy()[...] = src
         dst.copy_(st, non_blocking=True)
+
+    def _d2h_into(self, dst_np, src):
+        """Queue an HBM -> host copy into the caller's array (synchronise later)."""
+        view = self._host_view(dst_np, np.float64 if src.dtype == F64 else np.int8)
+        if view is not None and tuple(view.shape) == tuple(src.shape):
+            view.copy_(src, non_blocking=True)
+            return None
+        st = self._pinned(("out",) + tuple(src.shape) + (str(src.dtype),), src.shape, src.dtype)
+        st.copy_(src, non_blocking=True)
+        return (dst_np, st)
 
     def _d2h(self, src, key):
         st = self._pinned(key, src.shape, src.dtype)
@@ -267,48 +303,66 @@ class DeviceSystem:
         return st.numpy()
 
     def upload_elements(self, el, p_prev=None, q_prev=None):
-        """Host -> HBM copy of the element state through pinned staging."""
+        """Host -> HBM copy of the element state (caller arrays page-locked)."""
         for name in ("p", "q", "v", "qdot"):
             self._h2d(getattr(self, name), getattr(el, name), name)
         if p_prev is not None:
             self._h2d(self.p_prev, p_prev, "p_prev")
             self._h2d(self.q_prev, q_prev, "q_prev")
 
-    def upload_bond_state(self, b):
-        if self.nb == 0:
-            return
-        st = self._pinned("bstate", (L.BS["COUNT"], self.nb))
-        h = st.numpy()
-        h[L.BS["SCALE"]] = b.stiffness_scale
-        h[L.BS["DAMAGE"]] = b.damage
-        h[L.BS["PLASTIC"]] = b.plastic_strain
-        h[L.BS["SIGMA"]] = b.sigma
-        h[L.BS["TAU"]] = b.tau
-        pos = self.pos_of_bond_d
-        self.bstate[:, pos] = st.to(self.device, non_blocking=True)
-        stt = self._pinned("status", (self.nb,), torch.int8)
-        stt.numpy()[...] = b.status
-        self.status[pos] = stt.to(self.device, non_blocking=True)
+    _BSTATE = (("stiffness_scale", "SCALE"), ("damage", "DAMAGE"),
+               ("plastic_strain", "PLASTIC"), ("sigma", "SIGMA"), ("tau", "TAU"))
 
-    def download_bond_state(self, b):
+    def upload_bond_state(self, b):
+        """Host -> HBM copy of the mutable bond state, scattered to SELL positions."""
         if self.nb == 0:
             return
+        if getattr(self, "_bs_stage", None) is None:
+            self._bs_stage = torch.empty((L.BS["COUNT"], self.nb), dtype=F64, device=self.device)
+            self._st_stage = torch.empty(self.nb, dtype=torch.int8, device=self.device)
+        for name, plane in self._BSTATE:
+            self._h2d(self._bs_stage[L.BS[plane]], getattr(b, name), "bs_" + name)
+        self._h2d(self._st_stage, np.asarray(b.status, dtype=np.int8), "bs_status")
         pos = self.pos_of_bond_d
-        h = self._d2h(self.bstate[:, pos], "bstate_out")
-        b.stiffness_scale[:] = h[L.BS["SCALE"]]
-        b.damage[:] = h[L.BS["DAMAGE"]]
-        b.plastic_strain[:] = h[L.BS["PLASTIC"]]
-        b.sigma[:] = h[L.BS["SIGMA"]]
-        b.tau[:] = h[L.BS["TAU"]]
-        b.status[:] = self._d2h(self.status[pos], "status_out")
+        self.bstate[:, pos] = self._bs_stage
+        self.status[pos] = self._st_stage
+
+    def download_bond_state(self, b, sync=True):
+        if self.nb == 0:
+            return []
+        pos = self.pos_of_bond_d
+        if getattr(self, "_bs_stage", None) is None:
+            self._bs_stage = torch.empty((L.BS["COUNT"], self.nb), dtype=F64, device=self.device)
+            self._st_stage = torch.empty(self.nb, dtype=torch.int8, device=self.device)
+        torch.index_select(self.bstate, 1, pos, out=self._bs_stage)
+        torch.index_select(self.status, 0, pos, out=self._st_stage)
+        pending = [self._d2h_into(getattr(b, name), self._bs_stage[L.BS[plane]])
+                   for name, plane in self._BSTATE]
+        pending.append(self._d2h_into(b.status, self._st_stage))
+        if sync:
+            self._finish(pending)
+            return []
+        return pending
+
+    def _finish(self, pending):
+        torch.cuda.current_stream(self.device).synchronize()
+        for item in pending:
+            if item is not None:
+                dst, st = item
+                dst[...] = st.numpy()
 
     def download_state(self, scene):
+        """HBM -> host copy of element and bond state into the caller's arrays."""
         el = scene.elements
-        for name in ("p", "q", "v", "qdot"):
-            getattr(el, name)[:] = self._d2h(getattr(self, name), name + "_out")
-        scene.p_prev = self._d2h(self.p_prev, "p_prev_out").copy()
-        scene.q_prev = self._d2h(self.q_prev, "q_prev_out").copy()
-        self.download_bond_state(scene.bonds)
+        pending = [self._d2h_into(getattr(el, name), getattr(self, name))
+                   for name in ("p", "q", "v", "qdot")]
+        if not isinstance(scene.p_prev, np.ndarray) or scene.p_prev.shape != (self.n, 3):
+            scene.p_prev = np.empty((self.n, 3))
+            scene.q_prev = np.empty((self.n, 4))
+        pending.append(self._d2h_into(scene.p_prev, self.p_prev))
+        pending.append(self._d2h_into(scene.q_prev, self.q_prev))
+        pending += self.download_bond_state(scene.bonds, sync=False)
+        self._finish(pending)
 
     def bootstrap_history(self, dt):
         """p_prev = p - dt v, q_prev = normalize(geodesic(q, -dt qdot))
@@ -400,6 +454,17 @@ class DeviceSystem:
         self.launches += 1
         if rc != 0:
             raise L.BdemLibraryError(f"{name} failed with status {rc}")
+
+
+_REGISTERED: dict = {}
+
+
+def _unregister(key):
+    if _REGISTERED.pop(key, None):
+        try:
+            torch.cuda.cudart().cudaHostUnregister(key[0])
+        except Exception:
+            pass
 
 
 def _host(a):
