@@ -83,14 +83,16 @@ enum {
 /* per-bond staging written by bdem_bond_assemble (each n_bond doubles) */
 enum {
   BDEM_ST_E = 0,     /* bond energy                                   */
-  BDEM_ST_GPJ = 1,   /* d E / d p_j [3]  (d/dp_i = -this)             */
-  BDEM_ST_GQI = 4,   /* d E / d q_i [4]                               */
-  BDEM_ST_GQJ = 8,   /* d E / d q_j [4]                               */
-  BDEM_ST_APOS = 12, /* clamped stretch block a+ (sym: xx xy xz yy yz zz); off-diag = -a+ */
-  BDEM_ST_C = 18,    /* clamped reduced rotation block (i,j) quadrant, 3x3 row-major */
-  BDEM_ST_A = 27,    /* clamped (i,i) rotation quadrant (sym 6)        */
-  BDEM_ST_D = 33,    /* clamped (j,j) rotation quadrant (sym 6)        */
-  BDEM_ST_COUNT = 39
+  BDEM_ST_N = 1,     /* unit bond direction n [3]                     */
+  BDEM_ST_KC = 4,    /* k c: dE/dp_j = kc n, dE/dp_i = -kc n          */
+  BDEM_ST_ALPHA = 5, /* clamped stretch block a+ = alpha n n^T + beta I */
+  BDEM_ST_BETA = 6,  /*   (off-diagonal coupling -a+)                 */
+  BDEM_ST_GQI = 7,   /* d E / d q_i [4]                               */
+  BDEM_ST_GQJ = 11,  /* d E / d q_j [4]                               */
+  BDEM_ST_C = 15,    /* clamped reduced rotation block (i,j) quadrant, 3x3 row-major */
+  BDEM_ST_A = 24,    /* clamped (i,i) rotation quadrant (sym 6)        */
+  BDEM_ST_D = 30,    /* clamped (j,j) rotation quadrant (sym 6)        */
+  BDEM_ST_COUNT = 36
 };
 
 /* per-pair staging (each pair_cap doubles) */

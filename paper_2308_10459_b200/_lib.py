@@ -20,7 +20,7 @@ ERRSLOT_COUNT = 8
 BG = dict(L0=0, D0=1, FRAME=4, KN=13, KT=14, KDIAG=15, RADIUS=18, SECTION=19, SECOND=20,
           POLAR=21, TENSILE=22, SHEAR=23, COUNT=24)
 BS = dict(SCALE=0, DAMAGE=1, PLASTIC=2, SIGMA=3, TAU=4, COUNT=5)
-ST = dict(E=0, GPJ=1, GQI=4, GQJ=8, APOS=12, C=18, A=27, D=33, COUNT=39)
+ST = dict(E=0, N=1, KC=4, ALPHA=5, BETA=6, GQI=7, GQJ=11, C=15, A=24, D=30, COUNT=36)
 PS = dict(E=0, GI=1, A=4, COUNT=10)
 SC = dict(F=0, GNORM2=1, CNORM2=2, MAXDEV=3, SLOPE=4, FT=5, NSING=6, EBOND=7, ECOL=8, EGRAV=9,
           EKIN=10, EPAIR=11, COUNT=32)

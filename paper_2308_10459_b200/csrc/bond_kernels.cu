@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(128) k_bond_ambient(bdem_system_t S, const dou
 // fused production kernel: energy, gradient contributions and the clamped
 // reduced blocks (energy_terms + build_clamped_pieces, solver.py:141-162)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_bond_assemble(bdem_system_t S, const double *p,
+__global__ void __launch_bounds__(128, 4) k_bond_assemble(bdem_system_t S, const double *p,
                                                        const double *q) {
   const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nb = S.n_bond;
@@ -147,69 +147,33 @@ __global__ void __launch_bounds__(128) k_bond_assemble(bdem_system_t S, const do
 #pragma unroll
   for (int c = 0; c < 3; ++c) kds[c] = B.scale * B.kd[c];
 
-  // stretch: energy, gradient and the closed-form clamp of [[a,-a],[-a,a]]
+  // stretch: energy, gradient (kc n) and the closed-form clamp of
+  // [[a,-a],[-a,a]]: a+ = k (nn + max(c/l,0) (I - nn)) = alpha nn + beta I
   const Stretch st = stretch_eval(pi, pj, B.l0, ks);
   if (st.degenerate) flag_error(S.err, BDEM_ERR_DEGENERATE_BOND, b);
-  double apos[6];
-  stretch_block(st, st.c_over_l > 0.0 ? st.c_over_l : 0.0, apos);
+  const double f = st.c_over_l > 0.0 ? st.c_over_l : 0.0;
+  const double beta = ks * f;
+  const double alpha = ks - beta;
 
   const Shear sh = shear_eval(qi, qj, B.d0, kts);
   if (sh.antipodal) flag_error(S.err, BDEM_ERR_ANTIPODAL, b);
-  const BendTwist bt = bendtwist_eval(qi, qj, B.F, kds);
+  double S6[21];
+  const RotOut ro = reduced_rotation(qi, qj, B.d0, B.F, kds, sh, S6);
 
-  st_out[BDEM_ST_E * nb + b] = (st.E + sh.E) + bt.E;
+  st_out[BDEM_ST_E * nb + b] = (st.E + sh.E) + ro.E_b;
 #pragma unroll
-  for (int c = 0; c < 3; ++c) st_out[(BDEM_ST_GPJ + c) * nb + b] = st.gj[c];
+  for (int c = 0; c < 3; ++c) st_out[(BDEM_ST_N + c) * nb + b] = st.n[c];
+  st_out[BDEM_ST_KC * nb + b] = st.kc;
+  st_out[BDEM_ST_ALPHA * nb + b] = alpha;
+  st_out[BDEM_ST_BETA * nb + b] = beta;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
-    st_out[(BDEM_ST_GQI + c) * nb + b] = sh.g[c] + bt.gi[c];
-    st_out[(BDEM_ST_GQJ + c) * nb + b] = sh.g[c] + bt.gj[c];
+    st_out[(BDEM_ST_GQI + c) * nb + b] = sh.g[c] + ro.gbi[c];
+    st_out[(BDEM_ST_GQJ + c) * nb + b] = sh.g[c] + ro.gbj[c];
   }
-#pragma unroll
-  for (int c = 0; c < 6; ++c) st_out[(BDEM_ST_APOS + c) * nb + b] = apos[c];
 
-  // reduced rotation block T H_qq T^T with T = blockdiag(G_l(q_i), G_l(q_j))
-  double Gi[3][4], Gj[3][4];
-  gl_mat(qi, Gi);
-  gl_mat(qj, Gj);
-  double hu[4][4], H[4][4], R[3][3];
-  shear_hu(sh, B.d0, hu);
-  double S6[21];
-  // (i,i)
-  bendtwist_block(bt, B.F, 0, H);
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) H[r][c] = hu[r][c] + H[r][c];
-  reduce_block(Gi, H, Gi, R);
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int c = r; c < 3; ++c) S6[sidx<6>(r, c)] = 0.5 * (R[r][c] + R[c][r]);
-  // (j,j)
-  bendtwist_block(bt, B.F, 1, H);
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) H[r][c] = hu[r][c] + H[r][c];
-  reduce_block(Gj, H, Gj, R);
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int c = r; c < 3; ++c) S6[sidx<6>(r + 3, c + 3)] = 0.5 * (R[r][c] + R[c][r]);
-  // (i,j)
-  bendtwist_block(bt, B.F, 2, H);
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) H[r][c] = hu[r][c] + H[r][c];
-  reduce_block(Gi, H, Gj, R);
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) S6[sidx<6>(r, c + 3)] = R[r][c];
-
-  psd_clamp<6>(S6);
+  __shared__ double psd_work[21 * 128];
+  psd_clamp<6>(S6, psd_work + threadIdx.x, 128);
 
 #pragma unroll
   for (int r = 0; r < 3; ++r)

@@ -28,6 +28,19 @@ __device__ __forceinline__ void store_q(double *q, int64_t e, const double qe[4]
   q2[1] = make_double2(qe[2], qe[3]);
 }
 
+// staged stretch piece of bond position b: returns k c, fills n and the
+// clamped block a+ = alpha n n^T + beta I (sym6)
+__device__ __forceinline__ double stage_stretch(const double *st, int64_t nb, int64_t b,
+                                                double n[3], double a[6]) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) n[c] = st[(BDEM_ST_N + c) * nb + b];
+  const double al = st[BDEM_ST_ALPHA * nb + b], be = st[BDEM_ST_BETA * nb + b];
+  const int pr[6] = {0, 0, 0, 1, 1, 2}, pc[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+  for (int t = 0; t < 6; ++t) a[t] = al * (n[pr[t]] * n[pc[t]]) + (pr[t] == pc[t] ? be : 0.0);
+  return st[BDEM_ST_KC * nb + b];
+}
+
 // collider SDF value, gradient and Hessian (contact.py:38-133)
 __device__ void collider_eval(const bdem_collider_t &C, const double p[3], double &g,
                               double dg[3], double H[6]) {
@@ -103,13 +116,15 @@ __global__ void __launch_bounds__(kThreads) k_element_assemble(bdem_system_t S, 
     const int sl = (int)(e >> 5), lane = (int)(e & 31);
     // bonds with i == e: this element's SELL row (padding stages zeros)
     for (int64_t b = S.slice_base[sl] + lane; b < S.slice_base[sl + 1]; b += 32) {
+      double n[3], apos[6];
+      const double kc = stage_stretch(st, nb, b, n, apos);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) gp[c] += -st[(BDEM_ST_GPJ + c) * nb + b];
+      for (int c = 0; c < 3; ++c) gp[c] += -(kc * n[c]);
 #pragma unroll
       for (int c = 0; c < 4; ++c) gq[c] += st[(BDEM_ST_GQI + c) * nb + b];
 #pragma unroll
       for (int t = 0; t < 6; ++t) {
-        P[t] += st[(BDEM_ST_APOS + t) * nb + b];
+        P[t] += apos[t];
         R[t] += st[(BDEM_ST_A + t) * nb + b];
       }
       ebond += st[BDEM_ST_E * nb + b];
@@ -118,13 +133,15 @@ __global__ void __launch_bounds__(kThreads) k_element_assemble(bdem_system_t S, 
     for (int64_t k = S.jslice_base[sl] + lane; k < S.jslice_base[sl + 1]; k += 32) {
       const int64_t b = S.jpos[k];
       if (b < 0) continue;
+      double n[3], apos[6];
+      const double kc = stage_stretch(st, nb, b, n, apos);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) gp[c] += st[(BDEM_ST_GPJ + c) * nb + b];
+      for (int c = 0; c < 3; ++c) gp[c] += kc * n[c];
 #pragma unroll
       for (int c = 0; c < 4; ++c) gq[c] += st[(BDEM_ST_GQJ + c) * nb + b];
 #pragma unroll
       for (int t = 0; t < 6; ++t) {
-        P[t] += st[(BDEM_ST_APOS + t) * nb + b];
+        P[t] += apos[t];
         R[t] += st[(BDEM_ST_D + t) * nb + b];
       }
     }

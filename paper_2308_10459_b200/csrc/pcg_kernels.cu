@@ -188,15 +188,17 @@ __device__ __forceinline__ void slot_apply(const bdem_system_t &S, const double 
   if (r.o < 0) return;
   const int64_t nb = S.n_bond;
   const double *st = S.stage;
-  double xo[6], a[6], C[9];
+  double xo[6], n[3], C[9];
   load6_ro(x, r.o, S.vstride, xo);
 #pragma unroll
-  for (int t = 0; t < 6; ++t) a[t] = __ldg(st + (BDEM_ST_APOS + t) * nb + r.b);
+  for (int t = 0; t < 3; ++t) n[t] = __ldg(st + (BDEM_ST_N + t) * nb + r.b);
+  const double al = __ldg(st + BDEM_ST_ALPHA * nb + r.b), be = __ldg(st + BDEM_ST_BETA * nb + r.b);
 #pragma unroll
   for (int t = 0; t < 9; ++t) C[t] = __ldg(st + (BDEM_ST_C + t) * nb + r.b);
-  double ap[3];
-  symv3(a, xo, ap);
-  acc[0] -= ap[0]; acc[1] -= ap[1]; acc[2] -= ap[2];
+  // a+ x = alpha (n.x) n + beta x ; coupling -a+
+  const double nx = al * ((n[0] * xo[0] + n[1] * xo[1]) + n[2] * xo[2]);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) acc[c] -= nx * n[c] + be * xo[c];
   if (!r.tr) {
 #pragma unroll
     for (int q = 0; q < 3; ++q)

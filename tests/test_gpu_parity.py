@@ -181,7 +181,9 @@ def test_assembly_vs_golden(cuda_ok, tag):
     b = bonds_from(d, f"{tag}_b_")
     act = np.nonzero(b.status != 2)[0]
     st = dev.stage.cpu().numpy()[:, dev.sell.pos_of_bond]
-    apos = _sym6_to_mat(st[L.ST["APOS"]:L.ST["APOS"] + 6].T[act])
+    n = st[L.ST["N"]:L.ST["N"] + 3].T[act]
+    al, be = st[L.ST["ALPHA"]][act], st[L.ST["BETA"]][act]
+    apos = al[:, None, None] * n[:, :, None] * n[:, None, :] + be[:, None, None] * np.eye(3)
     want_pp = d[f"{tag}_bond_pp"]
     hs = np.abs(want_pp).max()
     _assert_close(apos, want_pp[:, :3, :3], 1e-10, 1e-12 * hs, "a+ (ii)")
