@@ -96,7 +96,7 @@ __device__ void collider_eval(const bdem_collider_t &C, const double p[3], doubl
 // ---------------------------------------------------------------------------
 // element assembly
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_element_assemble(bdem_system_t S, const double *p,
+__global__ void __launch_bounds__(kThreads, 2) k_element_assemble(bdem_system_t S, const double *p,
                                                                const double *q, double *z) {
   __shared__ double sh[kThreads / 32];
   double acc_f = 0.0, acc_g2 = 0.0, acc_c2 = 0.0, acc_dev = 0.0, acc_sing = 0.0;
