@@ -187,6 +187,7 @@ typedef struct {
   double *pcg;                   /* BDEM_PCG_COUNT                     */
   int32_t *err;                  /* BDEM_ERRSLOT_COUNT                 */
   unsigned int *counter;         /* last-block counters (zeroed)       */
+  int32_t *clamp_list;           /* (n_bond) queue of indefinite rotation blocks */
   /* physics */
   double gravity[3];
   double k_contact, k_element;

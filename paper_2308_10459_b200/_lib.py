@@ -48,7 +48,7 @@ class System(C.Structure):
         ("slice_base", _p), ("pos_oslot", _p), ("jslice_base", _p), ("jpos", _p), ("jslot", _p),
         ("pair_i", _p), ("pair_j", _p), ("pi_ptr", _p), ("pj_ptr", _p), ("pj_idx", _p),
         ("stage", _p), ("pstage", _p), ("diag", _p), ("minv", _p), ("red", _p),
-        ("scalars", _p), ("pcg", _p), ("err", _p), ("counter", _p),
+        ("scalars", _p), ("pcg", _p), ("err", _p), ("counter", _p), ("clamp_list", _p),
         ("gravity", C.c_double * 3), ("k_contact", C.c_double), ("k_element", C.c_double),
         ("n_colliders", C.c_int32), ("pad_", C.c_int32),
         ("colliders", Collider * MAX_COLLIDERS),

@@ -8,6 +8,7 @@
 namespace bdem {
 
 constexpr int kRedBlocks = BDEM_RED_BLOCKS;
+constexpr int kClampCounter = 5;  // sys->counter slot: queued indefinite blocks
 constexpr int kThreads = 256;
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }

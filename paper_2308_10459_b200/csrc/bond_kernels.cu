@@ -172,8 +172,17 @@ __global__ void __launch_bounds__(128, 4) k_bond_assemble(bdem_system_t S, const
     st_out[(BDEM_ST_GQJ + c) * nb + b] = sh.g[c] + ro.gbj[c];
   }
 
+  // PSD blocks (all of them at identity orientations) are final here;
+  // indefinite ones are queued for the register-resident eigen-clamp pass
+  // (k_bond_clamp) and staged unclamped meanwhile
   __shared__ double psd_work[21 * 128];
-  psd_clamp<6>(S6, psd_work + threadIdx.x, 128);
+  double mx = 0.0;
+#pragma unroll
+  for (int t = 0; t < 21; ++t) mx = fmax(mx, fabs(S6[t]));
+  if (mx != 0.0 && !psd_within<6>(S6, 4e-14 * mx, psd_work + threadIdx.x, 128)) {
+    const unsigned int slot = atomicAdd(S.counter + kClampCounter, 1u);
+    S.clamp_list[slot] = (int32_t)b;
+  }
 
 #pragma unroll
   for (int r = 0; r < 3; ++r)
@@ -184,6 +193,41 @@ __global__ void __launch_bounds__(128, 4) k_bond_assemble(bdem_system_t S, const
   for (int t = 0; t < 6; ++t) {
     st_out[(BDEM_ST_A + t) * nb + b] = S6[sidx<6>(pr[t], pc[t])];
     st_out[(BDEM_ST_D + t) * nb + b] = S6[sidx<6>(pr[t] + 3, pc[t] + 3)];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// eigen-clamp pass for the queued indefinite rotation blocks (spd_project,
+// solver.py:89-113): one thread per queued bond, Jacobi in registers
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_bond_clamp(bdem_system_t S) {
+  const unsigned int n = S.counter[kClampCounter];
+  const int64_t nb = S.n_bond;
+  double *st = S.stage;
+  for (unsigned int t = blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += gridDim.x * blockDim.x) {
+    const int64_t b = S.clamp_list[t];
+    double A[21];
+    const int pr[6] = {0, 0, 0, 1, 1, 2}, pc[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      A[sidx<6>(pr[q], pc[q])] = st[(BDEM_ST_A + q) * nb + b];
+      A[sidx<6>(pr[q] + 3, pc[q] + 3)] = st[(BDEM_ST_D + q) * nb + b];
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) A[sidx<6>(r, c + 3)] = st[(BDEM_ST_C + 3 * r + c) * nb + b];
+    jacobi_clamp_regs<6>(A);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      st[(BDEM_ST_A + q) * nb + b] = A[sidx<6>(pr[q], pc[q])];
+      st[(BDEM_ST_D + q) * nb + b] = A[sidx<6>(pr[q] + 3, pc[q] + 3)];
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) st[(BDEM_ST_C + 3 * r + c) * nb + b] = A[sidx<6>(r, c + 3)];
   }
 }
 
@@ -344,8 +388,12 @@ int bdem_bond_assemble(const bdem_system_t *sys, const double *p, const double *
                        void *stream) {
   if (!sys) return BDEM_ERR_ARG;
   if (sys->n_bond == 0) return BDEM_OK;
-  k_bond_assemble<<<grid_for(sys->n_bond, 128), 128, 0, as_stream(stream)>>>(*sys, p, q);
-  return launch_status();
+  cudaStream_t st = as_stream(stream);
+  cudaMemsetAsync(sys->counter + kClampCounter, 0, sizeof(unsigned int), st);
+  k_bond_assemble<<<grid_for(sys->n_bond, 128), 128, 0, st>>>(*sys, p, q);
+  // the clamp pass reads the queue length on the device; idle threads exit
+  k_bond_clamp<<<kRedBlocks, 128, 0, st>>>(*sys);
+  return launch_status(2);
 }
 
 int bdem_bond_energy(const bdem_system_t *sys, const double *p, const double *q, int col,

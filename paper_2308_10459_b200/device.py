@@ -185,6 +185,7 @@ class DeviceSystem:
         self.pcg_state = torch.zeros(L.PCG["COUNT"], dtype=F64, device=dev)
         self.err = torch.zeros(L.ERRSLOT_COUNT, dtype=I32, device=dev)
         self.counter = torch.zeros(L.N_COUNTERS, dtype=torch.int32, device=dev)
+        self.clamp_list = torch.zeros(npos, dtype=I32, device=dev)
         # host staging for scalar read-backs
         self.h_scalars = torch.zeros(L.SC["COUNT"], dtype=F64).pin_memory()
         self.h_pcg = torch.zeros(L.PCG["COUNT"], dtype=F64).pin_memory()
@@ -213,6 +214,7 @@ class DeviceSystem:
         s.stage, s.diag, s.minv = _ptr(self.stage), _ptr(self.diag), _ptr(self.minv)
         s.red, s.scalars, s.pcg = _ptr(self.red), _ptr(self.scalars), _ptr(self.pcg_state)
         s.err, s.counter = _ptr(self.err), _ptr(self.counter)
+        s.clamp_list = _ptr(self.clamp_list)
         self.sysp = C.pointer(s)
         # contact pairs (capacity grows on demand)
         self.n_pair = 0
