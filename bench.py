@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--epsilon", type=float, default=1e-3)
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 2M-block kernel leg")
+    ap.add_argument("--c5-side", type=int, default=126)
     ap.add_argument("--crop", type=int, nargs=2, default=(100, 60),
                     help="plate crop for the CPU sample (nx ny)")
     return ap.parse_args()
@@ -216,6 +218,56 @@ def restore(scene, snap):
             scene.device.device)
 
 
+def c5_leg(n_side, peak):
+    """BASELINE configs[4] (C5): 2M-sphere jittered block, random unit
+    quaternions, ~12M bonds.  Measures the fused assembly (random q sends
+    every rotation block through the eigen-clamp pass) and the SpMV at
+    memory-bound scale, each timed with CUDA events over repeated launches on
+    the predictor state of step 1."""
+    import torch
+
+    from paper_2308_10459_b200 import configs
+    from paper_2308_10459_b200.newton import GPUProblem
+    from paper_2308_10459_b200.scene import Scene
+    spec = configs.block(n_side=n_side, random_q=True)
+    scene = Scene.from_spec(spec, host_sync=False)
+    dev = scene.device
+    dev.set_physics(spec.gravity, spec.k_contact, 0.0, [])
+    dev.call("bdem_predict", dev.sysp, dev.p.data_ptr(), dev.q.data_ptr(), dev.v.data_ptr(),
+             dev.qdot.data_ptr(), dev.p_prev.data_ptr(), dev.q_prev.data_ptr(), spec.dt,
+             dev.p_hat.data_ptr(), dev.q_hat.data_ptr(), dev.mp_dt2.data_ptr(),
+             dev.mq_dt2.data_ptr(), dev.xp.data_ptr(), dev.xq.data_ptr(), dev.stream)
+    GPUProblem(dev).assemble(dev.xp, dev.xq)
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    asm_ms = timed(lambda: dev.call("bdem_bond_assemble", dev.sysp, dev.xp.data_ptr(),
+                                    dev.xq.data_ptr(), dev.stream), 3)
+    x = torch.randn(6 * dev.vstride, dtype=torch.float64, device="cuda")
+    y = torch.zeros_like(x)
+    spmv_ms = timed(lambda: dev.call("bdem_spmv", dev.sysp, x.data_ptr(), y.data_ptr(),
+                                     dev.stream), 20)
+    sb = spmv_bytes(dev)
+    out = {"workload": f"C5 block {n_side}^3 random q (BASELINE configs[4])",
+           "spheres": dev.n, "bonds": dev.nb, "assembly_ms": asm_ms,
+           "bonds_per_sec_assembled": dev.nb / (asm_ms * 1e-3),
+           "spmv_ms": spmv_ms, "spmv_bytes": sb, "spmv_gbs": sb / (spmv_ms * 1e-3) / 1e9,
+           "spmv_frac": sb / (spmv_ms * 1e-3) / 1e9 / peak}
+    del scene, dev
+    torch.cuda.empty_cache()
+    return out
+
+
 def reduce_across_ranks(times_ms, counts, world, device):
     """Replica aggregation: device times -> max over ranks, work -> sum."""
     import torch
@@ -370,6 +422,8 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
     }
+    if not args.no_c5:
+        line["c5_block"] = c5_leg(args.c5_side, peak)
     if not args.no_cpu_baseline and world == 1:
         rate, nb_crop, its, pcg, sec = cpu_sample(args.crop[0], args.crop[1], args.epsilon,
                                                   2, 6, 1)
