@@ -224,6 +224,45 @@ def gold_newton_solve():
     save("newton_solve.npz", **out)
 
 
+def gold_colliders():
+    """Sphere and box colliders (contact.py:61-133): the collider curvature
+    makes the element position blocks indefinite, exercising the 3x3 clamp of
+    build_clamped_pieces (solver.py:165-167)."""
+    spec = C.cube(n_side=4, r=0.002, seed=71, random_q=False, youngs=3e8, k_contact=1e8)
+    rng = np.random.default_rng(72)
+    el = spec.elements
+    el.v[:] = 0.02 * rng.normal(size=el.v.shape)
+    lo, hi = el.p.min(axis=0), el.p.max(axis=0)
+    mid = 0.5 * (lo + hi)
+    sphere = rc.SphereCollider(tuple(mid + np.array([0.0, 0.0, 0.004])), 0.005)
+    box = rc.BoxCollider(tuple(np.array([lo[0], mid[1], mid[2]])), (0.003, 0.02, 0.02))
+    sc = ref_scene(spec, colliders=[sphere, box])
+    ctx = ri.StepContext(sc.dt, sc.p_prev.copy(), sc.q_prev.copy(), sc.elements.p.copy(),
+                         sc.elements.q.copy())
+    model = ri.PotentialModel(sc.elements, sc.bonds, np.zeros((0, 2), dtype=np.int64),
+                              sc.colliders, sc.gravity, sc.k_contact, sc.k_element)
+    prob = ri.ImplicitProblem(model, ctx)
+    p, q = ri.predict_state(ctx, sc.elements.v, sc.elements.qdot, prob.free)
+    f, gp, gq = prob.value_and_gradient(p, q)
+    z = rsv.reduced_gradient(q, gp, gq, prob.free)
+    pieces = rsv.build_clamped_pieces(prob, p, q, gq)
+    mat, diag = rsv.assemble_reduced_system(pieces, q, prob.free)
+    hb = prob.hessian_blocks(p, q)
+    n_inside = int(np.count_nonzero(np.abs(hb.elem_pp).sum(axis=(1, 2))))
+    n_indef = int(np.count_nonzero(np.linalg.eigvalsh(
+        hb.elem_pp + prob.inertia_diag()[0][:, None, None] * np.eye(3)).min(axis=1) < 0))
+    print(f"  colliders: {n_inside} elements with collider curvature, {n_indef} indefinite")
+    out = pack("el_", spec.elements, ELEM_FIELDS)
+    out.update(pack("b_", spec.bonds, BOND_FIELDS))
+    out.update({"dt": sc.dt, "kc": sc.k_contact, "ke": sc.k_element, "gravity": sc.gravity,
+                "sphere": np.array([*sphere.center, sphere.radius]),
+                "box": np.array([*box.center, *box.half_extents]),
+                "p_prev": ctx.p_prev, "q_prev": ctx.q_prev, "p": p, "q": q, "f": f, "z": z,
+                "elem_pos": pieces.elem_pos, "diag": diag, "A": mat.toarray(),
+                "n_indef": n_indef, "value": prob.value(p, q)})
+    save("colliders.npz", **out)
+
+
 def _run_traj(name, spec, steps, eps, driver=None, schedule=None, max_iter=300):
     sc = ref_scene(spec, driver=driver)
     cfg = rsv.SolverConfig(epsilon=eps, max_iterations=max_iter)
@@ -342,7 +381,7 @@ def gold_broadphase_labels():
 if __name__ == "__main__":
     t = time.time()
     which = sys.argv[1:] or ["bond_terms", "fracture", "broadphase_labels", "newton_pieces",
-                             "newton_solve", "trajectories"]
+                             "newton_solve", "colliders", "trajectories"]
     for name in which:
         globals()[f"gold_{name}"]()
     print(f"done in {time.time() - t:.1f}s")

@@ -424,3 +424,43 @@ def test_spmv_matches_oracle_csr_random_q(cuda_ok):
     dev.call("bdem_spmv", dev.sysp, xd.data_ptr(), yd.data_ptr(), dev.stream)
     want = mat @ x
     _assert_close(_aos(yd, dev), want, 1e-9, 1e-10 * np.abs(want).max(), "A x (random q)")
+
+
+def test_sphere_box_colliders_vs_golden(cuda_ok):
+    """Sphere and box penalties (contact.py:61-133, 227-248): values, gradient
+    and the clamped element position blocks (8 of them indefinite before the
+    clamp), diagonal blocks and A x against the reference."""
+    import torch
+    from paper_2308_10459_b200 import BoxCollider, SphereCollider
+    from paper_2308_10459_b200.device import DeviceSystem
+    from paper_2308_10459_b200.newton import GPUProblem
+    d = load("colliders.npz")
+    el = elements_from(d, "el_")
+    b = bonds_from(d, "b_")
+    dev = DeviceSystem(elements=el, bonds=b)
+    sp, bx = d["sphere"], d["box"]
+    dev.set_physics(d["gravity"], float(d["kc"]), float(d["ke"]),
+                    [SphereCollider(tuple(sp[:3]), float(sp[3])),
+                     BoxCollider(tuple(bx[:3]), tuple(bx[3:]))])
+    dev.p_prev.copy_(torch.from_numpy(d["p_prev"]))
+    dev.q_prev.copy_(torch.from_numpy(d["q_prev"]))
+    dev.call("bdem_predict", dev.sysp, dev.p.data_ptr(), dev.q.data_ptr(), dev.v.data_ptr(),
+             dev.qdot.data_ptr(), dev.p_prev.data_ptr(), dev.q_prev.data_ptr(), float(d["dt"]),
+             dev.p_hat.data_ptr(), dev.q_hat.data_ptr(), dev.mp_dt2.data_ptr(),
+             dev.mq_dt2.data_ptr(), dev.xp.data_ptr(), dev.xq.data_ptr(), dev.stream)
+    _assert_close(dev.xp.cpu().numpy(), d["p"], 1e-15, 0.0, "p0")
+    prob = GPUProblem(dev)
+    f, gnorm, _, _ = prob.assemble(dev.xp, dev.xq)
+    assert f == pytest.approx(float(d["f"]), rel=1e-12)
+    _assert_close(_aos(dev.z, dev), d["z"], 1e-9, 1e-11 * np.abs(d["z"]).max(), "z")
+    diag = dev.diag[:, :dev.nf].cpu().numpy().T
+    want = d["diag"]
+    sc = np.abs(want).max()
+    _assert_close(_sym6_to_mat(diag[:, :6]), want[:, :3, :3], 1e-9, 1e-11 * sc, "diag pos")
+    x = np.random.default_rng(4).normal(size=want.shape[0] * 6)
+    xd = _soa(x, dev)
+    yd = torch.zeros_like(xd)
+    dev.call("bdem_spmv", dev.sysp, xd.data_ptr(), yd.data_ptr(), dev.stream)
+    wy = d["A"] @ x
+    _assert_close(_aos(yd, dev), wy, 1e-9, 1e-11 * np.abs(wy).max(), "A x")
+    assert prob.value(dev.xp, dev.xq) == pytest.approx(float(d["value"]), rel=1e-12)

@@ -164,3 +164,24 @@ def test_trajectory(name):
     ev = np.array(events, dtype=float).reshape(-1, 4)
     assert np.array_equal(ev[:, :2], d["events"][:, :2])
     assert np.array_equal(st.bonds.status, d["final_b_status"])
+
+
+def test_sphere_box_colliders():
+    from paper_2308_10459_b200.colliders import BoxCollider, SphereCollider
+    d = load("colliders.npz")
+    el = elements_from(d, "el_")
+    b = bonds_from(d, "b_")
+    sp, bx = d["sphere"], d["box"]
+    cols = [SphereCollider(tuple(sp[:3]), float(sp[3])), BoxCollider(tuple(bx[:3]), tuple(bx[3:]))]
+    obj = O.Objective(el, b, np.zeros((0, 2), dtype=np.int64), cols, d["gravity"],
+                      float(d["kc"]), float(d["ke"]), float(d["dt"]), d["p_prev"], d["q_prev"],
+                      el.p.copy(), el.q.copy())
+    p, q = d["p"], d["q"]
+    f, gp, gq = obj.value_and_gradient(p, q)
+    assert f == pytest.approx(float(d["f"]), rel=1e-14)
+    pc = O.clamped_pieces(obj, p, q, gq)
+    _assert_close(pc["elem_pos"], d["elem_pos"], 1e-11, 1e-12 * np.abs(d["elem_pos"]).max(),
+                  "elem_pos")
+    mat, diag = O.reduced_system(pc, obj.free)
+    _assert_close(diag, d["diag"], 1e-11, 1e-12 * np.abs(d["diag"]).max(), "diag")
+    assert int(d["n_indef"]) > 0
