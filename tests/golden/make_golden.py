@@ -263,6 +263,34 @@ def gold_colliders():
     save("colliders.npz", **out)
 
 
+def gold_runner():
+    """run_simulation + _step_with_retries + stats.csv (runner.py:20-164): a
+    plain run, a run whose third frame needs dt halving (max_iterations=4),
+    and one that gives up (max_iterations=3 -> StepFailure)."""
+    import tempfile
+
+    from bdem import runner as rr
+    out = {}
+    for tag, maxit in (("plain", 300), ("retry", 4)):
+        spec = C.cantilever(nx=10, ny=3, nz=3)
+        sc = ref_scene(spec)
+        d = tempfile.mkdtemp()
+        rr.run_simulation(sc, rsv.SolverConfig(epsilon=1e-7, max_iterations=maxit), frames=3,
+                          fps=500, outdir=d, write_meshes=False)
+        out[f"{tag}_csv"] = np.array(open(os.path.join(d, "stats.csv")).read())
+        out[f"{tag}_p"] = sc.elements.p
+    spec = C.cantilever(nx=10, ny=3, nz=3)
+    sc = ref_scene(spec)
+    try:
+        rr.run_simulation(sc, rsv.SolverConfig(epsilon=1e-7, max_iterations=3), frames=3,
+                          fps=500, write_meshes=False)
+        out["fail_msg"] = np.array("")
+    except rr.StepFailure as exc:
+        out["fail_msg"] = np.array(str(exc))
+        out["fail_residuals"] = np.array(exc.residuals)
+    save("runner.npz", **out)
+
+
 def _run_traj(name, spec, steps, eps, driver=None, schedule=None, max_iter=300):
     sc = ref_scene(spec, driver=driver)
     cfg = rsv.SolverConfig(epsilon=eps, max_iterations=max_iter)
@@ -381,7 +409,7 @@ def gold_broadphase_labels():
 if __name__ == "__main__":
     t = time.time()
     which = sys.argv[1:] or ["bond_terms", "fracture", "broadphase_labels", "newton_pieces",
-                             "newton_solve", "colliders", "trajectories"]
+                             "newton_solve", "colliders", "runner", "trajectories"]
     for name in which:
         globals()[f"gold_{name}"]()
     print(f"done in {time.time() - t:.1f}s")

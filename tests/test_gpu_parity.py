@@ -464,3 +464,42 @@ def test_sphere_box_colliders_vs_golden(cuda_ok):
     wy = d["A"] @ x
     _assert_close(_aos(yd, dev), wy, 1e-9, 1e-11 * np.abs(wy).max(), "A x")
     assert prob.value(dev.xp, dev.xq) == pytest.approx(float(d["value"]), rel=1e-12)
+
+
+@pytest.mark.parametrize("tag,maxit", [("plain", 300), ("retry", 4)])
+def test_runner_stats_vs_golden(cuda_ok, tmp_path, tag, maxit):
+    """run_simulation with dt-halving retries and the bdem-stats-1 CSV
+    (runner.py:20-164) against the reference's own stats.csv."""
+    import io
+
+    from paper_2308_10459_b200 import SolverConfig, configs
+    from paper_2308_10459_b200.runner import read_stats_csv, run_simulation
+    from paper_2308_10459_b200.scene import Scene
+    d = load("runner.npz")
+    scene = Scene.from_spec(configs.cantilever(nx=10, ny=3, nz=3))
+    run_simulation(scene, SolverConfig(epsilon=1e-7, max_iterations=maxit), frames=3, fps=500,
+                   outdir=tmp_path, write_meshes=False)
+    ref_path = tmp_path / "ref.csv"
+    ref_path.write_text(str(d[f"{tag}_csv"]))
+    got = read_stats_csv(tmp_path / "stats.csv")
+    want = read_stats_csv(ref_path)
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        assert g["frame"] == w["frame"] and g["time"] == w["time"]      # same dt sums, exact
+        assert g["intact_bonds"] == w["intact_bonds"] and g["bonds_broken"] == w["bonds_broken"]
+        assert abs(g["newton_iterations"] - w["newton_iterations"]) <= 1
+        for k in ("kinetic", "bond_energy", "gravity_energy"):
+            assert g[k] == pytest.approx(w[k], rel=1e-6, abs=1e-15)
+    _assert_close(scene.elements.p, d[f"{tag}_p"], 1e-8, 1e-9, "final p")
+
+
+def test_runner_step_failure(cuda_ok):
+    from paper_2308_10459_b200 import SolverConfig, configs
+    from paper_2308_10459_b200.runner import StepFailure, run_simulation
+    from paper_2308_10459_b200.scene import Scene
+    d = load("runner.npz")
+    scene = Scene.from_spec(configs.cantilever(nx=10, ny=3, nz=3))
+    with pytest.raises(StepFailure) as exc:
+        run_simulation(scene, SolverConfig(epsilon=1e-7, max_iterations=3), frames=3, fps=500,
+                       write_meshes=False)
+    assert str(exc.value) == str(d["fail_msg"])
