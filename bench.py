@@ -287,18 +287,18 @@ def reduce_across_ranks(times_ms, counts, world, device):
 
 def spmv_bytes(dev):
     """Algorithmic bytes of one SpMV in this library's format:
-    per bond with both ends free: a+ (6) + C (9) fp64 read once = 120 B, plus
-    two adjacency entries (bond id + other slot, int32) = 16 B; per free row:
-    x and y (48 + 48 B), diagonal P, R (96 B), adj_ptr/adj_mid/free_elem (12 B)."""
+    per bond with both ends free: n (3), alpha, beta, C (9) fp64 read once =
+    112 B, plus two adjacency entries (position/slot, int32) = 16 B; per free
+    row: x and y (48 + 48 B), diagonal P, R (96 B), slot/slice index (12 B)."""
     entries = int((dev.sell.pos_oslot >= 0).sum() + (dev.sell.jslot >= 0).sum())
-    return 60 * entries + 8 * entries + dev.nf * (48 + 48 + 96 + 12)
+    return 56 * entries + 8 * entries + dev.nf * (48 + 48 + 96 + 12)
 
 
 def assembly_bytes(dev):
     """Algorithmic bytes of one fused bond-assembly launch: per bond 161 B in
-    (i, j, status, 18 geometry fp64, scale) + 312 B staged out (39 fp64); per
+    (i, j, status, 18 geometry fp64, scale) + 288 B staged out (36 fp64); per
     element the gathered p, q rows once (56 B)."""
-    return dev.nb * (161 + 312) + dev.n * 56
+    return dev.nb * (161 + 288) + dev.n * 56
 
 
 def load_ncu_traffic():
