@@ -1,0 +1,96 @@
+"""Edge cases on the GPU against the CPU oracle: empty bond set, all bonds
+broken, all elements pinned, a single element resting on a collider, and
+unbonded fragments in contact (non-empty self-contact pair list, contact.py:
+140-224, solver.py:856-878)."""
+
+import numpy as np
+import pytest
+
+from _fixtures import close
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_both(el, b, steps, eps=1e-8, colliders=(), k_element=1e6, k_contact=1e6, dt=1e-3,
+              plastic=None):
+    from oracle import cpu_oracle as O
+    from paper_2308_10459_b200 import Scene, SolverConfig, stable_step
+    st = O.OracleState(el.copy(), b.copy(), dt, 1e7, colliders=list(colliders),
+                       k_contact=k_contact, k_element=k_element, plastic=plastic)
+    scene = Scene("edge", el.copy(), b.copy(), colliders=list(colliders), dt=dt, youngs=1e7,
+                  k_contact=k_contact, k_element=k_element, plastic=plastic)
+    reps = []
+    for _ in range(steps):
+        out = O.step(st, O.Config(epsilon=eps, max_iterations=100))
+        rep = stable_step(scene, SolverConfig(epsilon=eps, max_iterations=100))
+        assert rep.committed == out.committed
+        assert rep.contact_pairs == out.contact_pairs
+        assert [e[0] for e in rep.broken] == [e[0] for e in out.broken]
+        ok, info = close(scene.elements.p, st.elements.p, 1e-8, 1e-10)
+        assert ok, info
+        ok, info = close(scene.elements.q, st.elements.q, 1e-8, 1e-10)
+        assert ok, info
+        reps.append(rep)
+    return reps
+
+
+def _chain(n, spacing=0.01, r=0.005):
+    from paper_2308_10459_b200 import configs as C
+    pos = np.zeros((n, 3))
+    pos[:, 0] = spacing * np.arange(n)
+    el = C._elements(pos, np.tile([0.0, 0.0, 0.0, 1.0], (n, 1)), np.full(n, r), 1000.0)
+    return el, pos
+
+
+def test_no_bonds_free_fall(cuda_ok):
+    from paper_2308_10459_b200 import configs as C
+    el, pos = _chain(3, spacing=0.05)
+    b = C.build_bonds(pos, el.radius, np.zeros((0, 2), dtype=np.int64), 1e7, 4e6)
+    assert b.n == 0
+    _run_both(el, b, 3)
+
+
+def test_all_bonds_broken(cuda_ok):
+    from paper_2308_10459_b200 import configs as C
+    el, pos = _chain(4, spacing=0.0105)
+    b = C.build_bonds(pos, el.radius, np.array([[0, 1], [1, 2], [2, 3]]), 1e7, 4e6)
+    b.status[:] = 2
+    el.v[:, 2] = -0.1
+    _run_both(el, b, 3)
+
+
+def test_all_pinned(cuda_ok):
+    from paper_2308_10459_b200 import configs as C
+    el, pos = _chain(3)
+    b = C.build_bonds(pos, el.radius, np.array([[0, 1], [1, 2]]), 1e7, 4e6)
+    el.pinned[:] = True
+    reps = _run_both(el, b, 2)
+    assert reps[0].solve.iterations == 0
+
+
+def test_single_element_on_halfspace(cuda_ok):
+    from paper_2308_10459_b200 import HalfSpace
+    from paper_2308_10459_b200 import configs as C
+    el, pos = _chain(1)
+    el.p[0, 2] = 1e-4
+    el.v[0, 2] = -0.5
+    b = C.build_bonds(pos, el.radius, np.zeros((0, 2), dtype=np.int64), 1e7, 4e6)
+    _run_both(el, b, 4, colliders=[HalfSpace((0.0, 0.0, 1.0), 0.0)], k_contact=1e5)
+
+
+def test_unbonded_fragments_in_contact(cuda_ok):
+    """Two bonded rows, no bonds between them, overlapping spheres: the
+    broad phase returns cross-fragment pairs and the repulsion enters the
+    gradient, the diagonal blocks and the SpMV."""
+    from paper_2308_10459_b200 import configs as C
+    n = 5
+    pos = np.zeros((2 * n, 3))
+    pos[:n, 0] = 0.01 * np.arange(n)
+    pos[n:, 0] = 0.01 * np.arange(n) + 0.003
+    pos[n:, 1] = 0.0095                    # radius 0.005: overlapping rows
+    el = C._elements(pos, np.tile([0.0, 0.0, 0.0, 1.0], (2 * n, 1)), np.full(2 * n, 0.005),
+                     1000.0)
+    pairs = [[k, k + 1] for k in range(n - 1)] + [[n + k, n + k + 1] for k in range(n - 1)]
+    b = C.build_bonds(pos, el.radius, np.array(pairs), 1e7, 4e6)
+    reps = _run_both(el, b, 3, k_element=1e4, eps=1e-7)
+    assert reps[0].contact_pairs > 0
