@@ -352,6 +352,27 @@ int64_t bdem_select_workspace(int64_t n);
 int bdem_select_flagged(const uint8_t *flags, int64_t n, int32_t *out_idx, void *work,
                         int64_t *n_out, void *stream);
 
+/* ---- post-step friction (contact.py:267-350; solver.py:923-925) ---------
+ * Replaces apply_friction(elements, pairs, colliders, k_c, k_ec, mu_s, mu_r,
+ * dt) (contact.py:303).  Pairs are sys->pair_i/pair_j (the step's frozen
+ * candidates, ascending); v (n,3) and qdot (n,4) are corrected in place at
+ * the post-step positions p / orientations q.  The sequential pair sweep is
+ * executed as dependency waves (bdem_friction_schedule), which reproduces the
+ * reference's order of corrections for every element.  `work` holds
+ * bdem_friction_workspace(n_elem, pair_cap) bytes; *n_waves (optional) gets
+ * the number of waves.  Synchronises `stream` once when pairs are in contact.
+ * A no-op when mu_s == mu_r == 0, like the reference. */
+int64_t bdem_friction_workspace(int64_t n_elem, int64_t n_pair);
+int bdem_friction(const bdem_system_t *sys, const double *p, const double *q, double *v,
+                  double *qdot, double mu_s, double mu_r, double dt, void *work,
+                  int64_t *n_waves, void *stream);
+/* Host-only scheduler: pairs (m,2) int32 in sweep order -> wave of each pair
+ * = 1 + latest wave of an earlier pair sharing an element.  Writes `order`
+ * (m pair indices grouped by wave, ascending within a wave) and `wave_ptr`
+ * (depth+1 offsets); returns depth >= 0, or -BDEM_ERR_ARG.  No GPU needed. */
+int64_t bdem_friction_schedule(const int32_t *ends, int64_t m, int64_t n_elem, int32_t *order,
+                               int32_t *wave_ptr);
+
 #ifdef __cplusplus
 }
 #endif

@@ -825,6 +825,83 @@ def candidates(st, labels):
     return pairs[labels[pairs[:, 0]] != labels[pairs[:, 1]]]
 
 
+# ---------------------------------------------------------------------------
+# friction  (src/contact.py:267-350, src/quat.py:41-49, 116-140)
+# ---------------------------------------------------------------------------
+
+def qmul(a, b):
+    """Hamilton product, scalar last (src/quat.py:41-49)."""
+    at, asc = a[..., :3], a[..., 3:]
+    bt, bsc = b[..., :3], b[..., 3:]
+    vec = asc * bt + bsc * at + np.cross(at, bt)
+    return np.concatenate([vec, asc * bsc - np.sum(at * bt, axis=-1, keepdims=True)], axis=-1)
+
+
+def angular_velocity(q, qdot):
+    """2 tangent(qdot) * conj(q), vector part (src/quat.py:116-134)."""
+    radial = np.sum(q * qdot, axis=-1, keepdims=True)
+    conj = np.concatenate([-q[..., :3], q[..., 3:]], axis=-1)
+    return (2.0 * qmul(qdot - radial * q, conj))[..., :3]
+
+
+def quat_rate(q, w):
+    """0.5 (w, 0) * q (src/quat.py:137-141)."""
+    return 0.5 * qmul(np.concatenate([w, np.zeros(w.shape[:-1] + (1,))], axis=-1), q)
+
+
+def _friction_delta(rel, own, fn, coeff, scale, dt):
+    """src/contact.py:267-282."""
+    own_n = np.linalg.norm(own)
+    rel_n = np.linalg.norm(rel)
+    if own_n == 0.0 or rel_n == 0.0 or fn == 0.0:
+        return np.zeros(3)
+    factor = min(1.0, coeff * fn * dt / (scale * rel_n))
+    direction = own / own_n
+    along = min(0.0, max(float(np.dot(-factor * rel, direction)), -own_n))
+    return along * direction
+
+
+def apply_friction(el, pairs, colliders, k_c, k_ec, mu_s, mu_r, dt):
+    """Sequential post-step friction sweep (src/contact.py:303-350): pairs in
+    ascending order correcting both sides, then colliders in order, ascending
+    elements; quaternion rates of touched elements rebuilt from w."""
+    if mu_s == 0.0 and mu_r == 0.0:
+        return
+    p, v = el.p, el.v
+    w = angular_velocity(el.q, el.qdot)
+    touched = np.zeros(el.n, dtype=bool)
+    inertia = 0.4 * el.mass * el.radius**2
+
+    def correct(k, v_rel, w_rel, nrm, fn):
+        if el.pinned[k]:
+            return
+        v_t = v_rel - float(np.dot(v_rel, nrm)) * nrm
+        v[k] += _friction_delta(v_t, v[k], fn, mu_s, el.mass[k], dt)
+        w[k] += _friction_delta(w_rel, w[k], fn, mu_r, inertia[k] / el.radius[k]**3, dt)
+        touched[k] = True
+
+    for a, b in np.asarray(pairs).reshape(-1, 2):
+        d = p[a] - p[b]
+        dist = np.linalg.norm(d)
+        if dist >= el.radius[a] + el.radius[b]:
+            continue
+        nrm = d / dist if dist > 1e-12 else np.array([1.0, 0.0, 0.0])
+        fn = k_ec * dist
+        correct(a, v[a] - v[b], w[a] - w[b], nrm, fn)
+        correct(b, v[b] - v[a], w[b] - w[a], -nrm, fn)
+    for col in colliders:
+        g = collider_sdf(col, p)
+        inside = np.nonzero(g < 0.0)[0]
+        if inside.size == 0:
+            continue
+        grads, _ = collider_grad_hess(col, p[inside])
+        for row, k in enumerate(inside):
+            correct(int(k), v[k], w[k], grads[row], k_c * abs(g[k]) * np.linalg.norm(grads[row]))
+    upd = np.nonzero(touched)[0]
+    if upd.size:
+        el.qdot[upd] = quat_rate(el.q[upd], w[upd])
+
+
 @dataclass
 class OracleState:
     """Minimal scene state the step needs (src/scenes.py:32-77 fields)."""
@@ -836,6 +913,8 @@ class OracleState:
     gravity: np.ndarray = field(default_factory=lambda: np.array([0.0, 0.0, -9.81]))
     k_contact: float = 1e6
     k_element: float = 1e6
+    mu_s: float = 0.0
+    mu_r: float = 0.0
     plastic: object = None
     driver: object = None
     time: float = 0.0
@@ -889,6 +968,9 @@ def step(st: OracleState, cfg) -> StepOut:
         el.p[pin], el.q[pin], el.v[pin], el.qdot[pin] = saved
         return StepOut(res, [], int(pairs.shape[0]), {"kinetic": _kinetic(el)}, False)
     el.p[:], el.q[:], el.v[:], el.qdot[:] = res.p, res.q, v, qd
+    if st.mu_s > 0.0 or st.mu_r > 0.0:                 # src/solver.py:923-925
+        apply_friction(el, pairs, st.colliders, st.k_contact, st.k_element, st.mu_s,
+                       st.mu_r, st.dt)
     events = fracture_update(st.bonds, el.p, el.q, st.youngs, st.plastic)
     if events:
         st.labels = components(el.n, st.bonds)

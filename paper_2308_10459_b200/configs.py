@@ -58,6 +58,8 @@ class SceneSpec:
     k_element: float = 1e6
     plastic: PlasticParams | None = None
     driver: DriverSpec | None = None
+    mu_s: float = 0.0            # sliding friction (scenes.py:46-47)
+    mu_r: float = 0.0            # rolling friction
     epsilon: float = 1e-6
     steps: int = 1
     seed: int = 0
@@ -175,6 +177,47 @@ def cube(n_side=22, r=0.002, youngs=3e9, nu=0.25, density=2500.0, seed=2,
                      epsilon=epsilon, steps=steps, seed=seed, collider_schedule=plane,
                      notes=("random q" if random_q else "identity q")
                      + "; descending HalfSpace at 0.5 m/s; bottom layer pinned")
+
+
+# ---------------------------------------------------------------------------
+# friction scenario (apply_friction, contact.py:303-350)
+# ---------------------------------------------------------------------------
+
+def stack(n=4, r=0.002, youngs=1e7, nu=0.25, density=2500.0, mu_s=0.3, mu_r=0.05,
+          slide=0.3, spin=40.0, k_contact=1e6, k_element=1e6, dt=1e-4, seed=7,
+          steps=8, epsilon=1e-5) -> SceneSpec:
+    """Two unbonded lattice blocks: an n x n x 2 block sunk slightly into a
+    floor HalfSpace and an (n-1) x (n-1) x 2 block nested into the hollows of its top layer,
+    sliding along +x and spinning, with sliding and rolling friction (the
+    regime of scenes.py:239-256's drop-fracture: mu_s 0.2-0.3, mu_r 0.05)."""
+    rng = np.random.default_rng(seed)
+    h = 2.0 * r
+
+    def lattice(nx, nz, origin):
+        g = np.stack(np.meshgrid(np.arange(nx), np.arange(nx), np.arange(nz), indexing="ij"), -1)
+        return origin + h * g.reshape(-1, 3).astype(float)
+
+    lo = lattice(n, 2, np.array([0.0, 0.0, 0.0]))
+    up = lattice(n - 1, 2, np.array([0.5 * h, 0.5 * h, 1.0 * h + 0.69 * h]))
+    pos = np.concatenate([lo, up]) + rng.uniform(-0.02 * r, 0.02 * r, size=(lo.shape[0] + up.shape[0], 3))
+    n_lo = lo.shape[0]
+    npt = pos.shape[0]
+    radius = np.full(npt, r)
+    q = np.tile(Q.IDENTITY, (npt, 1))
+    el = _elements(pos, q, radius, density)
+    el.v[n_lo:, 0] = slide
+    w = np.zeros((npt, 3))
+    w[n_lo:] = spin * rng.normal(size=(npt - n_lo, 3))
+    el.qdot[:] = Q.rate_from_omega(q, w)
+    pairs = np.concatenate([_pairs_within(pos[:n_lo], 1.05 * h),
+                            n_lo + _pairs_within(pos[n_lo:], 1.05 * h)])
+    G = youngs / (2.0 * (1.0 + nu))
+    bonds = build_bonds(pos, radius, pairs, youngs, G)
+    floor = [HalfSpace((0.0, 0.0, 1.0), 0.05 * r)]
+    return SceneSpec("stack", el, bonds, dt, youngs, G, density, colliders=floor,
+                     k_contact=k_contact, k_element=k_element, mu_s=mu_s, mu_r=mu_r,
+                     epsilon=epsilon, steps=steps, seed=seed,
+                     notes="two unbonded blocks, floor contact, sliding + rolling friction")
 
 
 # ---------------------------------------------------------------------------

@@ -9,6 +9,7 @@
 // up to the per-bond arithmetic, bit-identical in summation order.
 #include "bdem_common.cuh"
 #include "bdem_math.cuh"
+#include "colliders.cuh"
 
 namespace bdem {
 
@@ -39,58 +40,6 @@ __device__ __forceinline__ double stage_stretch(const double *st, int64_t nb, in
 #pragma unroll
   for (int t = 0; t < 6; ++t) a[t] = al * (n[pr[t]] * n[pc[t]]) + (pr[t] == pc[t] ? be : 0.0);
   return st[BDEM_ST_KC * nb + b];
-}
-
-// collider SDF value, gradient and Hessian (contact.py:38-133)
-__device__ void collider_eval(const bdem_collider_t &C, const double p[3], double &g,
-                              double dg[3], double H[6]) {
-#pragma unroll
-  for (int t = 0; t < 6; ++t) H[t] = 0.0;
-  if (C.kind == BDEM_COLLIDER_HALFSPACE) {
-    g = ((p[0] * C.a[0] + p[1] * C.a[1]) + p[2] * C.a[2]) - C.a[3];
-    dg[0] = C.a[0]; dg[1] = C.a[1]; dg[2] = C.a[2];
-  } else if (C.kind == BDEM_COLLIDER_SPHERE) {
-    const double d[3] = {p[0] - C.a[0], p[1] - C.a[1], p[2] - C.a[2]};
-    const double r = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
-    const double rs = fmax(r, 1e-12);
-    g = r - C.a[3];
-    double n[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) { n[c] = d[c] / rs; dg[c] = n[c]; }
-    const int pr[6] = {0, 0, 0, 1, 1, 2}, pc[6] = {0, 1, 2, 1, 2, 2};
-#pragma unroll
-    for (int t = 0; t < 6; ++t) H[t] = ((pr[t] == pc[t] ? 1.0 : 0.0) - n[pr[t]] * n[pc[t]]) / rs;
-  } else {  // box
-    double loc[3], d[3], pos[3], sign[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      loc[c] = p[c] - C.a[c];
-      d[c] = fabs(loc[c]) - C.a[3 + c];
-      pos[c] = fmax(d[c], 0.0);
-      sign[c] = loc[c] >= 0.0 ? 1.0 : -1.0;
-    }
-    const double on = sqrt((pos[0] * pos[0] + pos[1] * pos[1]) + pos[2] * pos[2]);
-    const double inside = fmin(fmax(fmax(d[0], d[1]), d[2]), 0.0);
-    g = on + inside;
-    if (on > 0.0) {
-      const double ons = fmax(on, 1e-300);
-      double n[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) { n[c] = sign[c] * pos[c] / ons; dg[c] = n[c]; }
-      const int pr[6] = {0, 0, 0, 1, 1, 2}, pc[6] = {0, 1, 2, 1, 2, 2};
-#pragma unroll
-      for (int t = 0; t < 6; ++t) {
-        const double act = (pr[t] == pc[t] && pos[pr[t]] > 0.0) ? 1.0 : 0.0;
-        H[t] = (act - n[pr[t]] * n[pc[t]]) / ons;
-      }
-    } else {
-      int ax = 0;
-      if (d[1] > d[ax]) ax = 1;
-      if (d[2] > d[ax]) ax = 2;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) dg[c] = (c == ax ? 1.0 : 0.0) * sign[c];
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -193,8 +142,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_element_assemble(bdem_system_t 
     if (s >= 0) {
       const double mp = S.mp_dt2[e], mq = S.mq_dt2[e];
       double dpv[3], dqv[4];
-      const double2 *ph2 = nullptr;
-      (void)ph2;
 #pragma unroll
       for (int c = 0; c < 3; ++c) dpv[c] = pe[c] - S.p_hat[3 * e + c];
       double qh[4];

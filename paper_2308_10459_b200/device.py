@@ -451,6 +451,20 @@ class DeviceSystem:
         return self.h_scalars.numpy()
 
     # ---------------------------------------------------------------- kernels
+    def friction(self, mu_s: float, mu_r: float, dt: float) -> int:
+        """apply_friction (contact.py:303-350) on the device state in place;
+        returns the number of dependency waves the pair sweep used."""
+        need = int(self.lib.bdem_friction_workspace(self.n, self.pair_cap))
+        work = getattr(self, "_fric_work", None)
+        if work is None or work.numel() < need:
+            work = self._fric_work = torch.empty(max(need, 1), dtype=torch.uint8,
+                                                 device=self.device)
+        waves = C.c_int64(0)
+        self.call("bdem_friction", self.sysp, self.p.data_ptr(), self.q.data_ptr(),
+                  self.v.data_ptr(), self.qdot.data_ptr(), float(mu_s), float(mu_r), float(dt),
+                  work.data_ptr(), C.byref(waves), self.stream)
+        return int(waves.value)
+
     def call(self, name, *args):
         rc = getattr(self.lib, name)(*args)
         self.launches += 1

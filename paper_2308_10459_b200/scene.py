@@ -183,4 +183,5 @@ class Scene:
                    gravity=spec.gravity, dt=spec.dt, youngs=spec.youngs,
                    shear_modulus=spec.shear_modulus, density=spec.density,
                    k_contact=spec.k_contact, k_element=spec.k_element, plastic=spec.plastic,
-                   driver=driver_from_spec(spec.driver), host_sync=host_sync)
+                   driver=driver_from_spec(spec.driver), mu_s=spec.mu_s, mu_r=spec.mu_r,
+                   host_sync=host_sync)

@@ -221,8 +221,6 @@ def stable_step(scene, cfg: SolverConfig, method: str = "second-order") -> StepR
     """Advance ``scene`` by one implicit step on the GPU (solver.py:881-939)."""
     if method not in MINIMIZERS:
         raise ValueError(f"the GPU path implements {sorted(MINIMIZERS)}, got {method!r}")
-    if scene.mu_s > 0.0 or scene.mu_r > 0.0:
-        raise NotImplementedError("apply_friction (mu > 0) is outside the GPU hot path")
     dev = scene.device
     if scene.host_sync:
         dev.upload_elements(scene.elements, scene.p_prev, scene.q_prev)
@@ -263,6 +261,8 @@ def stable_step(scene, cfg: SolverConfig, method: str = "second-order") -> StepR
              dev.qdot.data_ptr(), st)
     dev.p.copy_(result.p)
     dev.q.copy_(result.q)
+    if scene.mu_s > 0.0 or scene.mu_r > 0.0:         # solver.py:923-925
+        dev.friction(scene.mu_s, scene.mu_r, scene.dt)
 
     events = _device_bond_update(dev, scene.youngs, scene.plastic)
     if events:

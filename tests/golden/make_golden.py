@@ -72,7 +72,7 @@ def ref_scene(spec, driver=None, colliders=None):
                     gravity=np.array(spec.gravity), dt=spec.dt, youngs=spec.youngs,
                     shear_modulus=spec.shear_modulus, density=spec.density,
                     k_contact=spec.k_contact, k_element=spec.k_element,
-                    plastic=spec.plastic, driver=driver,
+                    plastic=spec.plastic, driver=driver, mu_s=spec.mu_s, mu_r=spec.mu_r,
                     surface_flags=np.zeros(el.n, dtype=bool))
 
 
@@ -320,7 +320,8 @@ def _run_traj(name, spec, steps, eps, driver=None, schedule=None, max_iter=300):
                                            "plastic_strain", "sigma", "tau")))
     out["labels"] = sc.labels.labels
     out.update({"dt": spec.dt, "youngs": spec.youngs, "epsilon": eps, "k_contact": spec.k_contact,
-                "k_element": spec.k_element, "gravity": np.array(spec.gravity)})
+                "k_element": spec.k_element, "gravity": np.array(spec.gravity),
+                "mu_s": spec.mu_s, "mu_r": spec.mu_r})
     if spec.plastic is not None:
         pl = spec.plastic
         out["plastic"] = np.array([pl.fracture_strain, pl.yield_strain, pl.weakening,
@@ -389,6 +390,42 @@ def gold_fracture():
     save("fracture.npz", **out)
 
 
+def gold_friction():
+    """apply_friction (contact.py:303-350) on a dense random cloud: long
+    dependency chains through shared elements, pinned elements, radial qdot
+    components, and all three collider kinds; plus a stacked-blocks
+    trajectory through stable_step with mu_s, mu_r > 0 (solver.py:923-925)."""
+    rng = np.random.default_rng(81)
+    n = 600
+    pos = rng.uniform(-0.03, 0.03, size=(n, 3))
+    rad = rng.uniform(0.003, 0.006, size=n)
+    q = quat_normalize(rng.normal(size=(n, 4)))
+    v = rng.normal(size=(n, 3))
+    v[rng.random(n) < 0.05] = 0.0
+    qdot = rng.normal(size=(n, 4))                   # includes a radial part
+    mass = 2500.0 * (4.0 / 3.0) * np.pi * rad**3
+    pinned = rng.random(n) < 0.1
+    el = re_.ElementSet(pos.copy(), q.copy(), v.copy(), qdot.copy(), mass.copy(), rad.copy(),
+                        pinned.copy())
+    pairs = rc.broad_phase(pos, rad, 2.0 * rad.max() + 1e-12)
+    cols = [rc.HalfSpace((0.0, 0.0, 1.0), -0.02), rc.SphereCollider((0.01, 0.0, 0.0), 0.012),
+            rc.BoxCollider((-0.02, 0.01, 0.0), (0.008, 0.01, 0.03))]
+    k_c, k_ec, mu_s, mu_r, dt = 3e5, 2e5, 0.3, 0.05, 1e-4
+    rc.apply_friction(el, pairs, cols, k_c, k_ec, mu_s, mu_r, dt)
+    out = {"p": pos, "q": q, "v": v, "qdot": qdot, "mass": mass, "radius": rad,
+           "pinned": pinned, "pairs": pairs, "halfspace": np.array([0.0, 0.0, 1.0, -0.02]),
+           "sphere": np.array([0.01, 0.0, 0.0, 0.012]),
+           "box": np.array([-0.02, 0.01, 0.0, 0.008, 0.01, 0.03]),
+           "k_c": k_c, "k_ec": k_ec, "mu_s": mu_s, "mu_r": mu_r, "dt": dt,
+           "v_out": el.v, "qdot_out": el.qdot}
+    d = np.linalg.norm(pos[pairs[:, 0]] - pos[pairs[:, 1]], axis=1)
+    print(f"  friction: {pairs.shape[0]} pairs, {int((d < rad[pairs[:, 0]] + rad[pairs[:, 1]]).sum())}"
+          f" in contact")
+    save("friction.npz", **out)
+    spec = C.stack()
+    _run_traj("stack", spec, spec.steps, spec.epsilon)
+
+
 def gold_broadphase_labels():
     rng = np.random.default_rng(51)
     out = {}
@@ -409,7 +446,7 @@ def gold_broadphase_labels():
 if __name__ == "__main__":
     t = time.time()
     which = sys.argv[1:] or ["bond_terms", "fracture", "broadphase_labels", "newton_pieces",
-                             "newton_solve", "colliders", "runner", "trajectories"]
+                             "newton_solve", "colliders", "runner", "trajectories", "friction"]
     for name in which:
         globals()[f"gold_{name}"]()
     print(f"done in {time.time() - t:.1f}s")

@@ -275,7 +275,7 @@ def test_newton_solve_vs_golden(cuda_ok):
 # step level (solver.py:881-939)
 # ---------------------------------------------------------------------------
 
-@pytest.mark.parametrize("name", ["cantilever", "rope", "plate", "cube"])
+@pytest.mark.parametrize("name", ["cantilever", "rope", "plate", "cube", "stack"])
 def test_trajectory_vs_golden(cuda_ok, name):
     from paper_2308_10459_b200 import HalfSpace, PlasticParams, Scene, SolverConfig, stable_step
     from paper_2308_10459_b200 import configs as C
@@ -294,10 +294,13 @@ def test_trajectory_vs_golden(cuda_ok, name):
         sched = spec.collider_schedule
     if name == "plate":
         cols = [HalfSpace((0.0, 0.0, 1.0), 0.0)]
+    if name == "stack":
+        cols = C.stack().colliders
     plastic = PlasticParams(*d["plastic"]) if "plastic" in d else None
     scene = Scene(name, el, b, colliders=cols, gravity=d["gravity"], dt=float(d["dt"]),
                   youngs=float(d["youngs"]), k_contact=float(d["k_contact"]),
-                  k_element=float(d["k_element"]), plastic=plastic, driver=driver)
+                  k_element=float(d["k_element"]), plastic=plastic, driver=driver,
+                  mu_s=float(d.get("mu_s", 0.0)), mu_r=float(d.get("mu_r", 0.0)))
     cfg = SolverConfig(epsilon=float(d["epsilon"]), max_iterations=300)
     m_dt2 = (el.mass / float(d["dt"]) ** 2).min()
     atol_p = max(10 * float(d["epsilon"]) / m_dt2, 1e-12)
@@ -503,3 +506,76 @@ def test_runner_step_failure(cuda_ok):
         run_simulation(scene, SolverConfig(epsilon=1e-7, max_iterations=3), frames=3, fps=500,
                        write_meshes=False)
     assert str(exc.value) == str(d["fail_msg"])
+
+
+# ---------------------------------------------------------------------------
+# post-step friction (contact.py:303-350) through the C-ABI
+# ---------------------------------------------------------------------------
+
+def test_friction_sweep_vs_golden(cuda_ok):
+    import torch
+
+    from paper_2308_10459_b200 import Scene
+    from paper_2308_10459_b200 import configs as C
+    from test_oracle_golden import friction_inputs
+    d = load("friction.npz")
+    el, cols = friction_inputs(d)
+    b = C.build_bonds(el.p, el.radius, np.zeros((0, 2), dtype=np.int64), 1e7, 4e6)
+    scene = Scene("friction", el, b, colliders=cols, k_contact=float(d["k_c"]),
+                  k_element=float(d["k_ec"]), host_sync=False)
+    dev = scene.device
+    dev.set_physics(scene.gravity, scene.k_contact, scene.k_element, cols)
+    dev.set_pairs(torch.as_tensor(d["pairs"], dtype=torch.int32, device="cuda"))
+    before = dev.lib.bdem_launch_count()
+    waves = dev.friction(float(d["mu_s"]), float(d["mu_r"]), float(d["dt"]))
+    torch.cuda.synchronize()
+    assert dev.lib.bdem_launch_count() > before
+    assert 1 < waves < d["pairs"].shape[0]            # chained, yet parallel
+    _assert_close(dev.v.cpu().numpy(), d["v_out"], 1e-12, 1e-14, "v")
+    _assert_close(dev.qdot.cpu().numpy(), d["qdot_out"], 1e-12, 1e-14, "qdot")
+    # mu = 0 is a no-op, like the reference
+    v0 = dev.v.clone()
+    dev.friction(0.0, 0.0, float(d["dt"]))
+    assert torch.equal(v0, dev.v)
+
+
+def test_friction_large_wave_path_vs_oracle(cuda_ok):
+    """A contact set whose first wave exceeds the single-CTA threshold
+    (kWaveBig = 8192 pairs), so the grid-wide wave launch runs as well as the
+    single-CTA runs of small waves."""
+    import ctypes
+
+    import torch
+
+    from oracle import cpu_oracle as O
+    from paper_2308_10459_b200 import Scene
+    from paper_2308_10459_b200 import configs as C
+    from paper_2308_10459_b200.colliders import HalfSpace
+    from paper_2308_10459_b200.state import ElementSet
+    rng = np.random.default_rng(91)
+    n = 40_000
+    pos = rng.uniform(-2e-4, 2e-4, size=(n, 3))        # every listed pair touches
+    rad = np.full(n, 0.001)
+    el = ElementSet(pos, O.unit(rng.normal(size=(n, 4))), rng.normal(size=(n, 3)),
+                    rng.normal(size=(n, 4)) * 0.1, np.full(n, 1e-5), rad, rng.random(n) < 0.02)
+    k = np.arange(n // 2)
+    pairs = np.concatenate([np.stack([2 * k, 2 * k + 1], 1), np.stack([k, k + n // 2], 1)])
+    pairs = pairs[np.lexsort((pairs[:, 1], pairs[:, 0]))].astype(np.int32)
+    cols = [HalfSpace((0.0, 0.0, 1.0), 0.0)]
+    ref = el.copy()
+    O.apply_friction(ref, pairs, cols, 1e5, 1e5, 0.4, 0.1, 1e-4)
+    b = C.build_bonds(pos, rad, np.zeros((0, 2), dtype=np.int64), 1e7, 4e6)
+    scene = Scene("cluster", el, b, colliders=cols, k_contact=1e5, k_element=1e5,
+                  host_sync=False)
+    dev = scene.device
+    order = np.zeros(pairs.shape[0], dtype=np.int32)
+    wptr = np.zeros(pairs.shape[0] + 1, dtype=np.int32)
+    depth = dev.lib.bdem_friction_schedule(pairs.ctypes.data_as(ctypes.c_void_p), pairs.shape[0],
+                                           n, order.ctypes.data_as(ctypes.c_void_p),
+                                           wptr.ctypes.data_as(ctypes.c_void_p))
+    assert np.diff(wptr[:depth + 1]).max() >= 8192 and depth > 2
+    dev.set_physics(scene.gravity, 1e5, 1e5, cols)
+    dev.set_pairs(torch.as_tensor(pairs, device="cuda"))
+    assert dev.friction(0.4, 0.1, 1e-4) == depth
+    _assert_close(dev.v.cpu().numpy(), ref.v, 1e-12, 1e-14, "v")
+    _assert_close(dev.qdot.cpu().numpy(), ref.qdot, 1e-12, 1e-14, "qdot")

@@ -129,12 +129,16 @@ def _oracle_state(d, name, spec_driver=None):
     cols = []
     if name == "plate":
         cols = [HalfSpace((0.0, 0.0, 1.0), 0.0)]
+    if name == "stack":
+        from paper_2308_10459_b200 import configs as C
+        cols = C.stack().colliders
     return O.OracleState(el, b, float(d["dt"]), float(d["youngs"]), colliders=cols,
                          gravity=d["gravity"], k_contact=float(d["k_contact"]),
-                         k_element=float(d["k_element"]), plastic=plastic, driver=spec_driver)
+                         k_element=float(d["k_element"]), plastic=plastic, driver=spec_driver,
+                         mu_s=float(d.get("mu_s", 0.0)), mu_r=float(d.get("mu_r", 0.0)))
 
 
-@pytest.mark.parametrize("name", ["cantilever", "rope", "plate", "cube"])
+@pytest.mark.parametrize("name", ["cantilever", "rope", "plate", "cube", "stack"])
 def test_trajectory(name):
     from paper_2308_10459_b200 import configs as C
     d = load(f"traj_{name}.npz")
@@ -185,3 +189,26 @@ def test_sphere_box_colliders():
     mat, diag = O.reduced_system(pc, obj.free)
     _assert_close(diag, d["diag"], 1e-11, 1e-12 * np.abs(d["diag"]).max(), "diag")
     assert int(d["n_indef"]) > 0
+
+
+def friction_inputs(d):
+    """Host containers for friction.npz (contact.py:303-350 inputs)."""
+    from paper_2308_10459_b200.colliders import BoxCollider, SphereCollider
+    from paper_2308_10459_b200.state import ElementSet
+    el = ElementSet(d["p"].copy(), d["q"].copy(), d["v"].copy(), d["qdot"].copy(),
+                    d["mass"].copy(), d["radius"].copy(), d["pinned"].copy())
+    hs, sp, bx = d["halfspace"], d["sphere"], d["box"]
+    cols = [HalfSpace(tuple(hs[:3]), float(hs[3])), SphereCollider(tuple(sp[:3]), float(sp[3])),
+            BoxCollider(tuple(bx[:3]), tuple(bx[3:]))]
+    return el, cols
+
+
+def test_friction_sweep():
+    d = load("friction.npz")
+    el, cols = friction_inputs(d)
+    O.apply_friction(el, d["pairs"], cols, float(d["k_c"]), float(d["k_ec"]), float(d["mu_s"]),
+                     float(d["mu_r"]), float(d["dt"]))
+    _assert_close(el.v, d["v_out"], 1e-13, 1e-15, "v")
+    _assert_close(el.qdot, d["qdot_out"], 1e-13, 1e-15, "qdot")
+    assert not np.array_equal(d["v_out"], d["v"])          # the sweep did work
+    assert np.array_equal(el.v[el.pinned], d["v"][el.pinned])
