@@ -83,16 +83,26 @@ enum {
 /* per-bond staging written by bdem_bond_assemble (each n_bond doubles) */
 enum {
   BDEM_ST_E = 0,     /* bond energy                                   */
-  BDEM_ST_N = 1,     /* unit bond direction n [3]                     */
-  BDEM_ST_KC = 4,    /* k c: dE/dp_j = kc n, dE/dp_i = -kc n          */
-  BDEM_ST_ALPHA = 5, /* clamped stretch block a+ = alpha n n^T + beta I */
-  BDEM_ST_BETA = 6,  /*   (off-diagonal coupling -a+)                 */
-  BDEM_ST_GQI = 7,   /* d E / d q_i [4]                               */
-  BDEM_ST_GQJ = 11,  /* d E / d q_j [4]                               */
-  BDEM_ST_C = 15,    /* clamped reduced rotation block (i,j) quadrant, 3x3 row-major */
-  BDEM_ST_A = 24,    /* clamped (i,i) rotation quadrant (sym 6)        */
-  BDEM_ST_D = 30,    /* clamped (j,j) rotation quadrant (sym 6)        */
-  BDEM_ST_COUNT = 36
+  BDEM_ST_KC = 1,    /* k c: dE/dp_j = kc n, dE/dp_i = -kc n          */
+  BDEM_ST_GQI = 2,   /* d E / d q_i [4]                               */
+  BDEM_ST_GQJ = 6,   /* d E / d q_j [4]                               */
+  BDEM_ST_A = 10,    /* clamped (i,i) rotation quadrant (sym 6)        */
+  BDEM_ST_D = 16,    /* clamped (j,j) rotation quadrant (sym 6)        */
+  BDEM_ST_COUNT = 22
+};
+
+/* Off-diagonal coupling coefficients of a bond, read by the SpMV: stored
+ * AoSoA-32 in sys->scoef -- coefficient k of position pos at
+ * scoef[(pos & ~31) * BDEM_CF_COUNT + 32 k + (pos & 31)], so the 14 planes of
+ * one 32-position slot are one contiguous 3.5 KB block (a warp's slot reads
+ * stay 256-byte coalesced and touch one page) and the positions of
+ * consecutive slices are one contiguous range (one bulk copy per SpMV tile). */
+enum {
+  BDEM_CF_N = 0,     /* unit bond direction n [3]                     */
+  BDEM_CF_ALPHA = 3, /* clamped stretch block a+ = alpha n n^T + beta I */
+  BDEM_CF_BETA = 4,  /*   (off-diagonal coupling -a+)                 */
+  BDEM_CF_C = 5,     /* clamped reduced rotation block (i,j) quadrant, 3x3 row-major */
+  BDEM_CF_COUNT = 14
 };
 
 /* per-pair staging (each pair_cap doubles) */
@@ -149,6 +159,8 @@ typedef struct {
   int64_t n_elem, n_free, n_bond, n_pair, pair_cap;
   int64_t vstride;               /* plane stride of reduced vectors and diag/minv:
                                     n_free rounded up to 32 (256-B aligned planes) */
+  int64_t sell_kmax;             /* max i-role slots of any slice               */
+  int64_t sell_kjmax;            /* max j-role slots of any slice               */
   /* element data (device) */
   const double *mass, *radius;
   const double *mp_dt2, *mq_dt2; /* m/dt^2, 1.6 m r^2/dt^2; 0 when pinned */
@@ -162,10 +174,14 @@ typedef struct {
   double *bstate;                /* BDEM_BS_COUNT planes                */
   /* SELL-32 bond layout.  Every per-bond plane (geometry, state, staging,
    * bond_i/j, status) is indexed by POSITION, not by the caller's bond id.
-   * Elements are cut into slices of 32 consecutive ids; slice s owns the
-   * positions [slice_base[s], slice_base[s+1]), laid out slot-major
-   * (pos = slice_base[s] + 32 k + (e & 31)), slot k = the k-th bond with
-   * i == e in ascending bond id (np.add.at order, integrator.py:100-103).
+   * Elements are placed in SELL rows (row_elem / elem_row: a spatially
+   * compact Z-order of the initial positions) and rows are cut into slices
+   * of 32; slice s owns the positions [slice_base[s], slice_base[s+1]),
+   * laid out slot-major (pos = slice_base[s] + 32 k + (row & 31)), slot k =
+   * the k-th bond with i == e in ascending bond id (np.add.at order,
+   * integrator.py:100-103).  Free slots (reduced-vector indices) are
+   * numbered in row order, so the rows of a slice own the consecutive slots
+   * [slice_slot[s], slice_slot[s+1]).
    * Padding positions have status BROKEN.  n_bond is the padded length.
    * The j-role lists use the same shape: jpos[jslice_base[s] + 32 k + lane]
    * is the position of the k-th bond with j == e (ascending id), -1 pad. */
@@ -174,11 +190,19 @@ typedef struct {
   const int32_t *jslice_base;    /* (n_slices + 1)                      */
   const int32_t *jpos;           /* position of a j-role bond, -1 pad   */
   const int32_t *jslot;          /* free slot of its i end, -1          */
+  const int32_t *row_elem;       /* (n_slices * 32) element of a row, -1 pad */
+  const int32_t *elem_row;       /* (n_elem) row of an element          */
+  const int32_t *slice_slot;     /* (n_slices + 1) first free slot of a slice */
+  const int32_t *row_slot;       /* (n_slices * 32) free slot of a row, -1 pinned/pad */
+  const int32_t *tile_hdr;       /* per SpMV tile (bdem_spmv_tile_slices() slices):
+                                    BDEM_TILE_HDR ints = slice_base[t0..t0+TS],
+                                    jslice_base[t0..t0+TS], slice_slot[t0], slice_slot[t1] */
   /* contact pairs (sorted i<j); pairs with i == e are [pi_ptr[e], pi_ptr[e+1]),
    * pairs with j == e are pj_idx[pj_ptr[e] .. pj_ptr[e+1]) ascending */
   const int32_t *pair_i, *pair_j, *pi_ptr, *pj_ptr, *pj_idx;
   /* staging / workspace */
   double *stage;                 /* BDEM_ST_COUNT planes x n_bond      */
+  double *scoef;                 /* BDEM_CF_COUNT x n_bond, AoSoA-32    */
   double *pstage;                /* BDEM_PS_COUNT planes x pair_cap    */
   double *diag;                  /* 12 planes x n_free: P sym6, R sym6  */
   double *minv;                  /* 12 planes x n_free: P^-1, R^-1      */
@@ -306,6 +330,15 @@ int bdem_finish_step(const bdem_system_t *sys, const double *p, const double *q,
  * solver.py:198-258, applied as `mat @ v`, solver.py:475).  Also writes the
  * per-block partials of x.y, |y|^2, |x|^2 for PCG. */
 int bdem_spmv(const bdem_system_t *sys, const double *x, double *y, void *stream);
+/* SpMV kernel variant for every later SpMV launch: 0 = slot-parallel
+ * (default), 1 = tiled (cp.async.bulk + mbarrier ring, warp-specialised
+ * producer; pays off only with compact tiles, BDEM_ROW_ORDER=z).  Returns the
+ * previous variant; any other value only queries.  BDEM_SPMV_TILE=1 in the
+ * environment selects the tiled one at load time. */
+int bdem_spmv_set_kernel(int kernel);
+/* Slices per tile of the tiled SpMV and the int32 stride of sys->tile_hdr. */
+int bdem_spmv_tile_slices(void);
+int bdem_spmv_tile_hdr_ints(void);
 
 /* PCG (linalg.py:40-97) on device state sys->pcg; see pcg_kernels.cu. */
 int bdem_pcg_init(const bdem_system_t *sys, const double *b, double sign, double *x,

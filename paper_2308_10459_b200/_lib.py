@@ -20,7 +20,8 @@ ERRSLOT_COUNT = 8
 BG = dict(L0=0, D0=1, FRAME=4, KN=13, KT=14, KDIAG=15, RADIUS=18, SECTION=19, SECOND=20,
           POLAR=21, TENSILE=22, SHEAR=23, COUNT=24)
 BS = dict(SCALE=0, DAMAGE=1, PLASTIC=2, SIGMA=3, TAU=4, COUNT=5)
-ST = dict(E=0, N=1, KC=4, ALPHA=5, BETA=6, GQI=7, GQJ=11, C=15, A=24, D=30, COUNT=36)
+ST = dict(E=0, KC=1, GQI=2, GQJ=6, A=10, D=16, COUNT=22)
+CF = dict(N=0, ALPHA=3, BETA=4, C=5, COUNT=14)
 PS = dict(E=0, GI=1, A=4, COUNT=10)
 SC = dict(F=0, GNORM2=1, CNORM2=2, MAXDEV=3, SLOPE=4, FT=5, NSING=6, EBOND=7, ECOL=8, EGRAV=9,
           EKIN=10, EPAIR=11, COUNT=32)
@@ -42,12 +43,15 @@ class System(C.Structure):
     _fields_ = [
         ("n_elem", C.c_int64), ("n_free", C.c_int64), ("n_bond", C.c_int64),
         ("n_pair", C.c_int64), ("pair_cap", C.c_int64), ("vstride", C.c_int64),
+        ("sell_kmax", C.c_int64), ("sell_kjmax", C.c_int64),
         ("mass", _p), ("radius", _p), ("mp_dt2", _p), ("mq_dt2", _p), ("p_hat", _p),
         ("q_hat", _p), ("slot", _p), ("free_elem", _p),
         ("bond_i", _p), ("bond_j", _p), ("status", _p), ("geom", _p), ("bstate", _p),
         ("slice_base", _p), ("pos_oslot", _p), ("jslice_base", _p), ("jpos", _p), ("jslot", _p),
+        ("row_elem", _p), ("elem_row", _p), ("slice_slot", _p), ("row_slot", _p),
+        ("tile_hdr", _p),
         ("pair_i", _p), ("pair_j", _p), ("pi_ptr", _p), ("pj_ptr", _p), ("pj_idx", _p),
-        ("stage", _p), ("pstage", _p), ("diag", _p), ("minv", _p), ("red", _p),
+        ("stage", _p), ("scoef", _p), ("pstage", _p), ("diag", _p), ("minv", _p), ("red", _p),
         ("scalars", _p), ("pcg", _p), ("err", _p), ("counter", _p), ("clamp_list", _p),
         ("gravity", C.c_double * 3), ("k_contact", C.c_double), ("k_element", C.c_double),
         ("n_colliders", C.c_int32), ("pad_", C.c_int32),
@@ -93,6 +97,9 @@ SIGNATURES = {
     "bdem_components": (_int, [_i64, _i64, _p, _p, _p, _p, _p, C.POINTER(C.c_int64), _p]),
     "bdem_select_workspace": (_i64, [_i64]),
     "bdem_select_flagged": (_int, [_p, _i64, _p, _p, C.POINTER(C.c_int64), _p]),
+    "bdem_spmv_set_kernel": (_int, [_int]),
+    "bdem_spmv_tile_slices": (_int, []),
+    "bdem_spmv_tile_hdr_ints": (_int, []),
     "bdem_friction_workspace": (_i64, [_i64, _i64]),
     "bdem_friction": (_int, [_p, _p, _p, _p, _p, _dbl, _dbl, _dbl, _p, C.POINTER(C.c_int64), _p]),
     "bdem_friction_schedule": (_i64, [_p, _i64, _i64, _p, _p]),

@@ -11,6 +11,31 @@ constexpr int kRedBlocks = BDEM_RED_BLOCKS;
 constexpr int kClampCounter = 5;  // sys->counter slot: queued indefinite blocks
 constexpr int kThreads = 256;
 
+// index of coefficient k of position pos in sys->scoef (AoSoA-32, see BDEM_CF_*)
+__host__ __device__ __forceinline__ int64_t cf_idx(int64_t pos, int k) {
+  return (pos & ~int64_t(31)) * BDEM_CF_COUNT + 32 * k + (pos & 31);
+}
+
+// the 14 coupling coefficients of one position (plane stride 32 doubles)
+struct Coef {
+  double n[3], al, be, C[9];
+};
+template <bool kGlobal>
+__device__ __forceinline__ Coef load_coef(const double *base) {
+  Coef c;
+#pragma unroll
+  for (int t = 0; t < 3; ++t) c.n[t] = kGlobal ? __ldg(base + 32 * (BDEM_CF_N + t)) : base[32 * (BDEM_CF_N + t)];
+  c.al = kGlobal ? __ldg(base + 32 * BDEM_CF_ALPHA) : base[32 * BDEM_CF_ALPHA];
+  c.be = kGlobal ? __ldg(base + 32 * BDEM_CF_BETA) : base[32 * BDEM_CF_BETA];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) c.C[t] = kGlobal ? __ldg(base + 32 * (BDEM_CF_C + t)) : base[32 * (BDEM_CF_C + t)];
+  return c;
+}
+__device__ __forceinline__ void store_coef(double *base, const double v[BDEM_CF_COUNT]) {
+#pragma unroll
+  for (int k = 0; k < BDEM_CF_COUNT; ++k) base[32 * k] = v[k];
+}
+
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // kernels launched by this library (defined in topology_kernels.cu)

@@ -132,9 +132,11 @@ __global__ void __launch_bounds__(128, 4) k_bond_assemble(bdem_system_t S, const
   const int64_t nb = S.n_bond;
   if (b >= nb) return;
   double *st_out = S.stage;
-  if (S.status[b] == 2) {
+  if (S.status[b] == 2) {  // broken or padding: no energy, no coupling
 #pragma unroll
     for (int k = 0; k < BDEM_ST_COUNT; ++k) st_out[k * nb + b] = 0.0;
+    const double zero[BDEM_CF_COUNT] = {};
+    store_coef(S.scoef + cf_idx(b, 0), zero);
     return;
   }
   BondIn B;
@@ -161,11 +163,12 @@ __global__ void __launch_bounds__(128, 4) k_bond_assemble(bdem_system_t S, const
   const RotOut ro = reduced_rotation(qi, qj, B.d0, B.F, kds, sh, S6);
 
   st_out[BDEM_ST_E * nb + b] = (st.E + sh.E) + ro.E_b;
+  double cfv[BDEM_CF_COUNT];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) st_out[(BDEM_ST_N + c) * nb + b] = st.n[c];
+  for (int c = 0; c < 3; ++c) cfv[BDEM_CF_N + c] = st.n[c];
   st_out[BDEM_ST_KC * nb + b] = st.kc;
-  st_out[BDEM_ST_ALPHA * nb + b] = alpha;
-  st_out[BDEM_ST_BETA * nb + b] = beta;
+  cfv[BDEM_CF_ALPHA] = alpha;
+  cfv[BDEM_CF_BETA] = beta;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     st_out[(BDEM_ST_GQI + c) * nb + b] = sh.g[c] + ro.gbi[c];
@@ -187,7 +190,8 @@ __global__ void __launch_bounds__(128, 4) k_bond_assemble(bdem_system_t S, const
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) st_out[(BDEM_ST_C + 3 * r + c) * nb + b] = S6[sidx<6>(r, c + 3)];
+    for (int c = 0; c < 3; ++c) cfv[BDEM_CF_C + 3 * r + c] = S6[sidx<6>(r, c + 3)];
+  store_coef(S.scoef + cf_idx(b, 0), cfv);
   const int pr[6] = {0, 0, 0, 1, 1, 2}, pc[6] = {0, 1, 2, 1, 2, 2};
 #pragma unroll
   for (int t = 0; t < 6; ++t) {
@@ -217,7 +221,7 @@ __global__ void __launch_bounds__(128) k_bond_clamp(bdem_system_t S) {
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) A[sidx<6>(r, c + 3)] = st[(BDEM_ST_C + 3 * r + c) * nb + b];
+      for (int c = 0; c < 3; ++c) A[sidx<6>(r, c + 3)] = S.scoef[cf_idx(b, BDEM_CF_C + 3 * r + c)];
     jacobi_clamp_regs<6>(A);
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
@@ -227,7 +231,7 @@ __global__ void __launch_bounds__(128) k_bond_clamp(bdem_system_t S) {
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) st[(BDEM_ST_C + 3 * r + c) * nb + b] = A[sidx<6>(r, c + 3)];
+      for (int c = 0; c < 3; ++c) S.scoef[cf_idx(b, BDEM_CF_C + 3 * r + c)] = A[sidx<6>(r, c + 3)];
   }
 }
 

@@ -31,11 +31,12 @@ __device__ __forceinline__ void store_q(double *q, int64_t e, const double qe[4]
 
 // staged stretch piece of bond position b: returns k c, fills n and the
 // clamped block a+ = alpha n n^T + beta I (sym6)
-__device__ __forceinline__ double stage_stretch(const double *st, int64_t nb, int64_t b,
-                                                double n[3], double a[6]) {
+__device__ __forceinline__ double stage_stretch(const double *st, const double *cf, int64_t nb,
+                                                int64_t b, double n[3], double a[6]) {
+  const double *cb = cf + cf_idx(b, 0);
 #pragma unroll
-  for (int c = 0; c < 3; ++c) n[c] = st[(BDEM_ST_N + c) * nb + b];
-  const double al = st[BDEM_ST_ALPHA * nb + b], be = st[BDEM_ST_BETA * nb + b];
+  for (int c = 0; c < 3; ++c) n[c] = cb[32 * (BDEM_CF_N + c)];
+  const double al = cb[32 * BDEM_CF_ALPHA], be = cb[32 * BDEM_CF_BETA];
   const int pr[6] = {0, 0, 0, 1, 1, 2}, pc[6] = {0, 1, 2, 1, 2, 2};
 #pragma unroll
   for (int t = 0; t < 6; ++t) a[t] = al * (n[pr[t]] * n[pc[t]]) + (pr[t] == pc[t] ? be : 0.0);
@@ -54,19 +55,21 @@ __global__ void __launch_bounds__(kThreads, 2) k_element_assemble(bdem_system_t 
   bool any_col_hess = false;
   for (int i = 0; i < S.n_colliders; ++i) any_col_hess |= S.colliders[i].kind != BDEM_COLLIDER_HALFSPACE;
 
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < S.n_elem;
-       e += (int64_t)gridDim.x * blockDim.x) {
+  // one thread per SELL row (lane = row & 31 keeps the staged reads coalesced)
+  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < S.n_elem;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = S.row_elem[row];
     double pe[3], qe[4];
     load_p(p, e, pe);
     load_q(q, e, qe);
     double gp[3] = {0.0, 0.0, 0.0}, gq[4] = {0.0, 0.0, 0.0, 0.0};
     double P[6] = {0, 0, 0, 0, 0, 0}, R[6] = {0, 0, 0, 0, 0, 0};
     double ebond = 0.0;
-    const int sl = (int)(e >> 5), lane = (int)(e & 31);
+    const int sl = (int)(row >> 5), lane = (int)(row & 31);
     // bonds with i == e: this element's SELL row (padding stages zeros)
     for (int64_t b = S.slice_base[sl] + lane; b < S.slice_base[sl + 1]; b += 32) {
       double n[3], apos[6];
-      const double kc = stage_stretch(st, nb, b, n, apos);
+      const double kc = stage_stretch(st, S.scoef, nb, b, n, apos);
 #pragma unroll
       for (int c = 0; c < 3; ++c) gp[c] += -(kc * n[c]);
 #pragma unroll
@@ -83,7 +86,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_element_assemble(bdem_system_t 
       const int64_t b = S.jpos[k];
       if (b < 0) continue;
       double n[3], apos[6];
-      const double kc = stage_stretch(st, nb, b, n, apos);
+      const double kc = stage_stretch(st, S.scoef, nb, b, n, apos);
 #pragma unroll
       for (int c = 0; c < 3; ++c) gp[c] += kc * n[c];
 #pragma unroll

@@ -14,6 +14,8 @@
 // PCG control flow: every kernel reads sys->pcg[STATE] first and returns if
 // the solve has stopped, so the host can enqueue several iterations ahead
 // and synchronise only once per chunk.
+#include <cstdlib>
+
 #include "bdem_common.cuh"
 #include "bdem_math.cuh"
 
@@ -63,8 +65,8 @@ __device__ __forceinline__ void spmv_tail(const bdem_system_t &S, const double *
                                           double boost, double &acc_xy, double &acc_yy,
                                           double &acc_xx) {
   const int64_t nf = S.vstride;
-  const int64_t e = (int64_t)sl * 32 + lane;
-  const int s = e < S.n_elem ? __ldg(S.slot + e) : -1;
+  const int64_t e = __ldg(S.row_elem + (int64_t)sl * 32 + lane);
+  const int s = e >= 0 ? __ldg(S.slot + e) : -1;
   if (s < 0) return;
   for (int c = w; c < 6; c += W) {
     const int base = c < 3 ? 0 : 3, rr = c - base;
@@ -190,11 +192,12 @@ __device__ __forceinline__ void slot_apply(const bdem_system_t &S, const double 
   const double *st = S.stage;
   double xo[6], n[3], C[9];
   load6_ro(x, r.o, S.vstride, xo);
+  const Coef cv = load_coef<true>(S.scoef + cf_idx(r.b, 0));
 #pragma unroll
-  for (int t = 0; t < 3; ++t) n[t] = __ldg(st + (BDEM_ST_N + t) * nb + r.b);
-  const double al = __ldg(st + BDEM_ST_ALPHA * nb + r.b), be = __ldg(st + BDEM_ST_BETA * nb + r.b);
+  for (int t = 0; t < 3; ++t) n[t] = cv.n[t];
+  const double al = cv.al, be = cv.be;
 #pragma unroll
-  for (int t = 0; t < 9; ++t) C[t] = __ldg(st + (BDEM_ST_C + t) * nb + r.b);
+  for (int t = 0; t < 9; ++t) C[t] = cv.C[t];
   // a+ x = alpha (n.x) n + beta x ; coupling -a+
   const double nx = al * ((n[0] * xo[0] + n[1] * xo[1]) + n[2] * xo[2]);
 #pragma unroll
@@ -479,6 +482,461 @@ __global__ void __launch_bounds__(kThreads) k_pair(bdem_system_t S, const double
   if (threadIdx.x == 0) *red_slot(S.red, BDEM_SC_EPAIR, blockIdx.x) = s;
 }
 
+// ---------------------------------------------------------------------------
+// Tiled SpMV (default).  The slot-parallel kernel above moves ~1.8 GB of L2
+// sectors per plate SpMV -- every bond's coefficients are read twice (i-role
+// stream, j-role gather) plus one neighbour-x gather per slot -- which sits on
+// the chip's L2-slice throughput cap.  Here SELL rows are in Z-order, so a
+// tile of TS slices (TS*32 rows) is a compact patch and most bonds join two
+// rows of the same tile.  Per tile, warp 0 streams the tile's i-role
+// coefficient planes, their neighbour slots and the tile's own x and
+// diagonal blocks into a STAGES-deep shared-memory ring with cp.async.bulk
+// (one transaction-counted mbarrier per stage).  The warps read i-role
+// coefficients from shared memory, and j-role coefficients / neighbour x
+// from shared memory whenever the partner row is inside the tile: only
+// tile-boundary bonds go through L2.  Per-row summation order is the same
+// fixed order as k_spmv (deterministic).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int kTilePlanes = BDEM_CF_COUNT;
+
+// capacities of one stage (host and device agree through this struct)
+struct TileCaps {
+  int cap;   // i-role positions staged
+  int capj;  // j-role list entries staged
+  int xcap;  // slot window (TS*32 + 2 for the 16-byte alignment of the copies)
+  int rows;  // TS*32
+  bool diag; // stage the diagonal blocks too
+  __host__ __device__ int off_x() const { return kTilePlanes * cap; }
+  __host__ __device__ int off_diag() const { return off_x() + 6 * xcap; }
+  __host__ __device__ int off_int() const { return off_diag() + (diag ? 12 * xcap : 0); }
+  // int32 region: oslot[cap] | jslot[capj] | jpos[capj] | rslot[rows]
+  __host__ __device__ int stage_doubles() const {
+    return off_int() + (cap + 2 * capj + rows + 1) / 2;
+  }
+};
+
+// per-stage header, written by the producer before it arrives on the barrier
+template <int TS>
+struct TileHdr {
+  int64_t p0;        // first i-role position of the tile
+  int64_t jb[TS + 1];  // j-role list bounds of the tile's slices
+  int64_t ib[TS + 1];  // i-role position bounds of the tile's slices
+  int ncopy, njcopy, nrows;
+  int s0, s1, xa, xn;
+};
+
+#ifdef BDEM_TILE_PROF
+__device__ unsigned long long g_tile_prof[8];
+#define TPROF_DECL() long long _pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}
+#define TPROF_T0() long long _tp = clock64()
+#define TPROF_MARK(k)                  \
+  do {                                 \
+    const long long _n = clock64();    \
+    _pacc[k] += _n - _tp;              \
+    _tp = _n;                          \
+  } while (0)
+#define TPROF_FLUSH()                                                                    \
+  do {                                                                                   \
+    if (threadIdx.x == 0)                                                                \
+      for (int _k = 0; _k < 6; ++_k) atomicAdd(&g_tile_prof[_k], (unsigned long long)_pacc[_k]); \
+  } while (0)
+#else
+#define TPROF_DECL()
+#define TPROF_T0()
+#define TPROF_MARK(k)
+#define TPROF_FLUSH()
+#endif
+
+// Header words of a tile, one per lane of warp 0 (loaded early so their
+// latency hides under the previous tile's work): lanes 0..TS slice_base,
+// TS+1..2TS+1 jslice_base, 2TS+2 / 2TS+3 slice_slot of the first / end slice.
+// header record of a tile (host-built, BDEM_TILE_HDR ints, 16-byte multiple)
+template <int TS>
+struct TileHdrWords {
+  static constexpr int kInts = (2 * (TS + 1) + 2 + 3) & ~3;
+};
+template <int TS>
+__device__ __forceinline__ int64_t tile_hdr_word_g(const bdem_system_t &S, int tile, int lane) {
+  return lane < TileHdrWords<TS>::kInts
+             ? __ldg(S.tile_hdr + (int64_t)tile * TileHdrWords<TS>::kInts + lane)
+             : 0;
+}
+
+// warp 0 fills one stage: header + every bulk copy of the tile (copy q by
+// lane q % 32): 0..13 coefficient planes, 14..19 x planes, 20..31 diagonal
+// planes, 32 oslot, 33 jslot, 34 jpos, 35 row slots
+template <int TS>
+__device__ __forceinline__ void tile_issue(const bdem_system_t &S, const double *x, int tile,
+                                           int ns, const TileCaps &cp, double *buf,
+                                           TileHdr<TS> *hdr, uint64_t *bar, int lane,
+                                           int64_t word, int next_tile, int32_t *next_words) {
+  const int64_t vs = S.vstride;
+  const int t0 = tile * TS, t1 = min(ns, t0 + TS);
+  TileHdr<TS> h;
+#pragma unroll
+  for (int t = 0; t <= TS; ++t) {
+    h.ib[t] = __shfl_sync(0xffffffffu, word, t);
+    h.jb[t] = __shfl_sync(0xffffffffu, word, TS + 1 + t);
+  }
+  h.s0 = (int)__shfl_sync(0xffffffffu, word, 2 * TS + 2);
+  h.s1 = (int)__shfl_sync(0xffffffffu, word, 2 * TS + 3);
+  h.p0 = h.ib[0];
+  h.ncopy = (int)min(h.ib[TS] - h.p0, (int64_t)cp.cap);
+  h.njcopy = (int)min(h.jb[TS] - h.jb[0], (int64_t)cp.capj);
+  h.nrows = (t1 - t0) * 32;
+  h.xa = h.s0 & ~1;
+  h.xn = (h.s1 - h.xa + 1) & ~1;
+  const uint32_t cb = 8u * h.ncopy, xb = 8u * h.xn, jb = 4u * h.njcopy;
+  const uint32_t hb = next_tile >= 0 ? 4u * TileHdrWords<TS>::kInts : 0u;
+  const uint32_t total = kTilePlanes * cb + (cp.diag ? 18u : 6u) * xb + 4u * h.ncopy + 2u * jb +
+                         4u * h.nrows + hb;
+  if (lane == 0) {
+    *hdr = h;
+#ifndef BDEM_TILE_NOFENCE
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
+    mbar_arrive_expect_tx(bar, total);
+  }
+  __syncwarp();
+  // lane 0: the tile's AoSoA-32 coefficient block (one contiguous range);
+  // 1..6 x planes, 7..18 diagonal planes, 19..22 slot / j-list / row indices
+  int *ib = reinterpret_cast<int *>(buf + cp.off_int());
+  const int q = lane;
+  if (q == 0) {
+    if (cb) bulk_g2s(buf, S.scoef + h.p0 * kTilePlanes, kTilePlanes * cb, bar);
+  } else if (q <= 6) {
+    if (xb) bulk_g2s(buf + cp.off_x() + (q - 1) * cp.xcap, x + (q - 1) * vs + h.xa, xb, bar);
+  } else if (q <= 18) {
+    if (cp.diag && xb)
+      bulk_g2s(buf + cp.off_diag() + (q - 7) * cp.xcap, S.diag + (q - 7) * vs + h.xa, xb, bar);
+  } else if (q == 19) {
+    if (cb) bulk_g2s(ib, S.pos_oslot + h.p0, 4u * h.ncopy, bar);
+  } else if (q == 20) {
+    if (jb) bulk_g2s(ib + cp.cap, S.jslot + h.jb[0], jb, bar);
+  } else if (q == 21) {
+    if (jb) bulk_g2s(ib + cp.cap + cp.capj, S.jpos + h.jb[0], jb, bar);
+  } else if (q == 22) {
+    bulk_g2s(ib + cp.cap + 2 * cp.capj, S.row_slot + (int64_t)t0 * 32, 4u * h.nrows, bar);
+  } else if (q == 23) {
+    // the header of the next tile this stage will be refilled with
+    if (hb) bulk_g2s(next_words, S.tile_hdr + (int64_t)next_tile * TileHdrWords<TS>::kInts, hb, bar);
+  }
+}
+
+
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// named barrier among the NW consumer warps (the producer warp never joins)
+__device__ __forceinline__ void consumers_sync(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+// Warp-specialised: warps 0..NW-1 consume tiles, warp NW produces them.  The
+// producer refills stage s as soon as every consumer warp has arrived on
+// empty[s], so copy issue never sits on the consumers' critical path.
+template <int TS, int NW, int STAGES, int MINB>
+__global__ void __launch_bounds__((NW + 1) * 32, MINB)
+    k_spmv_tile(bdem_system_t S, const double *__restrict__ x, double *__restrict__ y, int mode,
+                TileCaps cp) {
+  extern __shared__ __align__(128) double tsm[];
+  __shared__ double part[NW][6][32];
+  __shared__ double sh[NW + 1];
+  __shared__ TileHdr<TS> hdrs[STAGES];
+  __shared__ __align__(16) int32_t hnext[STAGES][TileHdrWords<TS>::kInts];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  double *pcg = S.pcg;
+  if (mode == 1 && pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
+  const double boost = mode == 1 ? pcg[BDEM_PCG_BOOST] : 0.0;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t vs = S.vstride;
+  const int ns = (int)((S.n_elem + 31) >> 5);
+  const int ntiles = (ns + TS - 1) / TS;
+  const int sd = cp.stage_doubles();
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < STAGES; ++k) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double acc_xy = 0.0, acc_yy = 0.0, acc_xx = 0.0;
+  if (w == NW) {
+    // ---- producer ----
+    int i = 0;
+#pragma unroll 1
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+      const int stg = i % STAGES;
+      int64_t word;
+      if (i >= STAGES) {
+        mbar_wait(&empty[stg], (uint32_t)(((i / STAGES) - 1) & 1));
+        word = lane < TileHdrWords<TS>::kInts ? hnext[stg][lane] : 0;  // came with stage's copies
+      } else {
+        word = tile_hdr_word_g<TS>(S, tile, lane);
+      }
+      const int nxt = tile + STAGES * gridDim.x;
+      tile_issue<TS>(S, x, tile, ns, cp, tsm + stg * sd, &hdrs[stg], &full[stg], lane, word,
+                     nxt < ntiles ? nxt : -1, hnext[stg]);
+    }
+  } else {
+    // ---- consumers ----
+    TPROF_DECL();
+    const int t_mine = w % TS;   // slice of the tile this warp works on
+    constexpr int WPS = NW / TS;  // warps per slice
+    int it = 0;
+#pragma unroll 1
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int stg = it % STAGES;
+      double *buf = tsm + stg * sd;
+      const double *cf = buf;
+      const double *xs = buf + cp.off_x();
+      const int *osl = reinterpret_cast<const int *>(buf + cp.off_int());
+      const int *jsl = osl + cp.cap;
+      const int *jps = jsl + cp.capj;
+      const int *rsl = jps + cp.capj;
+      TPROF_T0();
+      mbar_wait(&full[stg], (uint32_t)((it / STAGES) & 1));
+      TPROF_MARK(0);
+      const TileHdr<TS> &h = hdrs[stg];
+      const int64_t p0 = h.p0, jb0 = h.jb[0];
+      const int ncopy = h.ncopy, njcopy = h.njcopy, s0 = h.s0, s1 = h.s1, xa = h.xa;
+      const int64_t i0 = h.ib[t_mine], j0 = h.jb[t_mine];
+      const int ki = (int)((h.ib[t_mine + 1] - i0) >> 5), kj = (int)((h.jb[t_mine + 1] - j0) >> 5);
+      double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  #pragma unroll 1
+      for (int k = w / TS; k < ki + kj; k += WPS) {
+        int64_t b;
+        int o;
+        bool tr;
+        if (k < ki) {
+          b = i0 + 32 * k + lane;
+          const int64_t lb = b - p0;
+          o = lb < ncopy ? osl[lb] : __ldg(S.pos_oslot + b);
+          tr = false;
+        } else {
+          const int64_t jk = j0 + 32 * (k - ki) + lane;
+          const int64_t lj = jk - jb0;
+          if (lj < njcopy) {
+            o = jsl[lj];
+            b = jps[lj];
+          } else {
+            o = __ldg(S.jslot + jk);
+            b = __ldg(S.jpos + jk);
+          }
+          tr = true;
+        }
+        if (o < 0) continue;
+        double xo[6], n[3], C[9], al, be;
+        if (o >= s0 && o < s1) {
+  #pragma unroll
+          for (int c = 0; c < 6; ++c) xo[c] = xs[c * cp.xcap + (o - xa)];
+        } else {
+          load6_ro(x, o, vs, xo);
+        }
+        const int64_t lb = b - p0;
+        const bool local = lb >= 0 && lb < ncopy;
+        const double *cb = local ? cf + cf_idx(lb, 0) : S.scoef + cf_idx(b, 0);
+        if (local) {
+  #pragma unroll
+          for (int t = 0; t < 3; ++t) n[t] = cb[32 * (BDEM_CF_N + t)];
+          al = cb[32 * BDEM_CF_ALPHA];
+          be = cb[32 * BDEM_CF_BETA];
+  #pragma unroll
+          for (int t = 0; t < 9; ++t) C[t] = cb[32 * (BDEM_CF_C + t)];
+        } else {
+  #pragma unroll
+          for (int t = 0; t < 3; ++t) n[t] = __ldg(cb + 32 * (BDEM_CF_N + t));
+          al = __ldg(cb + 32 * BDEM_CF_ALPHA);
+          be = __ldg(cb + 32 * BDEM_CF_BETA);
+  #pragma unroll
+          for (int t = 0; t < 9; ++t) C[t] = __ldg(cb + 32 * (BDEM_CF_C + t));
+        }
+        const double nx = al * ((n[0] * xo[0] + n[1] * xo[1]) + n[2] * xo[2]);
+  #pragma unroll
+        for (int c = 0; c < 3; ++c) acc[c] -= nx * n[c] + be * xo[c];
+        if (!tr) {
+  #pragma unroll
+          for (int q = 0; q < 3; ++q)
+            acc[3 + q] += (C[3 * q] * xo[3] + C[3 * q + 1] * xo[4]) + C[3 * q + 2] * xo[5];
+        } else {
+  #pragma unroll
+          for (int q = 0; q < 3; ++q)
+            acc[3 + q] += (C[q] * xo[3] + C[3 + q] * xo[4]) + C[6 + q] * xo[5];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 6; ++q) part[w][q][lane] = acc[q];
+      TPROF_MARK(1);
+      consumers_sync(NW * 32);
+      TPROF_MARK(2);
+      // tail: (slice, component) items; y = D x + partials (fixed warp order) - pairs
+  #pragma unroll 1
+      for (int item = w; item < TS * 6; item += NW) {
+        const int t = item / 6, c = item - 6 * t;
+        if (32 * t >= h.nrows) continue;
+        const int sslot = rsl[32 * t + lane];
+        if (sslot < 0) continue;
+        const int base = c < 3 ? 0 : 3, rr = c - base;
+        const int ls = sslot - xa;
+        double dg0, dg1, dg2;
+        if (cp.diag) {
+          const double *dg = buf + cp.off_diag() + (c < 3 ? 0 : 6 * cp.xcap);
+          dg0 = dg[sidx<3>(rr, 0) * cp.xcap + ls];
+          dg1 = dg[sidx<3>(rr, 1) * cp.xcap + ls];
+          dg2 = dg[sidx<3>(rr, 2) * cp.xcap + ls];
+        } else {
+          const double *dg = S.diag + (c < 3 ? 0 : 6 * vs);
+          dg0 = __ldg(dg + sidx<3>(rr, 0) * vs + sslot);
+          dg1 = __ldg(dg + sidx<3>(rr, 1) * vs + sslot);
+          dg2 = __ldg(dg + sidx<3>(rr, 2) * vs + sslot);
+        }
+        double yc = (dg0 * xs[(base + 0) * cp.xcap + ls] + dg1 * xs[(base + 1) * cp.xcap + ls]) +
+                    dg2 * xs[(base + 2) * cp.xcap + ls];
+  #pragma unroll
+        for (int ww = t; ww < NW; ww += TS) yc += part[ww][c][lane];
+        if (c < 3 && S.n_pair > 0) {
+          const int64_t e = __ldg(S.row_elem + (int64_t)(tile * TS + t) * 32 + lane);
+          const int64_t pc = S.pair_cap;
+          const double *ps = S.pstage;
+          for (int k = S.pi_ptr[e]; k < S.pi_ptr[e + 1]; ++k) {
+            const int o = S.slot[S.pair_j[k]];
+            if (o < 0) continue;
+            yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[0 * vs + o] +
+                   ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[1 * vs + o]) +
+                  ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[2 * vs + o];
+          }
+          for (int kk = S.pj_ptr[e]; kk < S.pj_ptr[e + 1]; ++kk) {
+            const int64_t k = S.pj_idx[kk];
+            const int o = S.slot[S.pair_i[k]];
+            if (o < 0) continue;
+            yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[0 * vs + o] +
+                   ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[1 * vs + o]) +
+                  ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[2 * vs + o];
+          }
+        }
+        const double xc = xs[c * cp.xcap + ls];
+        if (boost != 0.0) yc = yc + boost * xc;
+        y[c * vs + sslot] = yc;
+        acc_xy += xc * yc;
+        acc_yy += yc * yc;
+        acc_xx += xc * xc;
+      }
+      TPROF_MARK(3);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stg]);  // this warp is done with the stage
+      consumers_sync(NW * 32);                  // part[] is rewritten next tile
+      TPROF_MARK(4);
+    }
+    TPROF_FLUSH();
+  }
+  __syncthreads();
+  if (mode == 0) return;
+  spmv_pcg_epilogue<(NW + 1) * 32>(S, boost, acc_xy, acc_yy, acc_xx, sh);
+}
+
+#ifndef BDEM_TILE_TS
+#define BDEM_TILE_TS 1
+#endif
+#ifndef BDEM_TILE_NW
+#define BDEM_TILE_NW 8
+#endif
+#ifndef BDEM_TILE_STAGES
+#define BDEM_TILE_STAGES 3
+#endif
+#ifndef BDEM_TILE_MINB
+#define BDEM_TILE_MINB 2
+#endif
+#ifndef BDEM_TILE_DIAG
+#define BDEM_TILE_DIAG 1
+#endif
+#ifndef BDEM_TILE_KCAP
+#define BDEM_TILE_KCAP 8
+#endif
+constexpr int kTileTS = BDEM_TILE_TS, kTileNW = BDEM_TILE_NW, kTileStages = BDEM_TILE_STAGES;
+
+// tiled launch when enabled and the staging fits; returns false otherwise
+// SpMV variant: 0 slot-parallel k_spmv (default), 1 tiled k_spmv_tile
+static int g_spmv_kernel = -1;
+static int spmv_kernel() {
+  if (g_spmv_kernel < 0) {
+    const char *env = getenv("BDEM_SPMV_TILE");
+    g_spmv_kernel = (env && atoi(env) != 0) ? 1 : 0;
+  }
+  return g_spmv_kernel;
+}
+
+static bool launch_spmv_tile(const bdem_system_t &S, const double *x, double *y, int mode,
+                             cudaStream_t st) {
+  static int sms = 0;
+  if (spmv_kernel() != 1 || S.n_elem == 0 || !S.tile_hdr) return false;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  auto clampk = [](int64_t k) { return (int)(k < 1 ? 1 : (k > BDEM_TILE_KCAP ? BDEM_TILE_KCAP : k)); };
+  TileCaps cp;
+  cp.rows = kTileTS * 32;
+  cp.cap = cp.rows * clampk(S.sell_kmax);
+  cp.capj = cp.rows * clampk(S.sell_kjmax);
+  cp.xcap = cp.rows + 2;
+  cp.diag = BDEM_TILE_DIAG != 0;
+  const size_t bytes = sizeof(double) * (size_t)cp.stage_doubles() * kTileStages;
+  auto kern = k_spmv_tile<kTileTS, kTileNW, kTileStages, BDEM_TILE_MINB>;
+  static size_t configured = 0;
+  static int per_sm = 1;
+  if (bytes > configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    configured = bytes;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (kTileNW + 1) * 32, bytes);
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int ns = (int)((S.n_elem + 31) >> 5);
+  const int ntiles = (ns + kTileTS - 1) / kTileTS;
+  int g = sms * per_sm;
+  if (g > ntiles) g = ntiles;
+  if (g > kRedBlocks) g = kRedBlocks;
+  kern<<<g, (kTileNW + 1) * 32, bytes, st>>>(S, x, y, mode, cp);
+  return true;
+}
+
 // resident-grid size of k_spmv (one wave), capped by the partial-sum slots
 static unsigned int spmv_grid() {
   static unsigned int g = 0;
@@ -496,6 +954,7 @@ static unsigned int spmv_grid() {
 // one SpMV launch (plain or PCG mode) with the configured kernel
 static void launch_spmv(const bdem_system_t &S, const double *x, double *y, int mode,
                         cudaStream_t st) {
+  if (launch_spmv_tile(S, x, y, mode, st)) return;
   const unsigned int g = spmv_grid();
   k_spmv<<<g, kSpmvThreads, 0, st>>>(S, x, y, mode);
 }
@@ -505,6 +964,23 @@ static void launch_spmv(const bdem_system_t &S, const double *x, double *y, int 
 using namespace bdem;
 
 extern "C" {
+
+int bdem_spmv_tile_slices(void) { return kTileTS; }
+int bdem_spmv_set_kernel(int kernel) {
+  const int prev = spmv_kernel();
+  if (kernel == 0 || kernel == 1) g_spmv_kernel = kernel;
+  return prev;
+}
+int bdem_spmv_tile_hdr_ints(void) { return TileHdrWords<kTileTS>::kInts; }
+
+#ifdef BDEM_TILE_PROF
+int bdem_tile_prof(unsigned long long *out) {
+  cudaMemcpyFromSymbol(out, g_tile_prof, sizeof(unsigned long long) * 8);
+  unsigned long long z[8] = {0};
+  cudaMemcpyToSymbol(g_tile_prof, z, sizeof(z));
+  return 0;
+}
+#endif
 
 int bdem_spmv(const bdem_system_t *sys, const double *x, double *y, void *stream) {
   if (!sys) return BDEM_ERR_ARG;

@@ -39,40 +39,111 @@ def _ptr(t) -> int:
     return 0 if t is None else t.data_ptr()
 
 
+def _spread3(v):
+    """Spread the low 21 bits of v so bit k lands at bit 3k (Morton interleave)."""
+    v = v.astype(np.uint64) & np.uint64(0x1FFFFF)
+    for shift, mask in ((32, 0x1F00000000FFFF), (16, 0x1F0000FF0000FF), (8, 0x100F00F00F00F00F),
+                        (4, 0x10C30C30C30C30C3), (2, 0x1249249249249249)):
+        v = (v | (v << np.uint64(shift))) & np.uint64(mask)
+    return v
+
+
+def z_order(p: np.ndarray, cell: float) -> np.ndarray:
+    """Elements sorted along a Z-order curve of cells of size ``cell``, ties by id.
+
+    Consecutive runs of 32..128 elements then form compact patches, so the
+    bonds of a SELL tile mostly join two rows of the same tile."""
+    p = np.asarray(p, dtype=float)
+    if p.shape[0] == 0:
+        return np.zeros(0, dtype=np.int64)
+    g = np.floor((p - p.min(axis=0)) / max(cell, 1e-300))
+    g = np.clip(g, 0, 2**21 - 1).astype(np.uint64)
+    key = _spread3(g[:, 0]) | (_spread3(g[:, 1]) << np.uint64(1)) | (_spread3(g[:, 2]) << np.uint64(2))
+    return np.argsort(key, kind="stable")
+
+
+def row_order(el, mode: str | None = None) -> np.ndarray:
+    """SELL row order: the caller's element order (default: on lattices its
+    neighbour offsets are constant, so the SpMV's j-role and x gathers are
+    shift-coalesced) or a Z-order of the initial positions (``BDEM_ROW_ORDER=z``:
+    compact tiles for the tiled SpMV variant)."""
+    import os
+    mode = mode or os.environ.get("BDEM_ROW_ORDER", "id")
+    n = int(el.p.shape[0])
+    if mode == "id" or n == 0:
+        return np.arange(n, dtype=np.int64)
+    cell = 2.0 * float(np.median(np.asarray(el.radius)))
+    return z_order(el.p, cell)
+
+
 class SellLayout:
     """SELL-32 placement of the bonds (see bdem_system_t in the header).
 
-    Elements are cut into slices of 32 consecutive ids.  Each slice owns a
-    slot-major block of positions: slot k of lane l holds the k-th bond with
-    i == 32 s + l in ascending bond id (the order np.add.at accumulates in,
+    Elements are placed in rows (``rows[r]`` = element of row r) and rows are
+    cut into slices of 32.  Each slice owns a slot-major block of positions:
+    slot k of lane l holds the k-th bond with i == rows[32 s + l] in
+    ascending bond id (the order np.add.at accumulates in,
     integrator.py:100-103).  A warp that owns a slice therefore reads slot k
-    of 32 consecutive rows as one contiguous 256-byte segment per plane.  The
-    j-role lists (bonds with j == e, ascending id) use the same shape and hold
+    of 32 rows as one contiguous 256-byte segment per plane.  The j-role
+    lists (bonds with j == e, ascending id) use the same shape and hold
     positions.  Padding positions carry status BROKEN and zero data.
     """
 
-    def __init__(self, bi: np.ndarray, bj: np.ndarray, n: int, slot: np.ndarray):
+    def __init__(self, bi: np.ndarray, bj: np.ndarray, n: int, slot: np.ndarray,
+                 rows: np.ndarray | None = None):
         nb = bi.shape[0]
         self.n_slices = ns = max((n + 31) // 32, 1)
-        self.slice_base, rank_i = self._slices(bi, n, ns)
+        rows = np.arange(n, dtype=np.int64) if rows is None else np.asarray(rows, dtype=np.int64)
+        self.rows = rows
+        self.elem_row = np.empty(n, dtype=np.int64)
+        self.elem_row[rows] = np.arange(n)
+        self.row_elem = np.full(ns * 32, -1, dtype=np.int32)
+        self.row_elem[:n] = rows
+        ri = self.elem_row[bi]
+        rj = self.elem_row[bj]
+        self.slice_base, rank_i, self.kmax = self._slices(ri, n, ns)
         self.n_pos = int(self.slice_base[-1])
-        self.pos_of_bond = self.slice_base[bi // 32] + 32 * rank_i + (bi % 32)
+        self.pos_of_bond = self.slice_base[ri // 32] + 32 * rank_i + (ri % 32)
         self.bond_of_pos = np.full(self.n_pos, -1, dtype=np.int64)
         self.bond_of_pos[self.pos_of_bond] = np.arange(nb)
         self.pos_oslot = np.full(self.n_pos, -1, dtype=np.int32)
         self.pos_oslot[self.pos_of_bond] = slot[bj]
-        self.jslice_base, rank_j = self._slices(bj, n, ns)
+        self.jslice_base, rank_j, self.kjmax = self._slices(rj, n, ns)
         self.n_jpos = int(self.jslice_base[-1])
-        jidx = self.jslice_base[bj // 32] + 32 * rank_j + (bj % 32)
+        jidx = self.jslice_base[rj // 32] + 32 * rank_j + (rj % 32)
         self.jpos = np.full(self.n_jpos, -1, dtype=np.int32)
         self.jpos[jidx] = self.pos_of_bond
         self.jslot = np.full(self.n_jpos, -1, dtype=np.int32)
         self.jslot[jidx] = slot[bi]
+        free_row = np.zeros(ns * 32, dtype=np.int64)
+        free_row[:n] = slot[rows] >= 0
+        self.row_slot = np.full(ns * 32, -1, dtype=np.int32)
+        self.row_slot[:n] = slot[rows]
+        self.slice_slot = np.zeros(ns + 1, dtype=np.int64)
+        np.cumsum(free_row.reshape(ns, 32).sum(axis=1), out=self.slice_slot[1:])
+
+    def tile_headers(self, ts: int, stride: int) -> np.ndarray:
+        """Per-tile header records of the tiled SpMV (see bdem_system_t.tile_hdr)."""
+        ns = self.n_slices
+        if ts <= 0:
+            return np.zeros(max(stride, 1), dtype=np.int32)
+        nt = (ns + ts - 1) // ts
+        t0 = np.arange(nt) * ts
+        t1 = np.minimum(t0 + ts, ns)
+        out = np.zeros((nt, stride), dtype=np.int64)
+        for k in range(ts + 1):
+            sl = np.minimum(t0 + k, t1)
+            out[:, k] = self.slice_base[sl]
+            out[:, ts + 1 + k] = self.jslice_base[sl]
+        out[:, 2 * ts + 2] = self.slice_slot[t0]
+        out[:, 2 * ts + 3] = self.slice_slot[t1]
+        assert out.max() < 2**31
+        return out.astype(np.int32).reshape(-1)
 
     @staticmethod
     def _slices(key, n, ns):
-        """Slot rank of every bond within its element (ascending id) and the
-        slice base offsets (32 x max slots per slice)."""
+        """Slot rank of every bond within its row (ascending bond id), the
+        slice base offsets (32 x max slots per slice) and the max slots."""
         nb = key.shape[0]
         cnt = np.bincount(key, minlength=n)
         order = np.argsort(key, kind="stable")
@@ -84,7 +155,7 @@ class SellLayout:
         kmax = padded.reshape(ns, 32).max(axis=1)
         base = np.zeros(ns + 1, dtype=np.int64)
         np.cumsum(32 * kmax, out=base[1:])
-        return base, rank
+        return base, rank, int(kmax.max()) if kmax.size else 0
 
     def to_positions(self, arr, fill=0):
         """Scatter a per-bond array (..., nb) into positions (..., n_pos)."""
@@ -130,10 +201,15 @@ class DeviceSystem:
         self.nb = nb = int(b.i.shape[0])
         pinned = np.asarray(el.pinned, dtype=bool)
         self.free_np = ~pinned
+        # SELL rows in Z-order; free slots numbered in row order (contiguous per slice)
+        rows = row_order(el)
         slot = np.full(n, -1, dtype=np.int32)
+        free_rows = rows[self.free_np[rows]]
+        slot[free_rows] = np.arange(free_rows.size, dtype=np.int32)
         self.free_ids_np = np.nonzero(self.free_np)[0]
-        slot[self.free_ids_np] = np.arange(self.free_ids_np.size, dtype=np.int32)
         self.slot_np = slot
+        # slot of the k-th free element in ascending element id (oracle order)
+        self.slot_cols = slot[self.free_ids_np].astype(np.int64)
         self.nf = nf = int(self.free_ids_np.size)
         dev = self.device
 
@@ -141,7 +217,7 @@ class DeviceSystem:
         self.mass = _t(el.mass, device=dev)
         self.radius = _t(el.radius, device=dev)
         self.slot = _t(slot, I32, dev)
-        self.free_elem = _t(self.free_ids_np.astype(np.int32), I32, dev)
+        self.free_elem = _t(free_rows.astype(np.int32), I32, dev)
         # element state + step context
         z3 = lambda: torch.zeros((n, 3), dtype=F64, device=dev)  # noqa: E731
         z4 = lambda: torch.zeros((n, 4), dtype=F64, device=dev)  # noqa: E731
@@ -157,7 +233,7 @@ class DeviceSystem:
         # bonds, placed by SELL-32 position
         bi64 = np.asarray(b.i, dtype=np.int64)
         bj64 = np.asarray(b.j, dtype=np.int64)
-        self.sell = sell = SellLayout(bi64, bj64, n, slot)
+        self.sell = sell = SellLayout(bi64, bj64, n, slot, rows)
         self.npos = npos = max(sell.n_pos, 1)
         self.bond_i = _t(sell.to_positions(bi64.astype(np.int32)), I32, dev)
         self.bond_j = _t(sell.to_positions(bj64.astype(np.int32)), I32, dev)
@@ -170,9 +246,17 @@ class DeviceSystem:
         self.jslice_base = _t(sell.jslice_base.astype(np.int32), I32, dev)
         self.jpos = _t(np.append(sell.jpos, -1).astype(np.int32), I32, dev)
         self.jslot = _t(np.append(sell.jslot, -1).astype(np.int32), I32, dev)
+        self.row_elem = _t(sell.row_elem, I32, dev)
+        self.elem_row = _t(np.append(sell.elem_row, -1).astype(np.int32), I32, dev)
+        self.slice_slot = _t(sell.slice_slot.astype(np.int32), I32, dev)
+        self.row_slot = _t(sell.row_slot, I32, dev)
+        self.tile_hdr = _t(sell.tile_headers(int(self.lib.bdem_spmv_tile_slices()),
+                                             int(self.lib.bdem_spmv_tile_hdr_ints())), I32, dev)
         self.pos_of_bond_d = torch.as_tensor(sell.pos_of_bond).to(dev)
         # staging / reduced system
         self.stage = torch.zeros((L.ST["COUNT"], npos), dtype=F64, device=dev)
+        npos32 = (npos + 31) // 32 * 32
+        self.scoef = torch.zeros(L.CF["COUNT"] * npos32, dtype=F64, device=dev)
         # reduced vectors / diagonal blocks: planes of stride vstride (n_free
         # rounded up to 32 -> 256-byte aligned planes, zero padding)
         self.vstride = vs = max(32, (nf + 31) // 32 * 32)
@@ -202,6 +286,7 @@ class DeviceSystem:
         s = self.sys
         s.n_elem, s.n_free, s.n_bond = n, nf, (sell.n_pos if nb else 0)
         s.vstride = self.vstride
+        s.sell_kmax, s.sell_kjmax = sell.kmax, sell.kjmax
         s.mass, s.radius = _ptr(self.mass), _ptr(self.radius)
         s.mp_dt2, s.mq_dt2 = _ptr(self.mp_dt2), _ptr(self.mq_dt2)
         s.p_hat, s.q_hat = _ptr(self.p_hat), _ptr(self.q_hat)
@@ -211,7 +296,11 @@ class DeviceSystem:
         s.slice_base, s.pos_oslot = _ptr(self.slice_base), _ptr(self.pos_oslot)
         s.jslice_base, s.jpos, s.jslot = (_ptr(self.jslice_base), _ptr(self.jpos),
                                           _ptr(self.jslot))
+        s.row_elem, s.elem_row = _ptr(self.row_elem), _ptr(self.elem_row)
+        s.slice_slot, s.row_slot = _ptr(self.slice_slot), _ptr(self.row_slot)
+        s.tile_hdr = _ptr(self.tile_hdr)
         s.stage, s.diag, s.minv = _ptr(self.stage), _ptr(self.diag), _ptr(self.minv)
+        s.scoef = _ptr(self.scoef)
         s.red, s.scalars, s.pcg = _ptr(self.red), _ptr(self.scalars), _ptr(self.pcg_state)
         s.err, s.counter = _ptr(self.err), _ptr(self.counter)
         s.clamp_list = _ptr(self.clamp_list)
@@ -451,6 +540,12 @@ class DeviceSystem:
         return self.h_scalars.numpy()
 
     # ---------------------------------------------------------------- kernels
+    def coef_planes(self) -> torch.Tensor:
+        """The AoSoA-32 SpMV coefficients as (BDEM_CF_COUNT, n_pos) planes."""
+        npos32 = self.scoef.numel() // L.CF["COUNT"]
+        v = self.scoef.view(npos32 // 32, L.CF["COUNT"], 32).permute(1, 0, 2)
+        return v.reshape(L.CF["COUNT"], npos32)[:, :self.npos]
+
     def friction(self, mu_s: float, mu_r: float, dt: float) -> int:
         """apply_friction (contact.py:303-350) on the device state in place;
         returns the number of dependency waves the pair sweep used."""

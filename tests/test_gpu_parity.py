@@ -144,16 +144,17 @@ def _gpu_problem(d, tag):
 
 
 def _aos(t, dev):
-    """Reduced device vector (6 planes of stride vstride) -> 6 per slot."""
-    vs, nf = dev.vstride, dev.nf
-    return t[:6 * vs].reshape(6, vs)[:, :nf].T.reshape(-1).cpu().numpy()
+    """Reduced device vector (6 planes of stride vstride, slots in SELL row
+    order) -> 6 per free element in ascending id (the oracle's order)."""
+    vs = dev.vstride
+    return t[:6 * vs].reshape(6, vs)[:, dev.slot_cols].T.reshape(-1).cpu().numpy()
 
 
 def _soa(a, dev):
     import torch
     vs, nf = dev.vstride, dev.nf
     out = np.zeros((6, vs))
-    out[:, :nf] = a.reshape(nf, 6).T
+    out[:, dev.slot_cols] = a.reshape(nf, 6).T
     return torch.from_numpy(out).reshape(-1).cuda()
 
 
@@ -181,8 +182,9 @@ def test_assembly_vs_golden(cuda_ok, tag):
     b = bonds_from(d, f"{tag}_b_")
     act = np.nonzero(b.status != 2)[0]
     st = dev.stage.cpu().numpy()[:, dev.sell.pos_of_bond]
-    n = st[L.ST["N"]:L.ST["N"] + 3].T[act]
-    al, be = st[L.ST["ALPHA"]][act], st[L.ST["BETA"]][act]
+    cf = dev.coef_planes().cpu().numpy()[:, dev.sell.pos_of_bond]   # AoSoA-32 -> planes
+    n = cf[L.CF["N"]:L.CF["N"] + 3].T[act]
+    al, be = cf[L.CF["ALPHA"]][act], cf[L.CF["BETA"]][act]
     apos = al[:, None, None] * n[:, :, None] * n[:, None, :] + be[:, None, None] * np.eye(3)
     want_pp = d[f"{tag}_bond_pp"]
     hs = np.abs(want_pp).max()
@@ -192,18 +194,18 @@ def test_assembly_vs_golden(cuda_ok, tag):
     hr = np.abs(rot).max()
     A = _sym6_to_mat(st[L.ST["A"]:L.ST["A"] + 6].T[act])
     D = _sym6_to_mat(st[L.ST["D"]:L.ST["D"] + 6].T[act])
-    Cb = st[L.ST["C"]:L.ST["C"] + 9].T[act].reshape(-1, 3, 3)
+    Cb = cf[L.CF["C"]:L.CF["C"] + 9].T[act].reshape(-1, 3, 3)
     _assert_close(A, rot[:, :3, :3], 1e-9, 1e-11 * hr, "rot (ii)")
     _assert_close(D, rot[:, 3:, 3:], 1e-9, 1e-11 * hr, "rot (jj)")
     _assert_close(Cb, rot[:, :3, 3:], 1e-9, 1e-11 * hr, "rot (ij)")
     # diagonal blocks and block-Jacobi inverses
-    diag = dev.diag[:, :dev.nf].cpu().numpy().T
+    diag = dev.diag[:, dev.slot_cols].cpu().numpy().T
     P, R = _sym6_to_mat(diag[:, :6]), _sym6_to_mat(diag[:, 6:])
     want = d[f"{tag}_diag"]
     sc = np.abs(want).max()
     _assert_close(P, want[:, :3, :3], 1e-9, 1e-11 * sc, "diag pos")
     _assert_close(R, want[:, 3:, 3:], 1e-9, 1e-11 * sc, "diag rot")
-    minv = dev.minv[:, :dev.nf].cpu().numpy().T
+    minv = dev.minv[:, dev.slot_cols].cpu().numpy().T
     wm = d[f"{tag}_minv"]
     _assert_close(_sym6_to_mat(minv[:, :6]), wm[:, :3, :3], 1e-7, 1e-9 * np.abs(wm).max(), "Pinv")
     _assert_close(_sym6_to_mat(minv[:, 6:]), wm[:, 3:, 3:], 1e-7, 1e-9 * np.abs(wm).max(), "Rinv")
@@ -302,8 +304,12 @@ def test_trajectory_vs_golden(cuda_ok, name):
                   k_element=float(d["k_element"]), plastic=plastic, driver=driver,
                   mu_s=float(d.get("mu_s", 0.0)), mu_r=float(d.get("mu_r", 0.0)))
     cfg = SolverConfig(epsilon=float(d["epsilon"]), max_iterations=300)
+    # rtol 1e-8 with atol >= eps / (min inertia / dt^2) to absorb
+    # Newton-termination differences; rotations use m_q = 1.6 m r^2 (a8)
     m_dt2 = (el.mass / float(d["dt"]) ** 2).min()
+    mq_dt2 = (1.6 * el.mass * el.radius**2 / float(d["dt"]) ** 2).min()
     atol_p = max(10 * float(d["epsilon"]) / m_dt2, 1e-12)
+    atol_q = max(10 * float(d["epsilon"]) / mq_dt2, 1e-9)
     events = []
     for s in range(d["p"].shape[0]):
         if sched is not None:
@@ -312,7 +318,7 @@ def test_trajectory_vs_golden(cuda_ok, name):
         assert rep.committed == bool(d["committed"][s])
         events += [(s, bb) for (bb, _, _) in rep.broken]
         _assert_close(scene.elements.p, d["p"][s], 1e-8, atol_p, f"step {s} p")
-        _assert_close(scene.elements.q, d["q"][s], 1e-8, 1e-9, f"step {s} q")
+        _assert_close(scene.elements.q, d["q"][s], 1e-8, atol_q, f"step {s} q")
         _assert_close(scene.elements.v, d["v"][s], 1e-6, atol_p / float(d["dt"]), f"step {s} v")
     assert [tuple(e) for e in events] == [(int(a), int(bb)) for a, bb, _, _ in d["events"]]
     assert np.array_equal(scene.bonds.status, d["final_b_status"])
@@ -456,7 +462,7 @@ def test_sphere_box_colliders_vs_golden(cuda_ok):
     f, gnorm, _, _ = prob.assemble(dev.xp, dev.xq)
     assert f == pytest.approx(float(d["f"]), rel=1e-12)
     _assert_close(_aos(dev.z, dev), d["z"], 1e-9, 1e-11 * np.abs(d["z"]).max(), "z")
-    diag = dev.diag[:, :dev.nf].cpu().numpy().T
+    diag = dev.diag[:, dev.slot_cols].cpu().numpy().T
     want = d["diag"]
     sc = np.abs(want).max()
     _assert_close(_sym6_to_mat(diag[:, :6]), want[:, :3, :3], 1e-9, 1e-11 * sc, "diag pos")
@@ -579,3 +585,79 @@ def test_friction_large_wave_path_vs_oracle(cuda_ok):
     assert dev.friction(0.4, 0.1, 1e-4) == depth
     _assert_close(dev.v.cpu().numpy(), ref.v, 1e-12, 1e-14, "v")
     _assert_close(dev.qdot.cpu().numpy(), ref.qdot, 1e-12, 1e-14, "qdot")
+
+
+# ---------------------------------------------------------------------------
+# tiled SpMV variant (cp.async.bulk + mbarrier ring, warp-specialised)
+# ---------------------------------------------------------------------------
+
+def _spmv_both(dev, seed):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    x = torch.randn(6 * dev.vstride, generator=g, dtype=torch.float64, device="cuda")
+    ys = []
+    for kern in (0, 1):
+        prev = dev.lib.bdem_spmv_set_kernel(kern)
+        y = torch.full_like(x, float("nan"))
+        dev.call("bdem_spmv", dev.sysp, x.data_ptr(), y.data_ptr(), dev.stream)
+        torch.cuda.synchronize()
+        dev.lib.bdem_spmv_set_kernel(prev)
+        ys.append(y.view(6, dev.vstride)[:, :dev.nf].cpu().numpy())
+    return ys
+
+
+def _assembled(spec, k_element=None):
+    from paper_2308_10459_b200.newton import GPUProblem
+    from paper_2308_10459_b200.scene import Scene
+    from paper_2308_10459_b200.step import contact_candidates
+    scene = Scene.from_spec(spec, host_sync=False)
+    if k_element is not None:
+        scene.k_element = k_element
+    dev = scene.device
+    dev.set_physics(scene.gravity, scene.k_contact, scene.k_element, scene.colliders)
+    dev.set_pairs(contact_candidates(scene))
+    dev.call("bdem_predict", dev.sysp, dev.p.data_ptr(), dev.q.data_ptr(), dev.v.data_ptr(),
+             dev.qdot.data_ptr(), dev.p_prev.data_ptr(), dev.q_prev.data_ptr(), spec.dt,
+             dev.p_hat.data_ptr(), dev.q_hat.data_ptr(), dev.mp_dt2.data_ptr(),
+             dev.mq_dt2.data_ptr(), dev.xp.data_ptr(), dev.xq.data_ptr(), dev.stream)
+    GPUProblem(dev).assemble(dev.xp, dev.xq)
+    return dev
+
+
+@pytest.mark.parametrize("case", ["plate_z", "cube_random_q", "dense_overflow"])
+def test_tiled_spmv_matches_default(cuda_ok, monkeypatch, case):
+    """Same terms per row as k_spmv; with 8 warps per slice (k_spmv: 4) the
+    slot partials associate differently, so the two agree to round-off."""
+    from paper_2308_10459_b200 import configs as C
+    if case == "plate_z":
+        monkeypatch.setenv("BDEM_ROW_ORDER", "z")
+        spec = C.plate(nx=100, ny=60, epsilon=1e-6)
+    elif case == "cube_random_q":
+        spec = C.cube(n_side=9, seed=4, random_q=True)
+    else:
+        rng = np.random.default_rng(8)
+        n = 3000
+        pos = rng.uniform(0.0, 0.03, size=(n, 3))
+        rad = np.full(n, 0.002)
+        pairs = C._pairs_within(pos, 0.0042)
+        el = C._elements(pos, C._random_unit_quats(rng, n), rad, 2500.0,
+                         pinned=rng.random(n) < 0.05)
+        b = C.build_bonds(pos, rad, pairs, 1e7, 4e6)
+        spec = C.SceneSpec("dense", el, b, 1e-4, 1e7, 4e6, 2500.0)
+    dev = _assembled(spec)
+    if case == "dense_overflow":
+        assert dev.sell.kmax > 8 and dev.sell.kjmax > 8   # beyond the staged slots
+    y0, y1 = _spmv_both(dev, 11)
+    assert np.all(np.isfinite(y0))
+    np.testing.assert_allclose(y1, y0, rtol=1e-12, atol=1e-13 * np.abs(y0).max())
+
+
+def test_tiled_spmv_newton_solve_vs_golden(cuda_ok):
+    """The reference Newton solve (newton_solve.npz) through the tiled variant."""
+    import paper_2308_10459_b200._lib as L
+    lib = L.load()
+    prev = lib.bdem_spmv_set_kernel(1)
+    try:
+        test_newton_solve_vs_golden(cuda_ok)
+    finally:
+        lib.bdem_spmv_set_kernel(prev)
