@@ -301,6 +301,25 @@ def assembly_bytes(dev):
     return dev.nb * (161 + 288) + dev.n * 56
 
 
+# Chip-wide L2-slice (LTS) throughput cap per SM clock, measured on the
+# GB300 (B300_MICROARCH.md "LTS throughput cap ~6300 B/cyc full-chip"); the
+# SpMV's gathers re-read coefficients and x from L2, so this is its real bound.
+L2_BYTES_PER_CLK = 6300.0
+
+
+def l2_roofline(ncu, spmv_ms, clocks):
+    """L2 view of the SpMV: ncu lts__t_sectors x 32 B per launch over the live
+    launch time, against the LTS cap at the sampled SM clock."""
+    sectors = ncu.get("l2_sectors_per_launch")
+    mhz = (clocks.summary() or {}).get("sm_mhz") or 1965.0
+    if not sectors or not spmv_ms == spmv_ms:
+        return None
+    achieved = 32.0 * sectors / (spmv_ms * 1e-3) / 1e9
+    cap = L2_BYTES_PER_CLK * mhz * 1e6 / 1e9
+    return {"bytes_per_launch": 32.0 * sectors, "achieved": achieved, "cap": cap, "unit": "GB/s",
+            "frac": achieved / cap, "source": "ncu lts__t_sectors.sum x 32 B (profiles/ncu_traffic.json)"}
+
+
 def load_ncu_traffic():
     path = os.path.join(REPO, "profiles", "ncu_traffic.json")
     try:
@@ -420,7 +439,8 @@ def run_ours(args):
         "roofline": {"kernel": "bdem::k_spmv (PCG SpMV)", "bound": "hbm", "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": peak_kind,
-                     "traffic": traffic.get("k_spmv", {}).get("dram_bytes_per_launch")},
+                     "traffic": traffic.get("k_spmv", {}).get("dram_bytes_per_launch"),
+                     "l2": l2_roofline(traffic.get("k_spmv", {}), spmv_ms, clocks)},
         "e2e": {"value": e2e_newton_all / (e2e_ms_max * 1e-3) if n_e2e else None, "unit": UNIT,
                 "same_steps_as_value": True, "newton_iterations": e2e_newton,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n_e2e},

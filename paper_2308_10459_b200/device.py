@@ -62,6 +62,27 @@ def z_order(p: np.ndarray, cell: float) -> np.ndarray:
     return np.argsort(key, kind="stable")
 
 
+def strip_order(p: np.ndarray, a: float, width: int = 32) -> np.ndarray:
+    """Strip-major order: strips ``width`` spacings wide along the longest
+    axis, then layers, rows, and position inside the row.  Sheet-like scenes
+    are first rotated into their principal axes (a tilted plate keeps its
+    lattice rows).  A slice is then 32 consecutive elements of one lattice
+    row and its row neighbours sit in the adjacent slices, at fixed offsets."""
+    p = np.asarray(p, dtype=float)
+    c = p - p.mean(axis=0)
+    ext = c.max(axis=0) - c.min(axis=0)
+    if ext.min() < 0.1 * ext.max():          # sheet: use in-plane principal axes
+        _, _, vt = np.linalg.svd(c[:: max(1, c.shape[0] // 20000)], full_matrices=False)
+        c = c @ vt.T
+        ext = c.max(axis=0) - c.min(axis=0)
+    ax = np.argsort(-ext, kind="stable")
+    u = [c[:, k] - c[:, k].min() for k in ax]
+    strip = np.floor(u[0] / (width * a) + 1e-9).astype(np.int64)
+    row = np.round(u[1] / (0.5 * a)).astype(np.int64)
+    layer = np.round(u[2] / (0.5 * a)).astype(np.int64)
+    return np.lexsort((u[0], row, layer, strip))
+
+
 def row_order(el, mode: str | None = None) -> np.ndarray:
     """SELL row order: the caller's element order (default: on lattices its
     neighbour offsets are constant, so the SpMV's j-role and x gathers are
@@ -73,6 +94,8 @@ def row_order(el, mode: str | None = None) -> np.ndarray:
     if mode == "id" or n == 0:
         return np.arange(n, dtype=np.int64)
     cell = 2.0 * float(np.median(np.asarray(el.radius)))
+    if mode == "strip":
+        return strip_order(el.p, cell)
     return z_order(el.p, cell)
 
 
