@@ -194,6 +194,13 @@ typedef struct {
   const int32_t *elem_row;       /* (n_elem) row of an element          */
   const int32_t *slice_slot;     /* (n_slices + 1) first free slot of a slice */
   const int32_t *row_slot;       /* (n_slices * 32) free slot of a row, -1 pinned/pad */
+  /* contribution-table SpMV (bdem_spmv_set_kernel(2)): tiles of
+   * bdem_spmv_sym_slices() slices; a bond whose rows share a tile is read once
+   * and hands row j its product through a per-tile shared-memory table */
+  const int32_t *sym_jloc;       /* (n_bond) table slot k*R + (row_j - tile_row0), -1 boundary */
+  const int32_t *sym_jbase;      /* (n_slices + 1) boundary-only j-role lists, SELL shape */
+  const int32_t *sym_jpos, *sym_jslot;
+  int64_t sym_kc;                /* table depth (max in-tile j-role bonds of a row) */
   const int32_t *tile_hdr;       /* per SpMV tile (bdem_spmv_tile_slices() slices):
                                     BDEM_TILE_HDR ints = slice_base[t0..t0+TS],
                                     jslice_base[t0..t0+TS], slice_slot[t0], slice_slot[t1] */
@@ -332,13 +339,17 @@ int bdem_finish_step(const bdem_system_t *sys, const double *p, const double *q,
 int bdem_spmv(const bdem_system_t *sys, const double *x, double *y, void *stream);
 /* SpMV kernel variant for every later SpMV launch: 0 = slot-parallel
  * (default), 1 = tiled (cp.async.bulk + mbarrier ring, warp-specialised
- * producer; pays off only with compact tiles, BDEM_ROW_ORDER=z).  Returns the
+ * producer; pays off only with compact tiles, BDEM_ROW_ORDER=z), 2 =
+ * contribution table (BDEM_ROW_ORDER=strip).  Returns the
  * previous variant; any other value only queries.  BDEM_SPMV_TILE=1 in the
  * environment selects the tiled one at load time. */
 int bdem_spmv_set_kernel(int kernel);
 /* Slices per tile of the tiled SpMV and the int32 stride of sys->tile_hdr. */
 int bdem_spmv_tile_slices(void);
 int bdem_spmv_tile_hdr_ints(void);
+/* Slices per tile of the contribution-table SpMV and its table-depth cap. */
+int bdem_spmv_sym_slices(void);
+int bdem_spmv_sym_kcap(void);
 
 /* PCG (linalg.py:40-97) on device state sys->pcg; see pcg_kernels.cu. */
 int bdem_pcg_init(const bdem_system_t *sys, const double *b, double sign, double *x,

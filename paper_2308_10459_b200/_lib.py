@@ -49,7 +49,8 @@ class System(C.Structure):
         ("bond_i", _p), ("bond_j", _p), ("status", _p), ("geom", _p), ("bstate", _p),
         ("slice_base", _p), ("pos_oslot", _p), ("jslice_base", _p), ("jpos", _p), ("jslot", _p),
         ("row_elem", _p), ("elem_row", _p), ("slice_slot", _p), ("row_slot", _p),
-        ("tile_hdr", _p),
+        ("sym_jloc", _p), ("sym_jbase", _p), ("sym_jpos", _p), ("sym_jslot", _p),
+        ("sym_kc", C.c_int64), ("tile_hdr", _p),
         ("pair_i", _p), ("pair_j", _p), ("pi_ptr", _p), ("pj_ptr", _p), ("pj_idx", _p),
         ("stage", _p), ("scoef", _p), ("pstage", _p), ("diag", _p), ("minv", _p), ("red", _p),
         ("scalars", _p), ("pcg", _p), ("err", _p), ("counter", _p), ("clamp_list", _p),
@@ -99,6 +100,8 @@ SIGNATURES = {
     "bdem_select_flagged": (_int, [_p, _i64, _p, _p, C.POINTER(C.c_int64), _p]),
     "bdem_spmv_set_kernel": (_int, [_int]),
     "bdem_spmv_tile_slices": (_int, []),
+    "bdem_spmv_sym_slices": (_int, []),
+    "bdem_spmv_sym_kcap": (_int, []),
     "bdem_spmv_tile_hdr_ints": (_int, []),
     "bdem_friction_workspace": (_i64, [_i64, _i64]),
     "bdem_friction": (_int, [_p, _p, _p, _p, _p, _dbl, _dbl, _dbl, _p, C.POINTER(C.c_int64), _p]),

@@ -893,7 +893,8 @@ static int g_spmv_kernel = -1;
 static int spmv_kernel() {
   if (g_spmv_kernel < 0) {
     const char *env = getenv("BDEM_SPMV_TILE");
-    g_spmv_kernel = (env && atoi(env) != 0) ? 1 : 0;
+    g_spmv_kernel = env ? atoi(env) : 0;
+    if (g_spmv_kernel < 0 || g_spmv_kernel > 2) g_spmv_kernel = 0;
   }
   return g_spmv_kernel;
 }
@@ -937,6 +938,198 @@ static bool launch_spmv_tile(const bdem_system_t &S, const double *x, double *y,
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// Contribution-table SpMV (variant 2).  Rows in strip-major order; a CTA owns
+// a tile of TS slices (R = 32 TS rows).  Each i-role slot reads its bond once
+// from the coefficient stream and forms both products: row i's goes to the
+// thread's accumulator, and when row j is in the same tile, row j's product
+// (-a+ x_i, C^T x_i) is stored in the tile's shared-memory table at the
+// bond's precomputed slot (unique per bond: no atomics).  Only boundary bonds
+// (rows in different tiles) remain in the j-role lists and are gathered from
+// L2.  Row sums: D x + slot partials (fixed warp order) + table entries (rank
+// order) + boundary j-role partials -- deterministic.
+// ---------------------------------------------------------------------------
+#ifndef BDEM_SYM_TS
+#define BDEM_SYM_TS 4
+#endif
+#ifndef BDEM_SYM_NW
+#define BDEM_SYM_NW 8
+#endif
+#ifndef BDEM_SYM_MINB
+#define BDEM_SYM_MINB 2
+#endif
+#ifndef BDEM_SYM_KCAP
+#define BDEM_SYM_KCAP 8
+#endif
+constexpr int kSymTS = BDEM_SYM_TS, kSymNW = BDEM_SYM_NW;
+
+template <int TS, int NW, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB)
+    k_spmv_sym(bdem_system_t S, const double *__restrict__ x, double *__restrict__ y, int mode,
+               int kc) {
+  constexpr int R = TS * 32;
+  extern __shared__ __align__(16) double tab[];  // [kc][6][R]
+  __shared__ double part[NW][6][32];
+  __shared__ double sh[NW];
+  double *pcg = S.pcg;
+  if (mode == 1 && pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
+  const double boost = mode == 1 ? pcg[BDEM_PCG_BOOST] : 0.0;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t vs = S.vstride;
+  const int ns = (int)((S.n_elem + 31) >> 5);
+  const int ntiles = (ns + TS - 1) / TS;
+  const int t_mine = w % TS;
+  constexpr int WPS = NW / TS;
+  const int ntab = kc * 6 * R;
+  double acc_xy = 0.0, acc_yy = 0.0, acc_xx = 0.0;
+#pragma unroll 1
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int k = threadIdx.x; k < ntab; k += NW * 32) tab[k] = 0.0;
+    const int sl = tile * TS + t_mine;
+    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    if (sl < ns) {
+      const int64_t row = (int64_t)sl * 32 + lane;
+      const int myslot = __ldg(S.row_slot + row);
+      double xi[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      if (myslot >= 0) load6_ro(x, myslot, vs, xi);
+      const int64_t i0 = __ldg(S.slice_base + sl), j0 = __ldg(S.sym_jbase + sl);
+      const int ki = (int)((__ldg(S.slice_base + sl + 1) - i0) >> 5);
+      const int kj = (int)((__ldg(S.sym_jbase + sl + 1) - j0) >> 5);
+      __syncthreads();  // table zeroed before any warp writes into it
+#pragma unroll 1
+      for (int k = w / TS; k < ki + kj; k += WPS) {
+        int64_t b;
+        int o, jl = -1;
+        bool tr;
+        if (k < ki) {
+          b = i0 + 32 * k + lane;
+          o = __ldg(S.pos_oslot + b);
+          jl = myslot >= 0 ? __ldg(S.sym_jloc + b) : -1;
+          tr = false;
+        } else {
+          const int64_t jk = j0 + 32 * (k - ki) + lane;
+          o = __ldg(S.sym_jslot + jk);
+          b = __ldg(S.sym_jpos + jk);
+          tr = true;
+        }
+        if (o < 0 || myslot < 0) continue;
+        double xo[6];
+        load6_ro(x, o, vs, xo);
+        const Coef cv = load_coef<true>(S.scoef + cf_idx(b, 0));
+        const double nx = cv.al * ((cv.n[0] * xo[0] + cv.n[1] * xo[1]) + cv.n[2] * xo[2]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[c] -= nx * cv.n[c] + cv.be * xo[c];
+        if (!tr) {
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            acc[3 + q] += (cv.C[3 * q] * xo[3] + cv.C[3 * q + 1] * xo[4]) + cv.C[3 * q + 2] * xo[5];
+          if (jl >= 0) {  // row j in this tile: its product from the same read
+            const int rk = jl / R, rl = jl - rk * R;
+            double *tb = tab + (size_t)rk * 6 * R + rl;
+            const double ni = cv.al * ((cv.n[0] * xi[0] + cv.n[1] * xi[1]) + cv.n[2] * xi[2]);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) tb[c * R] = -(ni * cv.n[c] + cv.be * xi[c]);
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+              tb[(3 + q) * R] = (cv.C[q] * xi[3] + cv.C[3 + q] * xi[4]) + cv.C[6 + q] * xi[5];
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            acc[3 + q] += (cv.C[q] * xo[3] + cv.C[3 + q] * xo[4]) + cv.C[6 + q] * xo[5];
+        }
+      }
+    } else {
+      __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) part[w][q][lane] = acc[q];
+    __syncthreads();
+#pragma unroll 1
+    for (int item = w; item < TS * 6; item += NW) {
+      const int t = item / 6, c = item - 6 * t;
+      const int slc = tile * TS + t;
+      if (slc >= ns) continue;
+      const int64_t row = (int64_t)slc * 32 + lane;
+      const int sslot = __ldg(S.row_slot + row);
+      if (sslot < 0) continue;
+      const int base = c < 3 ? 0 : 3, rr = c - base;
+      const double *dg = S.diag + (c < 3 ? 0 : 6 * vs);
+      double xs3[3];
+#pragma unroll
+      for (int u = 0; u < 3; ++u) xs3[u] = __ldg(x + (base + u) * vs + sslot);
+      double yc = (__ldg(dg + sidx<3>(rr, 0) * vs + sslot) * xs3[0] +
+                   __ldg(dg + sidx<3>(rr, 1) * vs + sslot) * xs3[1]) +
+                  __ldg(dg + sidx<3>(rr, 2) * vs + sslot) * xs3[2];
+#pragma unroll
+      for (int ww = t; ww < NW; ww += TS) yc += part[ww][c][lane];
+      const int rl = t * 32 + lane;
+      for (int rk = 0; rk < kc; ++rk) yc += tab[((size_t)rk * 6 + c) * R + rl];
+      if (c < 3 && S.n_pair > 0) {
+        const int64_t e = __ldg(S.row_elem + row);
+        const int64_t pc = S.pair_cap;
+        const double *ps = S.pstage;
+        for (int k = S.pi_ptr[e]; k < S.pi_ptr[e + 1]; ++k) {
+          const int o = S.slot[S.pair_j[k]];
+          if (o < 0) continue;
+          yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[0 * vs + o] +
+                 ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[1 * vs + o]) +
+                ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[2 * vs + o];
+        }
+        for (int kk = S.pj_ptr[e]; kk < S.pj_ptr[e + 1]; ++kk) {
+          const int64_t k = S.pj_idx[kk];
+          const int o = S.slot[S.pair_i[k]];
+          if (o < 0) continue;
+          yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[0 * vs + o] +
+                 ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[1 * vs + o]) +
+                ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[2 * vs + o];
+        }
+      }
+      const double xc = xs3[rr];
+      if (boost != 0.0) yc = yc + boost * xc;
+      y[c * vs + sslot] = yc;
+      acc_xy += xc * yc;
+      acc_yy += yc * yc;
+      acc_xx += xc * xc;
+    }
+    __syncthreads();
+  }
+  if (mode == 0) return;
+  spmv_pcg_epilogue<NW * 32>(S, boost, acc_xy, acc_yy, acc_xx, sh);
+}
+
+static bool launch_spmv_sym(const bdem_system_t &S, const double *x, double *y, int mode,
+                            cudaStream_t st) {
+  static int sms = 0, per_sm = 0;
+  static size_t configured = 0;
+  if (S.n_elem == 0 || !S.sym_jloc || S.sym_kc > BDEM_SYM_KCAP) return false;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int kc = (int)(S.sym_kc > 0 ? S.sym_kc : 1);
+  const size_t bytes = sizeof(double) * (size_t)kc * 6 * kSymTS * 32;
+  auto kern = k_spmv_sym<kSymTS, kSymNW, BDEM_SYM_MINB>;
+  if (bytes > configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    configured = bytes;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSymNW * 32, bytes);
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int ns = (int)((S.n_elem + 31) >> 5);
+  const int ntiles = (ns + kSymTS - 1) / kSymTS;
+  int g = sms * per_sm;
+  if (g > ntiles) g = ntiles;
+  if (g > kRedBlocks) g = kRedBlocks;
+  kern<<<g, kSymNW * 32, bytes, st>>>(S, x, y, mode, kc);
+  return true;
+}
+
 // resident-grid size of k_spmv (one wave), capped by the partial-sum slots
 static unsigned int spmv_grid() {
   static unsigned int g = 0;
@@ -954,6 +1147,7 @@ static unsigned int spmv_grid() {
 // one SpMV launch (plain or PCG mode) with the configured kernel
 static void launch_spmv(const bdem_system_t &S, const double *x, double *y, int mode,
                         cudaStream_t st) {
+  if (spmv_kernel() == 2 && launch_spmv_sym(S, x, y, mode, st)) return;
   if (launch_spmv_tile(S, x, y, mode, st)) return;
   const unsigned int g = spmv_grid();
   k_spmv<<<g, kSpmvThreads, 0, st>>>(S, x, y, mode);
@@ -968,9 +1162,11 @@ extern "C" {
 int bdem_spmv_tile_slices(void) { return kTileTS; }
 int bdem_spmv_set_kernel(int kernel) {
   const int prev = spmv_kernel();
-  if (kernel == 0 || kernel == 1) g_spmv_kernel = kernel;
+  if (kernel >= 0 && kernel <= 2) g_spmv_kernel = kernel;
   return prev;
 }
+int bdem_spmv_sym_slices(void) { return kSymTS; }
+int bdem_spmv_sym_kcap(void) { return BDEM_SYM_KCAP; }
 int bdem_spmv_tile_hdr_ints(void) { return TileHdrWords<kTileTS>::kInts; }
 
 #ifdef BDEM_TILE_PROF

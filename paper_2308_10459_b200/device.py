@@ -145,6 +145,42 @@ class SellLayout:
         self.slice_slot = np.zeros(ns + 1, dtype=np.int64)
         np.cumsum(free_row.reshape(ns, 32).sum(axis=1), out=self.slice_slot[1:])
 
+    def sym_tables(self, bi, bj, slot, ts: int, kcap: int):
+        """Tables of the contribution-table SpMV for tiles of ``ts`` slices.
+
+        A bond whose two rows lie in one tile gets the table slot
+        ``rank * R + (row_j - tile_row0)`` (R = 32 ts; rank = its order among
+        row j's in-tile bonds, ascending bond id); the others -- and in-tile
+        bonds beyond ``kcap`` -- stay in boundary-only j-role lists of the
+        usual SELL shape."""
+        n = self.elem_row.shape[0]
+        ns = self.n_slices
+        R = 32 * max(ts, 1)
+        ri, rj = self.elem_row[bi], self.elem_row[bj]
+        same = (ri // R) == (rj // R)
+        order = np.lexsort((np.arange(bi.shape[0]), rj))          # by row j, then bond id
+        rank = np.empty(bi.shape[0], dtype=np.int64)
+        same_sorted = same[order]
+        cs = np.cumsum(same_sorted) - same_sorted                  # in-tile bonds before, globally
+        rj_sorted = rj[order]
+        first = np.ones(order.shape[0], dtype=bool)
+        first[1:] = rj_sorted[1:] != rj_sorted[:-1]
+        base = np.maximum.accumulate(np.where(first, cs, 0))
+        rank[order] = cs - base
+        inside = same & (rank < kcap)
+        jloc = np.full(self.n_pos, -1, dtype=np.int32)
+        jloc[self.pos_of_bond[inside]] = (rank[inside] * R + (rj[inside] % R)).astype(np.int32)
+        kc = int(rank[inside].max()) + 1 if inside.any() else 1
+        bnd = np.nonzero(~inside)[0]
+        jb_base, rank_b, _ = self._slices(rj[bnd], n, ns)
+        nj = int(jb_base[-1])
+        jidx = jb_base[rj[bnd] // 32] + 32 * rank_b + (rj[bnd] % 32)
+        jpos = np.full(max(nj, 1), -1, dtype=np.int32)
+        jslot = np.full(max(nj, 1), -1, dtype=np.int32)
+        jpos[jidx] = self.pos_of_bond[bnd]
+        jslot[jidx] = slot[bi[bnd]]
+        return jloc, jb_base.astype(np.int32), jpos, jslot, kc, float(inside.mean()) if inside.size else 0.0
+
     def tile_headers(self, ts: int, stride: int) -> np.ndarray:
         """Per-tile header records of the tiled SpMV (see bdem_system_t.tile_hdr)."""
         ns = self.n_slices
@@ -275,6 +311,12 @@ class DeviceSystem:
         self.row_slot = _t(sell.row_slot, I32, dev)
         self.tile_hdr = _t(sell.tile_headers(int(self.lib.bdem_spmv_tile_slices()),
                                              int(self.lib.bdem_spmv_tile_hdr_ints())), I32, dev)
+        jloc, jbase, jpos_b, jslot_b, kc, self.sym_inside = sell.sym_tables(
+            bi64, bj64, slot, int(self.lib.bdem_spmv_sym_slices()),
+            int(self.lib.bdem_spmv_sym_kcap()))
+        self.sym_jloc = _t(np.append(jloc, -1), I32, dev)
+        self.sym_jbase, self.sym_jpos = _t(jbase, I32, dev), _t(jpos_b, I32, dev)
+        self.sym_jslot, self.sym_kc = _t(jslot_b, I32, dev), kc
         self.pos_of_bond_d = torch.as_tensor(sell.pos_of_bond).to(dev)
         # staging / reduced system
         self.stage = torch.zeros((L.ST["COUNT"], npos), dtype=F64, device=dev)
@@ -322,6 +364,8 @@ class DeviceSystem:
         s.row_elem, s.elem_row = _ptr(self.row_elem), _ptr(self.elem_row)
         s.slice_slot, s.row_slot = _ptr(self.slice_slot), _ptr(self.row_slot)
         s.tile_hdr = _ptr(self.tile_hdr)
+        s.sym_jloc, s.sym_jbase = _ptr(self.sym_jloc), _ptr(self.sym_jbase)
+        s.sym_jpos, s.sym_jslot, s.sym_kc = _ptr(self.sym_jpos), _ptr(self.sym_jslot), self.sym_kc
         s.stage, s.diag, s.minv = _ptr(self.stage), _ptr(self.diag), _ptr(self.minv)
         s.scoef = _ptr(self.scoef)
         s.red, s.scalars, s.pcg = _ptr(self.red), _ptr(self.scalars), _ptr(self.pcg_state)

@@ -591,12 +591,12 @@ def test_friction_large_wave_path_vs_oracle(cuda_ok):
 # tiled SpMV variant (cp.async.bulk + mbarrier ring, warp-specialised)
 # ---------------------------------------------------------------------------
 
-def _spmv_both(dev, seed):
+def _spmv_both(dev, seed, variant=1):
     import torch
     g = torch.Generator(device="cuda").manual_seed(seed)
     x = torch.randn(6 * dev.vstride, generator=g, dtype=torch.float64, device="cuda")
     ys = []
-    for kern in (0, 1):
+    for kern in (0, variant):
         prev = dev.lib.bdem_spmv_set_kernel(kern)
         y = torch.full_like(x, float("nan"))
         dev.call("bdem_spmv", dev.sysp, x.data_ptr(), y.data_ptr(), dev.stream)
@@ -624,13 +624,14 @@ def _assembled(spec, k_element=None):
     return dev
 
 
+@pytest.mark.parametrize("variant", [1, 2])
 @pytest.mark.parametrize("case", ["plate_z", "cube_random_q", "dense_overflow"])
-def test_tiled_spmv_matches_default(cuda_ok, monkeypatch, case):
+def test_tiled_spmv_matches_default(cuda_ok, monkeypatch, case, variant):
     """Same terms per row as k_spmv; with 8 warps per slice (k_spmv: 4) the
     slot partials associate differently, so the two agree to round-off."""
     from paper_2308_10459_b200 import configs as C
     if case == "plate_z":
-        monkeypatch.setenv("BDEM_ROW_ORDER", "z")
+        monkeypatch.setenv("BDEM_ROW_ORDER", "z" if variant == 1 else "strip")
         spec = C.plate(nx=100, ny=60, epsilon=1e-6)
     elif case == "cube_random_q":
         spec = C.cube(n_side=9, seed=4, random_q=True)
@@ -647,16 +648,19 @@ def test_tiled_spmv_matches_default(cuda_ok, monkeypatch, case):
     dev = _assembled(spec)
     if case == "dense_overflow":
         assert dev.sell.kmax > 8 and dev.sell.kjmax > 8   # beyond the staged slots
-    y0, y1 = _spmv_both(dev, 11)
+    if variant == 2:
+        assert 0.0 < dev.sym_inside <= 1.0
+    y0, y1 = _spmv_both(dev, 11, variant)
     assert np.all(np.isfinite(y0))
     np.testing.assert_allclose(y1, y0, rtol=1e-12, atol=1e-13 * np.abs(y0).max())
 
 
-def test_tiled_spmv_newton_solve_vs_golden(cuda_ok):
-    """The reference Newton solve (newton_solve.npz) through the tiled variant."""
+@pytest.mark.parametrize("variant", [1, 2])
+def test_tiled_spmv_newton_solve_vs_golden(cuda_ok, variant):
+    """The reference Newton solve (newton_solve.npz) through the SpMV variants."""
     import paper_2308_10459_b200._lib as L
     lib = L.load()
-    prev = lib.bdem_spmv_set_kernel(1)
+    prev = lib.bdem_spmv_set_kernel(variant)
     try:
         test_newton_solve_vs_golden(cuda_ok)
     finally:
