@@ -410,6 +410,20 @@ int64_t bdem_friction_workspace(int64_t n_elem, int64_t n_pair);
 int bdem_friction(const bdem_system_t *sys, const double *p, const double *q, double *v,
                   double *qdot, double mu_s, double mu_r, double dt, void *work,
                   int64_t *n_waves, void *stream);
+/* ---- surface reconstruction (reconstruct_surface, geometry.py:313-343) ---
+ * Replaces reconstruct_surface(mesh, bonds, labeling, p, q).  Per element:
+ * tet_rel (n,4,3) rest tet vertices minus the centroid, bmask (n) bit mask of
+ * boundary faces; per bond position: face_i / face_j local face (-1 none).
+ * labels (n) fragment ids.  Writes faces ordered by (fragment, element,
+ * local face): verts (F,3,3) transported vertices, face_comp (F) fragment.
+ * *n_faces = F; when F > cap_faces nothing is written (call again with room).
+ * `work` holds bdem_surface_workspace(n_elem) bytes.  Synchronises once. */
+int64_t bdem_surface_workspace(int64_t n_elem);
+int bdem_surface(const bdem_system_t *sys, const double *p, const double *q,
+                 const double *tet_rel, const int32_t *bmask, const int8_t *face_i,
+                 const int8_t *face_j, const int64_t *labels, void *work, double *verts,
+                 int32_t *face_comp, int64_t cap_faces, int64_t *n_faces, void *stream);
+
 /* Host-only scheduler: pairs (m,2) int32 in sweep order -> wave of each pair
  * = 1 + latest wave of an earlier pair sharing an element.  Writes `order`
  * (m pair indices grouped by wave, ascending within a wave) and `wave_ptr`

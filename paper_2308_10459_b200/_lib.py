@@ -106,6 +106,9 @@ SIGNATURES = {
     "bdem_friction_workspace": (_i64, [_i64, _i64]),
     "bdem_friction": (_int, [_p, _p, _p, _p, _p, _dbl, _dbl, _dbl, _p, C.POINTER(C.c_int64), _p]),
     "bdem_friction_schedule": (_i64, [_p, _i64, _i64, _p, _p]),
+    "bdem_surface_workspace": (_i64, [_i64]),
+    "bdem_surface": (_int, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i64,
+                            C.POINTER(C.c_int64), _p]),
 }
 
 

@@ -60,6 +60,7 @@ class SceneSpec:
     driver: DriverSpec | None = None
     mu_s: float = 0.0            # sliding friction (scenes.py:46-47)
     mu_r: float = 0.0            # rolling friction
+    mesh: object = None          # TetMesh for scenes built from tets (surface output)
     epsilon: float = 1e-6
     steps: int = 1
     seed: int = 0
@@ -218,6 +219,29 @@ def stack(n=4, r=0.002, youngs=1e7, nu=0.25, density=2500.0, mu_s=0.3, mu_r=0.05
                      k_contact=k_contact, k_element=k_element, mu_s=mu_s, mu_r=mu_r,
                      epsilon=epsilon, steps=steps, seed=seed,
                      notes="two unbonded blocks, floor contact, sliding + rolling friction")
+
+
+# ---------------------------------------------------------------------------
+# tet-mesh scene of the reference (scenes.py:239-256)
+# ---------------------------------------------------------------------------
+
+def drop_fracture(resolution=1, youngs=1e9, density=2500.0, speed=4.0, tensile_strength=3e5,
+                  shear_strength=3e5, dt=0.002, steps=10, epsilon=1e-5) -> SceneSpec:
+    """The reference's drop-fracture scene: a (4r x 4r x 1) cube-grid plate of
+    Kuhn tets (cell 0.4/(4r), bottom at z=0.05) falling at ``speed`` onto a
+    floor, sliding/rolling friction 0.2/0.05, contact stiffness 2e7."""
+    from .mesh import build_elements_and_bonds, grid_tet_mesh
+    n = 4 * resolution
+    h = 0.4 / n
+    G = youngs / 2.5
+    mesh = grid_tet_mesh(n, n, 1, h, origin=(0.0, 0.0, 0.05))
+    el, bonds = build_elements_and_bonds(mesh, density, youngs, G, tensile_strength,
+                                         shear_strength)
+    el.v[:, 2] = -speed
+    return SceneSpec("drop-fracture", el, bonds, dt, youngs, G, density,
+                     colliders=[HalfSpace((0.0, 0.0, 1.0), 0.0)], k_contact=2e7, k_element=2e7,
+                     mu_s=0.2, mu_r=0.05, mesh=mesh, epsilon=epsilon, steps=steps,
+                     notes="tet-mesh plate (one element per tet, one bond per interior face)")
 
 
 # ---------------------------------------------------------------------------

@@ -607,6 +607,58 @@ class DeviceSystem:
         return self.h_scalars.numpy()
 
     # ---------------------------------------------------------------- kernels
+    # ------------------------------------------------------------- surfaces
+    def set_mesh(self, mesh, bonds):
+        """Static inputs of the surface reconstruction: rest tet vertices about
+        the centroid, boundary-face masks, and each bond's local faces."""
+        from .mesh import boundary_masks
+        rel = mesh.vertices[mesh.tets] - mesh.centroids[:, None, :]       # (n, 4, 3)
+        self.tet_rel = _t(np.ascontiguousarray(rel), device=self.device)
+        self.bmask = _t(boundary_masks(mesh), I32, self.device)
+        fi = np.asarray(bonds.face_i, dtype=np.int8)
+        fj = np.asarray(bonds.face_j, dtype=np.int8)
+        self.face_i = _t(self.sell.to_positions(fi, fill=-1), torch.int8, self.device)
+        self.face_j = _t(self.sell.to_positions(fj, fill=-1), torch.int8, self.device)
+
+    def surface(self, labels: torch.Tensor):
+        """reconstruct_surface (geometry.py:313-343) of the device state:
+        [(component, verts (3F,3), tris (F,3))] in the reference's order."""
+        if getattr(self, "tet_rel", None) is None:
+            raise ValueError("surface reconstruction needs a tet mesh (Scene(mesh=...))")
+        need = int(self.lib.bdem_surface_workspace(self.n))
+        if getattr(self, "_surf_work", None) is None or self._surf_work.numel() < need:
+            self._surf_work = torch.empty(need, dtype=torch.uint8, device=self.device)
+        cap = getattr(self, "_surf_cap", 0)
+        nf = C.c_int64(0)
+        for _ in range(2):
+            if cap > 0 and getattr(self, "_surf_verts", None) is not None:
+                vp, cp_ = self._surf_verts.data_ptr(), self._surf_comp.data_ptr()
+            else:
+                vp = cp_ = None
+            self.call("bdem_surface", self.sysp, self.p.data_ptr(), self.q.data_ptr(),
+                      self.tet_rel.data_ptr(), self.bmask.data_ptr(), self.face_i.data_ptr(),
+                      self.face_j.data_ptr(), labels.data_ptr(), self._surf_work.data_ptr(),
+                      vp, cp_, cap, C.byref(nf), self.stream)
+            if int(nf.value) <= cap:
+                break
+            cap = max(int(nf.value), 2 * cap)
+            self._surf_cap = cap
+            self._surf_verts = torch.empty((cap, 3, 3), dtype=F64, device=self.device)
+            self._surf_comp = torch.empty(cap, dtype=I32, device=self.device)
+        F = int(nf.value)
+        verts = self._surf_verts[:F].reshape(-1, 3).cpu().numpy() if F else np.zeros((0, 3))
+        comp = self._surf_comp[:F].cpu().numpy() if F else np.zeros(0, dtype=np.int32)
+        n_comp = int(labels.max()) + 1 if labels.numel() else 0
+        counts = np.bincount(comp, minlength=n_comp)
+        groups, start = [], 0
+        for c in range(n_comp):
+            k = int(counts[c])
+            v = verts[3 * start:3 * (start + k)]
+            tris = np.arange(3 * k, dtype=np.int64).reshape(-1, 3)
+            groups.append((c, v, tris))
+            start += k
+        return groups
+
     def coef_planes(self) -> torch.Tensor:
         """The AoSoA-32 SpMV coefficients as (BDEM_CF_COUNT, n_pos) planes."""
         npos32 = self.scoef.numel() // L.CF["COUNT"]

@@ -126,8 +126,13 @@ class Scene:
         self.mu_s, self.mu_r = mu_s, mu_r
         self.plastic, self.driver, self.time = plastic, driver, time
         self.p_prev, self.q_prev = p_prev, q_prev
-        self.surface_flags = (np.zeros(elements.n, dtype=bool) if surface_flags is None
-                              else surface_flags)
+        if surface_flags is None:                       # scenes.py:59-60
+            if mesh is not None:
+                from .mesh import mark_surface_elements
+                surface_flags = mark_surface_elements(mesh)
+            else:
+                surface_flags = np.zeros(elements.n, dtype=bool)
+        self.surface_flags = surface_flags
         self.host_sync = host_sync
         self._labels = labels
         self._device = None
@@ -171,7 +176,18 @@ class Scene:
         if self._device is None:
             from .device import DeviceSystem
             self._device = DeviceSystem(self)
+            if self.mesh is not None:
+                self._device.set_mesh(self.mesh, self.bonds)
         return self._device
+
+    def reconstruct_surface(self):
+        """reconstruct_surface(mesh, bonds, labels, p, q) of the current state
+        (geometry.py:313-343), computed on the GPU."""
+        from .step import label_components
+        dev = self.device
+        if getattr(dev, "labels", None) is None:
+            label_components(dev.n, self.bonds, self)
+        return dev.surface(dev.labels)
 
     def sync_to_host(self):
         if self._device is not None:
@@ -184,4 +200,4 @@ class Scene:
                    shear_modulus=spec.shear_modulus, density=spec.density,
                    k_contact=spec.k_contact, k_element=spec.k_element, plastic=spec.plastic,
                    driver=driver_from_spec(spec.driver), mu_s=spec.mu_s, mu_r=spec.mu_r,
-                   host_sync=host_sync)
+                   mesh=spec.mesh, host_sync=host_sync)

@@ -426,6 +426,59 @@ def gold_friction():
     _run_traj("stack", spec, spec.steps, spec.epsilon)
 
 
+def gold_mesh():
+    """The reference's tet-mesh scene (scenes.py:239-256, strengths lowered so
+    the impact breaks bonds): mesh arrays, elements/bonds with face ids, 10
+    implicit steps with friction and fracture, and reconstruct_surface /
+    write_surface_obj (geometry.py:313-358) of the initial and final states."""
+    import tempfile
+    sc = rs.drop_fracture(resolution=1, tensile_strength=3e4, shear_strength=3e4)
+    m = sc.mesh
+    out = {"mesh_vertices": m.vertices, "mesh_tets": m.tets, "mesh_interior": m.interior,
+           "mesh_boundary": m.boundary, "mesh_volumes": m.volumes,
+           "mesh_centroids": m.centroids}
+    # copies: stepping mutates the scene's arrays in place
+    out.update({k: v.copy() for k, v in pack("init_el_", sc.elements, ELEM_FIELDS).items()})
+    out.update({k: v.copy() for k, v in
+                pack("init_b_", sc.bonds, BOND_FIELDS + ("face_i", "face_j")).items()})
+
+    def surface(tag):
+        groups = rg.reconstruct_surface(sc.mesh, sc.bonds, sc.labels, sc.elements.p,
+                                        sc.elements.q)
+        out[f"{tag}_verts"] = np.concatenate([v for _, v, _ in groups]).reshape(-1, 3)
+        out[f"{tag}_counts"] = np.array([v.shape[0] for _, v, _ in groups])
+        out[f"{tag}_tris"] = np.concatenate([t for _, _, t in groups]).reshape(-1, 3)
+        path = os.path.join(tempfile.mkdtemp(), "s.obj")
+        rg.write_surface_obj(path, groups)
+        out[f"{tag}_obj"] = np.array(open(path).read())
+
+    surface("surf0")
+    cfg = rsv.SolverConfig(epsilon=1e-5, max_iterations=300)
+    rec = {k: [] for k in ("p", "q", "v", "qdot", "newton", "committed", "pairs")}
+    events = []
+    for s in range(10):
+        rep = rsv.stable_step(sc, cfg)
+        for k, v in (("p", sc.elements.p), ("q", sc.elements.q), ("v", sc.elements.v),
+                     ("qdot", sc.elements.qdot)):
+            rec[k].append(v.copy())
+        rec["newton"].append(rep.solve.iterations)
+        rec["committed"].append(rep.committed)
+        rec["pairs"].append(rep.contact_pairs)
+        events += [(s, b, sg, tu) for (b, sg, tu) in rep.broken]
+    out.update({k: np.array(v) for k, v in rec.items()})
+    out["events"] = np.array(events, dtype=float).reshape(-1, 4)
+    out["final_status"] = sc.bonds.status.copy()
+    out["labels"] = sc.labels.labels.copy()
+    out["surface_flags"] = sc.surface_flags.copy()
+    surface("surf1")
+    out.update({"dt": sc.dt, "youngs": sc.youngs, "epsilon": 1e-5, "k_contact": sc.k_contact,
+                "k_element": sc.k_element, "mu_s": sc.mu_s, "mu_r": sc.mu_r,
+                "gravity": sc.gravity})
+    print(f"  mesh: {m.n_tets} tets, {sc.bonds.i.shape[0]} bonds, newton {rec['newton']}, "
+          f"broken {len(events)}, components {sc.labels.n_components}")
+    save("mesh_drop.npz", **out)
+
+
 def gold_broadphase_labels():
     rng = np.random.default_rng(51)
     out = {}
@@ -446,7 +499,7 @@ def gold_broadphase_labels():
 if __name__ == "__main__":
     t = time.time()
     which = sys.argv[1:] or ["bond_terms", "fracture", "broadphase_labels", "newton_pieces",
-                             "newton_solve", "colliders", "runner", "trajectories", "friction"]
+                             "newton_solve", "colliders", "runner", "trajectories", "friction", "mesh"]
     for name in which:
         globals()[f"gold_{name}"]()
     print(f"done in {time.time() - t:.1f}s")

@@ -212,3 +212,23 @@ def test_friction_sweep():
     _assert_close(el.qdot, d["qdot_out"], 1e-13, 1e-15, "qdot")
     assert not np.array_equal(d["v_out"], d["v"])          # the sweep did work
     assert np.array_equal(el.v[el.pinned], d["v"][el.pinned])
+
+
+def test_mesh_drop_trajectory():
+    """The reference's tet-mesh drop scene (friction, fracture) through the oracle."""
+    from paper_2308_10459_b200 import configs as C
+    d = load("mesh_drop.npz")
+    spec = C.drop_fracture(tensile_strength=3e4, shear_strength=3e4)
+    st = O.OracleState(spec.elements.copy(), spec.bonds.copy(), spec.dt, spec.youngs,
+                       colliders=spec.colliders, gravity=d["gravity"], k_contact=spec.k_contact,
+                       k_element=spec.k_element, mu_s=spec.mu_s, mu_r=spec.mu_r)
+    cfg = O.Config(epsilon=float(d["epsilon"]), max_iterations=300)
+    events = []
+    for s in range(d["p"].shape[0]):
+        out = O.step(st, cfg)
+        assert out.committed == bool(d["committed"][s])
+        events += [(s, b) for b, _, _ in out.broken]
+        _assert_close(st.elements.p, d["p"][s], 1e-8, 1e-9, f"step {s} p")
+        _assert_close(st.elements.q, d["q"][s], 1e-8, 1e-9, f"step {s} q")
+    assert events == [(int(a), int(b)) for a, b, _, _ in d["events"]]
+    assert np.array_equal(st.bonds.status, d["final_status"])
