@@ -201,6 +201,15 @@ typedef struct {
   const int32_t *sym_jbase;      /* (n_slices + 1) boundary-only j-role lists, SELL shape */
   const int32_t *sym_jpos, *sym_jslot;
   int64_t sym_kc;                /* table depth (max in-tile j-role bonds of a row) */
+  /* dataflow SpMV (bdem_spmv_set_kernel(3)): needs row(i) < row(j) for every
+   * bond.  wave_jring[jk] = ring slot of j-role entry jk's product written by
+   * the i-role pass, -1 none; wave_lag = max slice(j) - slice(i) (-1: variant
+   * unavailable); ring of wave_ring_slices slices x sell_kmax slots x 32 */
+  const int32_t *wave_jring;
+  int64_t wave_lag, wave_ring_slices;
+  double *wave_ring;             /* 6 planes x wave_ring_slices * sell_kmax * 32 */
+  double *wave_ypart;            /* 6 planes x vstride: rows' i-role sums */
+  int32_t *wave_flags;           /* 2 x n_slices epoch stamps (A done, B done) + ticket */
   const int32_t *tile_hdr;       /* per SpMV tile (bdem_spmv_tile_slices() slices):
                                     BDEM_TILE_HDR ints = slice_base[t0..t0+TS],
                                     jslice_base[t0..t0+TS], slice_slot[t0], slice_slot[t1] */

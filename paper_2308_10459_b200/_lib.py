@@ -50,7 +50,9 @@ class System(C.Structure):
         ("slice_base", _p), ("pos_oslot", _p), ("jslice_base", _p), ("jpos", _p), ("jslot", _p),
         ("row_elem", _p), ("elem_row", _p), ("slice_slot", _p), ("row_slot", _p),
         ("sym_jloc", _p), ("sym_jbase", _p), ("sym_jpos", _p), ("sym_jslot", _p),
-        ("sym_kc", C.c_int64), ("tile_hdr", _p),
+        ("sym_kc", C.c_int64), ("wave_jring", _p), ("wave_lag", C.c_int64),
+        ("wave_ring_slices", C.c_int64), ("wave_ring", _p), ("wave_ypart", _p),
+        ("wave_flags", _p), ("tile_hdr", _p),
         ("pair_i", _p), ("pair_j", _p), ("pi_ptr", _p), ("pj_ptr", _p), ("pj_idx", _p),
         ("stage", _p), ("scoef", _p), ("pstage", _p), ("diag", _p), ("minv", _p), ("red", _p),
         ("scalars", _p), ("pcg", _p), ("err", _p), ("counter", _p), ("clamp_list", _p),

@@ -894,7 +894,7 @@ static int spmv_kernel() {
   if (g_spmv_kernel < 0) {
     const char *env = getenv("BDEM_SPMV_TILE");
     g_spmv_kernel = env ? atoi(env) : 0;
-    if (g_spmv_kernel < 0 || g_spmv_kernel > 2) g_spmv_kernel = 0;
+    if (g_spmv_kernel < 0 || g_spmv_kernel > 3) g_spmv_kernel = 0;
   }
   return g_spmv_kernel;
 }
@@ -1130,6 +1130,213 @@ static bool launch_spmv_sym(const bdem_system_t &S, const double *x, double *y, 
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// Dataflow SpMV (variant 3).  Rows in the caller order with row(i) < row(j)
+// for every bond.  Work items, taken in ticket order by persistent CTAs:
+//   A(s): slice s's i-role slots -- each bond read ONCE from the coefficient
+//         stream; row i's product is summed (-> wave_ypart), row j's product
+//         (-a+ x_i, C^T x_i) goes to a ring slot in L2 (wave_ring);
+//   B(s): slice s's j-role entries read those 48-byte products from the ring
+//         (no coefficient re-read, no x_i gather), then the row tail.
+// B(s) needs A(s-lag .. s): tickets run A lag+1 slices ahead and B spins on
+// epoch-stamped done flags (its producers hold earlier tickets, so they are
+// running or done: no deadlock).  The ring holds wave_ring_slices slices
+// (far beyond the in-flight window, and A checks the B flags of the slot's
+// previous owners), so products are consumed from L2 and never written back.
+// Row sum: D x + i-role sum + j-role sum + pairs, fixed order.
+// ---------------------------------------------------------------------------
+#ifndef BDEM_WAVE_NW
+#define BDEM_WAVE_NW 4
+#endif
+#ifndef BDEM_WAVE_MINB
+#define BDEM_WAVE_MINB 8
+#endif
+constexpr int kWaveNW = BDEM_WAVE_NW;
+
+__device__ __forceinline__ int ld_acquire(const int32_t *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int32_t *p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// warp-wide spin until flags[lo..hi] all equal epoch (acquire loads)
+__device__ __forceinline__ void wait_flags(const int32_t *flags, int lo, int hi, int epoch,
+                                           int lane) {
+  for (int base = lo; base <= hi; base += 32) {
+    const int k = base + lane;
+    if (k <= hi)
+      while (ld_acquire(flags + k) != epoch) __nanosleep(32);
+  }
+  __syncwarp();
+}
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, BDEM_WAVE_MINB)
+    k_spmv_wave(bdem_system_t S, const double *__restrict__ x, double *__restrict__ y, int mode,
+                int epoch, int lead_rounds) {
+  __shared__ double part[NW][6][32];
+  __shared__ double sh[NW];
+  double *pcg = S.pcg;
+  if (mode == 1 && pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
+  const double boost = mode == 1 ? pcg[BDEM_PCG_BOOST] : 0.0;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t vs = S.vstride;
+  const int ns = (int)((S.n_elem + 31) >> 5);
+  const int L = (int)S.wave_lag, RING = (int)S.wave_ring_slices;
+  const int kmax = (int)(S.sell_kmax > 0 ? S.sell_kmax : 1);
+  const int64_t rs = (int64_t)RING * kmax * 32;  // ring plane stride
+  int32_t *flagA = S.wave_flags, *flagB = flagA + ns;
+  double *ring = S.wave_ring, *ypart = S.wave_ypart;
+  const int G = gridDim.x;
+  double acc_xy = 0.0, acc_yy = 0.0, acc_xx = 0.0;
+  // round m: A(blockIdx + (m + lead) G) then B(blockIdx + (m - 0) G); the first
+  // `lead` rounds only produce.  A waits on nothing but the ring's previous
+  // owners; B waits on A(s - L .. s), produced lead rounds earlier.
+  const int rounds = (ns + G - 1) / G + lead_rounds;
+#pragma unroll 1
+  for (int m = 0; m < rounds; ++m) {
+    const int sa = blockIdx.x + m * G;             // A slice of this round
+    const int sb = blockIdx.x + (m - lead_rounds) * G;  // B slice of this round
+    if (sa < ns) {
+      const int64_t row = (int64_t)sa * 32 + lane;
+      const int myslot = __ldg(S.row_slot + row);
+      if (sa >= RING && w == 0) wait_flags(flagB, sa - RING, min(sa - RING + L, ns - 1), epoch, lane);
+      __syncthreads();
+      double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      double xi[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      if (myslot >= 0) load6_ro(x, myslot, vs, xi);
+      const int64_t i0 = __ldg(S.slice_base + sa);
+      const int ki = (int)((__ldg(S.slice_base + sa + 1) - i0) >> 5);
+      double *rb = ring + ((int64_t)(sa % RING) * kmax) * 32 + lane;
+#pragma unroll 1
+      for (int k = w; k < ki; k += NW) {
+        const int64_t b = i0 + 32 * k + lane;
+        const int o = __ldg(S.pos_oslot + b);
+        if (o < 0 || myslot < 0) continue;
+        double xo[6];
+        load6_ro(x, o, vs, xo);
+        const Coef cv = load_coef<true>(S.scoef + cf_idx(b, 0));
+        const double nx = cv.al * ((cv.n[0] * xo[0] + cv.n[1] * xo[1]) + cv.n[2] * xo[2]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[c] -= nx * cv.n[c] + cv.be * xo[c];
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          acc[3 + q] += (cv.C[3 * q] * xo[3] + cv.C[3 * q + 1] * xo[4]) + cv.C[3 * q + 2] * xo[5];
+        // row j's product: -(a+ x_i) and C^T x_i (what k_spmv's j-role slot computes)
+        const double ni = cv.al * ((cv.n[0] * xi[0] + cv.n[1] * xi[1]) + cv.n[2] * xi[2]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) __stcg(rb + c * rs + (int64_t)k * 32, -(ni * cv.n[c] + cv.be * xi[c]));
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          __stcg(rb + (3 + q) * rs + (int64_t)k * 32,
+                 (cv.C[q] * xi[3] + cv.C[3 + q] * xi[4]) + cv.C[6 + q] * xi[5]);
+      }
+#pragma unroll
+      for (int q = 0; q < 6; ++q) part[w][q][lane] = acc[q];
+      __syncthreads();
+      for (int c = w; c < 6; c += NW) {
+        if (myslot < 0) continue;
+        double v = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < NW; ++ww) v += part[ww][c][lane];
+        __stcg(ypart + c * vs + myslot, v);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) st_release(flagA + sa, epoch);
+    }
+    if (sb >= 0 && sb < ns) {
+      const int64_t row = (int64_t)sb * 32 + lane;
+      const int myslot = __ldg(S.row_slot + row);
+      const int64_t j0 = __ldg(S.jslice_base + sb);
+      const int kj = (int)((__ldg(S.jslice_base + sb + 1) - j0) >> 5);
+      if (w == 0) wait_flags(flagA, max(sb - L, 0), sb, epoch, lane);
+      __syncthreads();
+      double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
+      for (int k = w; k < kj; k += NW) {
+        const int r = __ldg(S.wave_jring + j0 + 32 * k + lane);
+        if (r < 0 || myslot < 0) continue;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) acc[c] += __ldcg(ring + c * rs + r);
+      }
+#pragma unroll
+      for (int q = 0; q < 6; ++q) part[w][q][lane] = acc[q];
+      __syncthreads();
+      for (int c = w; c < 6; c += NW) {
+        if (myslot < 0) continue;
+        const int base = c < 3 ? 0 : 3, rr = c - base;
+        const double *dg = S.diag + (c < 3 ? 0 : 6 * vs);
+        double xs3[3];
+#pragma unroll
+        for (int u = 0; u < 3; ++u) xs3[u] = __ldg(x + (base + u) * vs + myslot);
+        double yc = (__ldg(dg + sidx<3>(rr, 0) * vs + myslot) * xs3[0] +
+                     __ldg(dg + sidx<3>(rr, 1) * vs + myslot) * xs3[1]) +
+                    __ldg(dg + sidx<3>(rr, 2) * vs + myslot) * xs3[2];
+        yc += __ldcg(ypart + c * vs + myslot);
+#pragma unroll
+        for (int ww = 0; ww < NW; ++ww) yc += part[ww][c][lane];
+        if (c < 3 && S.n_pair > 0) {
+          const int64_t e = __ldg(S.row_elem + row);
+          const int64_t pc = S.pair_cap;
+          const double *ps = S.pstage;
+          for (int k = S.pi_ptr[e]; k < S.pi_ptr[e + 1]; ++k) {
+            const int o = S.slot[S.pair_j[k]];
+            if (o < 0) continue;
+            yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[0 * vs + o] +
+                   ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[1 * vs + o]) +
+                  ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[2 * vs + o];
+          }
+          for (int kk = S.pj_ptr[e]; kk < S.pj_ptr[e + 1]; ++kk) {
+            const int64_t k = S.pj_idx[kk];
+            const int o = S.slot[S.pair_i[k]];
+            if (o < 0) continue;
+            yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[0 * vs + o] +
+                   ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[1 * vs + o]) +
+                  ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[2 * vs + o];
+          }
+        }
+        const double xc = xs3[rr];
+        if (boost != 0.0) yc = yc + boost * xc;
+        y[c * vs + myslot] = yc;
+        acc_xy += xc * yc;
+        acc_yy += yc * yc;
+        acc_xx += xc * xc;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) st_release(flagB + sb, epoch);
+    }
+  }
+  if (mode == 0) return;
+  spmv_pcg_epilogue<NW * 32>(S, boost, acc_xy, acc_yy, acc_xx, sh);
+}
+
+static bool launch_spmv_wave(const bdem_system_t &S, const double *x, double *y, int mode,
+                             cudaStream_t st) {
+  static int sms = 0, per_sm = 0, epoch = 0;
+  if (S.n_elem == 0 || S.wave_lag < 0 || !S.wave_flags || !S.wave_ring) return false;
+  auto kern = k_spmv_wave<kWaveNW>;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWaveNW * 32, 0);
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int ns = (int)((S.n_elem + 31) >> 5);
+  int g = sms * per_sm;
+  if (g > kRedBlocks) g = kRedBlocks;
+  // A runs lead rounds (lead * g slices) ahead of B: at least the lag, and the
+  // ring must outlast lead + lag + one round of slices
+  int lead_rounds = (int)((S.wave_lag + g) / g);
+  if ((int64_t)(lead_rounds + 2) * g + S.wave_lag > S.wave_ring_slices) return false;
+  if (++epoch <= 0) epoch = 1;
+  kern<<<g, kWaveNW * 32, 0, st>>>(S, x, y, mode, epoch, lead_rounds);
+  return true;
+}
+
 // resident-grid size of k_spmv (one wave), capped by the partial-sum slots
 static unsigned int spmv_grid() {
   static unsigned int g = 0;
@@ -1147,6 +1354,7 @@ static unsigned int spmv_grid() {
 // one SpMV launch (plain or PCG mode) with the configured kernel
 static void launch_spmv(const bdem_system_t &S, const double *x, double *y, int mode,
                         cudaStream_t st) {
+  if (spmv_kernel() == 3 && launch_spmv_wave(S, x, y, mode, st)) return;
   if (spmv_kernel() == 2 && launch_spmv_sym(S, x, y, mode, st)) return;
   if (launch_spmv_tile(S, x, y, mode, st)) return;
   const unsigned int g = spmv_grid();
@@ -1162,7 +1370,7 @@ extern "C" {
 int bdem_spmv_tile_slices(void) { return kTileTS; }
 int bdem_spmv_set_kernel(int kernel) {
   const int prev = spmv_kernel();
-  if (kernel >= 0 && kernel <= 2) g_spmv_kernel = kernel;
+  if (kernel >= 0 && kernel <= 3) g_spmv_kernel = kernel;
   return prev;
 }
 int bdem_spmv_sym_slices(void) { return kSymTS; }

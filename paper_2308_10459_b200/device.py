@@ -181,6 +181,30 @@ class SellLayout:
         jslot[jidx] = slot[bi[bnd]]
         return jloc, jb_base.astype(np.int32), jpos, jslot, kc, float(inside.mean()) if inside.size else 0.0
 
+    def wave_tables(self, bi, bj, slot, ring_slices: int):
+        """Tables of the dataflow SpMV: per j-role list entry the ring slot its
+        bond's i-role pass writes row j's product to (-1 when either end is
+        pinned or the entry is padding), and the lag = max slice(j) - slice(i).
+        Returns lag -1 when some bond has row(i) > row(j)."""
+        ri, rj = self.elem_row[bi], self.elem_row[bj]
+        kmax = max(self.kmax, 1)
+        jring = np.full(max(self.n_jpos, 1), -1, dtype=np.int32)
+        if bi.shape[0] == 0:
+            return jring, 0
+        if np.any(ri >= rj):
+            return jring, -1
+        si, sj = ri // 32, rj // 32
+        pos = self.pos_of_bond
+        k = (pos - self.slice_base[si]) // 32
+        ring = ((si % ring_slices) * kmax + k) * 32 + (ri % 32)
+        live = (slot[bi] >= 0) & (slot[bj] >= 0)
+        inv = np.full(self.n_pos, -1, dtype=np.int64)
+        inv[pos[live]] = ring[live]
+        valid = self.jpos >= 0
+        jring[:self.n_jpos][valid] = inv[self.jpos[valid]]
+        lag = int((sj - si)[live].max()) if live.any() else 0
+        return jring, lag
+
     def tile_headers(self, ts: int, stride: int) -> np.ndarray:
         """Per-tile header records of the tiled SpMV (see bdem_system_t.tile_hdr)."""
         ns = self.n_slices
@@ -317,6 +341,12 @@ class DeviceSystem:
         self.sym_jloc = _t(np.append(jloc, -1), I32, dev)
         self.sym_jbase, self.sym_jpos = _t(jbase, I32, dev), _t(jpos_b, I32, dev)
         self.sym_jslot, self.sym_kc = _t(jslot_b, I32, dev), kc
+        ring = 4096
+        jring, lag = sell.wave_tables(bi64, bj64, slot, ring)
+        self.wave_jring, self.wave_lag, self.wave_ring_slices = _t(jring, I32, dev), lag, ring
+        self.wave_ring = torch.zeros(6 * ring * max(sell.kmax, 1) * 32, dtype=F64, device=dev)
+        self.wave_ypart = torch.zeros(6 * max(32, (nf + 31) // 32 * 32), dtype=F64, device=dev)
+        self.wave_flags = torch.zeros(2 * sell.n_slices + 4, dtype=I32, device=dev)
         self.pos_of_bond_d = torch.as_tensor(sell.pos_of_bond).to(dev)
         # staging / reduced system
         self.stage = torch.zeros((L.ST["COUNT"], npos), dtype=F64, device=dev)
@@ -366,6 +396,9 @@ class DeviceSystem:
         s.tile_hdr = _ptr(self.tile_hdr)
         s.sym_jloc, s.sym_jbase = _ptr(self.sym_jloc), _ptr(self.sym_jbase)
         s.sym_jpos, s.sym_jslot, s.sym_kc = _ptr(self.sym_jpos), _ptr(self.sym_jslot), self.sym_kc
+        s.wave_jring, s.wave_lag = _ptr(self.wave_jring), self.wave_lag
+        s.wave_ring_slices, s.wave_ring = self.wave_ring_slices, _ptr(self.wave_ring)
+        s.wave_ypart, s.wave_flags = _ptr(self.wave_ypart), _ptr(self.wave_flags)
         s.stage, s.diag, s.minv = _ptr(self.stage), _ptr(self.diag), _ptr(self.minv)
         s.scoef = _ptr(self.scoef)
         s.red, s.scalars, s.pcg = _ptr(self.red), _ptr(self.scalars), _ptr(self.pcg_state)

@@ -5,6 +5,7 @@ sys.path.insert(0, os.getcwd())
 from paper_2308_10459_b200 import _build
 # name: extra flags
 V = {"blocked": ["-DBDEM_SPMV_BLOCKED=1"],
+     "wave_m6": ["-DBDEM_WAVE_MINB=6"], "wave_m5": ["-DBDEM_WAVE_MINB=5"],
      "sym_t2w8m3": ["-DBDEM_SYM_TS=2", "-DBDEM_SYM_NW=8", "-DBDEM_SYM_MINB=3"],
      "sym_t2w4m6": ["-DBDEM_SYM_TS=2", "-DBDEM_SYM_NW=4", "-DBDEM_SYM_MINB=6"],
      "sym_t4w16m1": ["-DBDEM_SYM_TS=4", "-DBDEM_SYM_NW=16", "-DBDEM_SYM_MINB=1"],
