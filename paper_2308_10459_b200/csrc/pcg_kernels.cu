@@ -22,6 +22,14 @@
 namespace bdem {
 
 enum { PCG_RUNNING = 0, PCG_CONVERGED = 1, PCG_BREAKDOWN = 2, PCG_MAXIT = 3 };
+
+// Programmatic dependent launch: the PCG kernels are launched with
+// programmatic stream serialisation, so a kernel's CTAs are scheduled as the
+// previous kernel's CTAs retire; each waits here until the previous grid has
+// completed and its writes are visible (a no-op for ordinary launches).
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 enum { CNT_SPMV = 2, CNT_UPDATE = 3, CNT_INIT = 4 };
 // partial-sum columns of sys->red owned by PCG (disjoint from BDEM_SC_*)
 enum { RC_PAP = 20, RC_AP2 = 21, RC_PP2 = 22, RC_RR = 23, RC_RZ = 24, RC_IRR = 25, RC_IRZ = 26 };
@@ -246,6 +254,7 @@ __global__ void __launch_bounds__(kSpmvThreads, BDEM_SPMV_MINB) k_spmv(bdem_syst
                                                        int mode) {
   __shared__ double part[kSpmvWarps][6][32];
   __shared__ double sh[kSpmvThreads / 32];
+  griddep_wait();
   double *pcg = S.pcg;
   if (mode == 1 && pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
   const double boost = mode == 1 ? pcg[BDEM_PCG_BOOST] : 0.0;
@@ -295,6 +304,7 @@ __global__ void __launch_bounds__(kThreads, BDEM_UPD_MINB) k_pcg_update(bdem_sys
                                                          double *zv, const double *p,
                                                          const double *ap) {
   __shared__ double sh[kThreads / 32];
+  griddep_wait();
   double *pcg = S.pcg;
   if (pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
   const double alpha = pcg[BDEM_PCG_ALPHA];
@@ -371,6 +381,7 @@ __global__ void __launch_bounds__(kThreads, BDEM_UPD_MINB) k_pcg_update(bdem_sys
 // p = z + beta p (linalg.py:91)
 __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(bdem_system_t S, double *p,
                                                           const double *zv) {
+  griddep_wait();
   const double *pcg = S.pcg;
   if (pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
   const double beta = pcg[BDEM_PCG_BETA];
@@ -1337,6 +1348,31 @@ static bool launch_spmv_wave(const bdem_system_t &S, const double *x, double *y,
   return true;
 }
 
+// launch with programmatic stream serialisation (see griddep_wait)
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+static bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char *env = getenv("BDEM_PDL");
+    on = env ? atoi(env) != 0 : 1;
+  }
+  return on != 0;
+}
+
 // resident-grid size of k_spmv (one wave), capped by the partial-sum slots
 static unsigned int spmv_grid() {
   static unsigned int g = 0;
@@ -1412,10 +1448,18 @@ int bdem_pcg_iterate(const bdem_system_t *sys, double *x, double *r, double *zv,
                      double *ap, int n_iter, void *stream) {
   if (!sys || n_iter < 0) return BDEM_ERR_ARG;
   cudaStream_t st = as_stream(stream);
+  const bool pdl = pdl_enabled() && spmv_kernel() == 0;
   for (int it = 0; it < n_iter; ++it) {
-    launch_spmv(*sys, pv, ap, 1, st);
-    k_pcg_update<<<kRedBlocks, kThreads, 0, st>>>(*sys, x, r, zv, pv, ap);
-    k_pcg_pupdate<<<kRedBlocks, kThreads, 0, st>>>(*sys, pv, zv);
+    if (pdl) {
+      launch_pdl(k_spmv, spmv_grid(), kSpmvThreads, st, *sys, (const double *)pv, ap, 1);
+      launch_pdl(k_pcg_update, kRedBlocks, kThreads, st, *sys, x, r, zv, (const double *)pv,
+                 (const double *)ap);
+      launch_pdl(k_pcg_pupdate, kRedBlocks, kThreads, st, *sys, pv, (const double *)zv);
+    } else {
+      launch_spmv(*sys, pv, ap, 1, st);
+      k_pcg_update<<<kRedBlocks, kThreads, 0, st>>>(*sys, x, r, zv, pv, ap);
+      k_pcg_pupdate<<<kRedBlocks, kThreads, 0, st>>>(*sys, pv, zv);
+    }
   }
   return launch_status(3 * (int64_t)n_iter);
 }
