@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define BDEM_ABI_VERSION 1
+#define BDEM_ABI_VERSION 2
 
 enum {
   BDEM_OK = 0,

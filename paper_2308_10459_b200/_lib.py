@@ -28,6 +28,7 @@ SC = dict(F=0, GNORM2=1, CNORM2=2, MAXDEV=3, SLOPE=4, FT=5, NSING=6, EBOND=7, EC
 PCG = dict(RZ=0, PAP=1, ALPHA=2, BETA=3, RR=4, BNORM=5, REL=6, TOL=7, BOOST=8, APNORM2=9,
            PNORM2=10, K=11, MAXIT=12, STATE=13, COUNT=16)
 PCG_RUNNING, PCG_CONVERGED, PCG_BREAKDOWN, PCG_MAXIT = 0, 1, 2, 3
+ABI_VERSION = 2
 RED_BLOCKS = 1184
 MAX_COLLIDERS = 8
 N_COUNTERS = 16
@@ -136,6 +137,9 @@ def load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    if lib.bdem_abi_version() != ABI_VERSION:
+        raise BdemLibraryError(f"library ABI {lib.bdem_abi_version()} != expected {ABI_VERSION}; "
+                               "rebuild with __graft_entry__.build()")
     if lib.bdem_system_size() != C.sizeof(System):
         raise BdemLibraryError(f"bdem_system_t size mismatch: C {lib.bdem_system_size()} "
                                f"vs ctypes {C.sizeof(System)}")
