@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--c5-side", type=int, default=126)
     ap.add_argument("--crop", type=int, nargs=2, default=(100, 60),
                     help="plate crop for the CPU sample (nx ny)")
+    ap.add_argument("--ref-crop", type=int, nargs=2, default=(60, 36),
+                    help="plate crop of one reference-arm step (nx ny)")
     return ap.parse_args()
 
 
@@ -75,13 +77,12 @@ def peaks():
 # CPU reference arm (oracle on a bounded crop)
 # ---------------------------------------------------------------------------
 
-def cpu_sample(nx, ny, eps, warmup_steps, min_newton, threads):
+def cpu_sample(nx, ny, eps, warmup_steps, timed_steps, threads):
     """The reference algorithm (CPU oracle) on a bounded sample of the same
     workload: full implicit steps (stable_step) of an nx x ny crop of the
-    plate with the bench's epsilon; `warmup_steps` untimed, then timed steps
-    until at least `min_newton` Newton iterations (at least one step).
-    Returns (Newton it/s on the crop, crop bonds, iterations, PCG per
-    iteration, seconds, steps)."""
+    plate with the bench's epsilon; `warmup_steps` untimed, then exactly
+    `timed_steps` timed steps (at least one).  Returns (Newton it/s on the
+    crop, crop bonds, iterations, PCG per iteration, seconds, steps)."""
     from threadpoolctl import threadpool_limits
 
     from oracle import cpu_oracle as O
@@ -96,7 +97,7 @@ def cpu_sample(nx, ny, eps, warmup_steps, min_newton, threads):
             O.step(st, cfg)
         its = pcg = steps = 0
         t0 = time.perf_counter()
-        while steps == 0 or its < min_newton:
+        while steps < max(timed_steps, 1):
             out = O.step(st, cfg)
             its += out.solve.iterations
             pcg += out.solve.pcg_total
@@ -115,15 +116,15 @@ def run_reference(args):
         C.plate(nx=args.nx, ny=args.ny).bonds.n
     cores = os.cpu_count() or 1
     rate, nb_crop, its, pcg, sec, steps = cpu_sample(
-        args.crop[0], args.crop[1], args.epsilon, min(args.warmup, 1), args.steps, cores)
+        args.ref_crop[0], args.ref_crop[1], args.epsilon, args.warmup, args.steps, cores)
     value = rate * nb_crop / nb_full
-    sample = (f"oracle (numpy/scipy, {cores} threads) {steps} implicit step(s) after "
-              f"{min(args.warmup, 1)} warm-up of a {args.crop[0]}x{args.crop[1]} crop of the "
-              f"plate ({nb_crop} bonds): {its} Newton iterations, {pcg:.1f} PCG/it, {sec:.1f}s; "
-              f"scaled by bonds {nb_crop}/{nb_full}")
+    sample = (f"oracle (numpy/scipy, {cores} threads): each step one implicit step of a "
+              f"{args.ref_crop[0]}x{args.ref_crop[1]} crop of the plate ({nb_crop} bonds); {steps} "
+              f"timed after {args.warmup} warm-up: {its} Newton iterations, {pcg:.1f} PCG/it, "
+              f"{sec:.1f}s; scaled by bonds {nb_crop}/{nb_full}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": steps, "warmup": min(args.warmup, 1),
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
         "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_block(args), "pcg_per_newton": pcg,
