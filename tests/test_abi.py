@@ -92,3 +92,14 @@ def test_friction_schedule_edges(lib):
     disjoint = np.stack([np.arange(0, 10, 2), np.arange(1, 10, 2)], 1)
     assert _schedule(lib, disjoint, 10)[0] == 1
     assert _schedule(lib, np.array([[0, 10]]), 10)[0] == -L.ERR_ARG   # out-of-range element
+
+
+def test_graft_entry_build(lib):
+    """The driver's build check: __graft_entry__.build() (incremental here)
+    compiles, loads the library and checks its ABI version."""
+    import importlib
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    entry = importlib.import_module("__graft_entry__")
+    entry.build()
