@@ -126,7 +126,10 @@ __global__ void __launch_bounds__(128) k_bond_ambient(bdem_system_t S, const dou
 // fused production kernel: energy, gradient contributions and the clamped
 // reduced blocks (energy_terms + build_clamped_pieces, solver.py:141-162)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128, 4) k_bond_assemble(bdem_system_t S, const double *p,
+#ifndef BDEM_ASM_MINB
+#define BDEM_ASM_MINB 4
+#endif
+__global__ void __launch_bounds__(128, BDEM_ASM_MINB) k_bond_assemble(bdem_system_t S, const double *p,
                                                        const double *q) {
   const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nb = S.n_bond;
@@ -139,64 +142,75 @@ __global__ void __launch_bounds__(128, 4) k_bond_assemble(bdem_system_t S, const
     store_coef(S.scoef + cf_idx(b, 0), zero);
     return;
   }
-  BondIn B;
-  load_bond(S, b, B);
+  // Outputs are stored as soon as each piece is final so the stretch state
+  // is dead before the rotation block is formed (register pressure).
+  const int bi = S.bond_i[b], bj = S.bond_j[b];
+  const double *g = S.geom;
+  const double scale = S.bstate[BDEM_BS_SCALE * nb + b];
+  double *cf = S.scoef + cf_idx(b, 0);
   double pi[3], pj[3], qi[4], qj[4];
-  load_pq(p, q, B.i, pi, qi);
-  load_pq(p, q, B.j, pj, qj);
-  const double ks = B.scale * B.kn, kts = B.scale * B.kt;
-  double kds[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) kds[c] = B.scale * B.kd[c];
+  load_pq(p, q, bi, pi, qi);
+  load_pq(p, q, bj, pj, qj);
 
   // stretch: energy, gradient (kc n) and the closed-form clamp of
   // [[a,-a],[-a,a]]: a+ = k (nn + max(c/l,0) (I - nn)) = alpha nn + beta I
-  const Stretch st = stretch_eval(pi, pj, B.l0, ks);
-  if (st.degenerate) flag_error(S.err, BDEM_ERR_DEGENERATE_BOND, b);
-  const double f = st.c_over_l > 0.0 ? st.c_over_l : 0.0;
-  const double beta = ks * f;
-  const double alpha = ks - beta;
+  double e_s;
+  {
+    const double ks = scale * g[BDEM_BG_KN * nb + b];
+    const Stretch st = stretch_eval(pi, pj, g[BDEM_BG_L0 * nb + b], ks);
+    if (st.degenerate) flag_error(S.err, BDEM_ERR_DEGENERATE_BOND, b);
+    const double f = st.c_over_l > 0.0 ? st.c_over_l : 0.0;
+    const double beta = ks * f;
+    const double alpha = ks - beta;
+    e_s = st.E;
+    st_out[BDEM_ST_KC * nb + b] = st.kc;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) cf[32 * (BDEM_CF_N + c)] = st.n[c];
+    cf[32 * BDEM_CF_ALPHA] = alpha;
+    cf[32 * BDEM_CF_BETA] = beta;
+  }
 
-  const Shear sh = shear_eval(qi, qj, B.d0, kts);
-  if (sh.antipodal) flag_error(S.err, BDEM_ERR_ANTIPODAL, b);
   double S6[21];
-  const RotOut ro = reduced_rotation(qi, qj, B.d0, B.F, kds, sh, S6);
-
-  st_out[BDEM_ST_E * nb + b] = (st.E + sh.E) + ro.E_b;
-  double cfv[BDEM_CF_COUNT];
+  {
+    double d0[3], F[3][3], kds[3];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) cfv[BDEM_CF_N + c] = st.n[c];
-  st_out[BDEM_ST_KC * nb + b] = st.kc;
-  cfv[BDEM_CF_ALPHA] = alpha;
-  cfv[BDEM_CF_BETA] = beta;
+    for (int c = 0; c < 3; ++c) d0[c] = g[(BDEM_BG_D0 + c) * nb + b];
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    st_out[(BDEM_ST_GQI + c) * nb + b] = sh.g[c] + ro.gbi[c];
-    st_out[(BDEM_ST_GQJ + c) * nb + b] = sh.g[c] + ro.gbj[c];
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) F[r][c] = g[(BDEM_BG_FRAME + 3 * r + c) * nb + b];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) kds[c] = scale * g[(BDEM_BG_KDIAG + c) * nb + b];
+    const Shear sh = shear_eval(qi, qj, d0, scale * g[BDEM_BG_KT * nb + b]);
+    if (sh.antipodal) flag_error(S.err, BDEM_ERR_ANTIPODAL, b);
+    const RotOut ro = reduced_rotation(qi, qj, d0, F, kds, sh, S6);
+    st_out[BDEM_ST_E * nb + b] = (e_s + sh.E) + ro.E_b;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      st_out[(BDEM_ST_GQI + c) * nb + b] = sh.g[c] + ro.gbi[c];
+      st_out[(BDEM_ST_GQJ + c) * nb + b] = sh.g[c] + ro.gbj[c];
+    }
   }
-
-  // PSD blocks (all of them at identity orientations) are final here;
-  // indefinite ones are queued for the register-resident eigen-clamp pass
-  // (k_bond_clamp) and staged unclamped meanwhile
-  __shared__ double psd_work[21 * 128];
-  double mx = 0.0;
-#pragma unroll
-  for (int t = 0; t < 21; ++t) mx = fmax(mx, fabs(S6[t]));
-  if (mx != 0.0 && !psd_within<6>(S6, 4e-14 * mx, psd_work + threadIdx.x, 128)) {
-    const unsigned int slot = atomicAdd(S.counter + kClampCounter, 1u);
-    S.clamp_list[slot] = (int32_t)b;
-  }
-
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) cfv[BDEM_CF_C + 3 * r + c] = S6[sidx<6>(r, c + 3)];
-  store_coef(S.scoef + cf_idx(b, 0), cfv);
+    for (int c = 0; c < 3; ++c) cf[32 * (BDEM_CF_C + 3 * r + c)] = S6[sidx<6>(r, c + 3)];
   const int pr[6] = {0, 0, 0, 1, 1, 2}, pc[6] = {0, 1, 2, 1, 2, 2};
 #pragma unroll
   for (int t = 0; t < 6; ++t) {
     st_out[(BDEM_ST_A + t) * nb + b] = S6[sidx<6>(pr[t], pc[t])];
     st_out[(BDEM_ST_D + t) * nb + b] = S6[sidx<6>(pr[t] + 3, pc[t] + 3)];
+  }
+
+  // PSD blocks (all of them at identity orientations) are final as staged;
+  // indefinite ones are queued for the register-resident eigen-clamp pass
+  // (k_bond_clamp), which overwrites the staged block
+  double mx = 0.0;
+#pragma unroll
+  for (int t = 0; t < 21; ++t) mx = fmax(mx, fabs(S6[t]));
+  if (mx != 0.0 && !psd6_regs(S6, 4e-14 * mx)) {
+    const unsigned int slot = atomicAdd(S.counter + kClampCounter, 1u);
+    S.clamp_list[slot] = (int32_t)b;
   }
 }
 
