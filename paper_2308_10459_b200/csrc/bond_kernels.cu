@@ -174,22 +174,23 @@ __global__ void __launch_bounds__(128, BDEM_ASM_MINB) k_bond_assemble(bdem_syste
   {
     double d0[3], F[3][3], kds[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) d0[c] = g[(BDEM_BG_D0 + c) * nb + b];
-#pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
       for (int c = 0; c < 3; ++c) F[r][c] = g[(BDEM_BG_FRAME + 3 * r + c) * nb + b];
 #pragma unroll
     for (int c = 0; c < 3; ++c) kds[c] = scale * g[(BDEM_BG_KDIAG + c) * nb + b];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) d0[c] = g[(BDEM_BG_D0 + c) * nb + b];
     const Shear sh = shear_eval(qi, qj, d0, scale * g[BDEM_BG_KT * nb + b]);
     if (sh.antipodal) flag_error(S.err, BDEM_ERR_ANTIPODAL, b);
-    const RotOut ro = reduced_rotation(qi, qj, d0, F, kds, sh, S6);
+    const RotGrad ro = rot_grad(qi, qj, F, kds);
     st_out[BDEM_ST_E * nb + b] = (e_s + sh.E) + ro.E_b;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       st_out[(BDEM_ST_GQI + c) * nb + b] = sh.g[c] + ro.gbi[c];
       st_out[(BDEM_ST_GQJ + c) * nb + b] = sh.g[c] + ro.gbj[c];
     }
+    rot_block(qi, qj, d0, F, kds, sh, ro.rs, ro.rv, ro.w, S6);
   }
 #pragma unroll
   for (int r = 0; r < 3; ++r)
