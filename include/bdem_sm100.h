@@ -353,6 +353,12 @@ int bdem_spmv(const bdem_system_t *sys, const double *x, double *y, void *stream
  * previous variant; any other value only queries.  BDEM_SPMV_TILE=1 in the
  * environment selects the tiled one at load time. */
 int bdem_spmv_set_kernel(int kernel);
+/* PCG update path of bdem_pcg_iterate: 0 = k_pcg_update + k_pcg_pupdate
+ * (default), 1 = one fused kernel over a co-resident grid (grid barrier
+ * between the r/z and the x/p halves; bit-identical iterates; used only when
+ * n_free <= BDEM_RED_BLOCKS * 512).  Returns the previous setting; any other
+ * value only queries.  BDEM_FUSED_UPD=1 selects it at load time. */
+int bdem_pcg_set_fused(int on);
 /* Slices per tile of the tiled SpMV and the int32 stride of sys->tile_hdr. */
 int bdem_spmv_tile_slices(void);
 int bdem_spmv_tile_hdr_ints(void);

@@ -102,6 +102,7 @@ SIGNATURES = {
     "bdem_select_workspace": (_i64, [_i64]),
     "bdem_select_flagged": (_int, [_p, _i64, _p, _p, C.POINTER(C.c_int64), _p]),
     "bdem_spmv_set_kernel": (_int, [_int]),
+    "bdem_pcg_set_fused": (_int, [_int]),
     "bdem_spmv_tile_slices": (_int, []),
     "bdem_spmv_sym_slices": (_int, []),
     "bdem_spmv_sym_kcap": (_int, []),

@@ -219,7 +219,17 @@ __global__ void __launch_bounds__(128, BDEM_ASM_MINB) k_bond_assemble(bdem_syste
 // eigen-clamp pass for the queued indefinite rotation blocks (spd_project,
 // solver.py:89-113): one thread per queued bond, Jacobi in registers
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_bond_clamp(bdem_system_t S) {
+// occupancy: unbounded, the Jacobi pass takes 182 registers (2 CTAs = 8
+// warps per SM); capped at 168 (3 CTAs, 36 B of spills) it runs 12% faster
+// (C5-like random-q blocks, profiles/r01/README.md); 32- or 64-thread CTAs
+// at 182 registers do not help
+#ifndef BDEM_CLAMP_THREADS
+#define BDEM_CLAMP_THREADS 128
+#endif
+#ifndef BDEM_CLAMP_MINB
+#define BDEM_CLAMP_MINB 3
+#endif
+__global__ void __launch_bounds__(BDEM_CLAMP_THREADS, BDEM_CLAMP_MINB) k_bond_clamp(bdem_system_t S) {
   const unsigned int n = S.counter[kClampCounter];
   const int64_t nb = S.n_bond;
   double *st = S.stage;
@@ -411,7 +421,7 @@ int bdem_bond_assemble(const bdem_system_t *sys, const double *p, const double *
   cudaMemsetAsync(sys->counter + kClampCounter, 0, sizeof(unsigned int), st);
   k_bond_assemble<<<grid_for(sys->n_bond, 128), 128, 0, st>>>(*sys, p, q);
   // the clamp pass reads the queue length on the device; idle threads exit
-  k_bond_clamp<<<kRedBlocks, 128, 0, st>>>(*sys);
+  k_bond_clamp<<<kRedBlocks * (128 / BDEM_CLAMP_THREADS), BDEM_CLAMP_THREADS, 0, st>>>(*sys);
   return launch_status(2);
 }
 

@@ -667,3 +667,30 @@ def test_tiled_spmv_newton_solve_vs_golden(cuda_ok, variant):
         test_newton_solve_vs_golden(cuda_ok)
     finally:
         lib.bdem_spmv_set_kernel(prev)
+
+
+def test_fused_pcg_update_bit_identical(cuda_ok):
+    """k_pcg_update_fused (grid barrier between the r/z and x/p halves) gives
+    the same iterate, bit for bit, as the two-kernel path: same virtual
+    blocks, same partial sums, same state transitions, through convergence."""
+    import torch
+    from paper_2308_10459_b200 import configs as C
+    dev = _assembled(C.plate(nx=100, ny=60, epsilon=1e-6))
+    ptrs = (dev.y.data_ptr(), dev.r.data_ptr(), dev.zv.data_ptr(), dev.pv.data_ptr())
+    out = []
+    for fused in (0, 1):
+        prev = dev.lib.bdem_pcg_set_fused(fused)
+        try:
+            dev.call("bdem_pcg_init", dev.sysp, dev.z.data_ptr(), -1.0, *ptrs, 1e-7, 3000, 0.0,
+                     dev.stream)
+            for _ in range(50):
+                dev.call("bdem_pcg_iterate", dev.sysp, *ptrs, dev.ap.data_ptr(), 64, dev.stream)
+            torch.cuda.synchronize()
+        finally:
+            dev.lib.bdem_pcg_set_fused(prev)
+        st = dev.pcg_state.cpu().numpy().copy()
+        out.append((st, dev.y.cpu().numpy().copy(), dev.pv.cpu().numpy().copy()))
+    (s0, y0, p0), (s1, y1, p1) = out
+    assert s0[13] in (1, 3) and s0[11] > 50   # stopped (converged / max-it) after many iterations
+    assert np.array_equal(s0, s1)
+    assert np.array_equal(y0, y1) and np.array_equal(p0, p1)
