@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define BDEM_ABI_VERSION 2
+#define BDEM_ABI_VERSION 3
 
 enum {
   BDEM_OK = 0,
@@ -210,6 +210,14 @@ typedef struct {
   double *wave_ring;             /* 6 planes x wave_ring_slices * sell_kmax * 32 */
   double *wave_ypart;            /* 6 planes x vstride: rows' i-role sums */
   int32_t *wave_flags;           /* 2 x n_slices epoch stamps (A done, B done) + ticket */
+  /* warp-shuffle SpMV (bdem_spmv_set_kernel(4)): a bond whose two rows share
+   * a slice hands row j its product -a+ x_i, C^T x_i through a warp shuffle
+   * at its i-role slot.  shfl_src[pos] = sending lane for the RECEIVING lane
+   * (pos & 31) at that slot, -1 none (at most one sender per receiver and
+   * slot; the rest stay in the lists); shfl_jbase/jpos/jslot: the j-role
+   * lists without the handed-over bonds, SELL shape */
+  const int8_t *shfl_src;
+  const int32_t *shfl_jbase, *shfl_jpos, *shfl_jslot;
   const int32_t *tile_hdr;       /* per SpMV tile (bdem_spmv_tile_slices() slices):
                                     BDEM_TILE_HDR ints = slice_base[t0..t0+TS],
                                     jslice_base[t0..t0+TS], slice_slot[t0], slice_slot[t1] */
@@ -349,7 +357,9 @@ int bdem_spmv(const bdem_system_t *sys, const double *x, double *y, void *stream
 /* SpMV kernel variant for every later SpMV launch: 0 = slot-parallel
  * (default), 1 = tiled (cp.async.bulk + mbarrier ring, warp-specialised
  * producer; pays off only with compact tiles, BDEM_ROW_ORDER=z), 2 =
- * contribution table (BDEM_ROW_ORDER=strip).  Returns the
+ * contribution table (BDEM_ROW_ORDER=strip), 3 = dataflow ring, 4 =
+ * slot-parallel with in-slice hand-over by warp shuffle (compact slices:
+ * BDEM_ROW_ORDER=strip8 or z).  Returns the
  * previous variant; any other value only queries.  BDEM_SPMV_TILE=1 in the
  * environment selects the tiled one at load time. */
 int bdem_spmv_set_kernel(int kernel);

@@ -296,6 +296,110 @@ __global__ void __launch_bounds__(kSpmvThreads, BDEM_SPMV_MINB) k_spmv(bdem_syst
   spmv_pcg_epilogue<kSpmvThreads>(S, boost, acc_xy, acc_yy, acc_xx, sh);
 }
 
+// ---------------------------------------------------------------------------
+// SpMV variant 4: slot-parallel as k_spmv, plus in-slice hand-over.  At an
+// i-role slot every lane also forms the transposed product of its bond for
+// row j, t = -a+ x_i (+) C^T x_i, from its OWN row's x; the lane of row j
+// takes it with a warp shuffle when the host marked it as the receiver
+// (shfl_src).  Such a bond's coefficients and x_i are therefore read once
+// instead of twice (no j-role re-read from L2, no x_i gather); the j-role
+// lists hold only the remaining bonds.  Same terms per row as k_spmv in a
+// different (fixed) order: deterministic, equal to round-off.
+// ---------------------------------------------------------------------------
+#ifndef BDEM_SHFL_MINB
+#define BDEM_SHFL_MINB 6
+#endif
+__global__ void __launch_bounds__(kSpmvThreads, BDEM_SHFL_MINB)
+    k_spmv_shfl(bdem_system_t S, const double *x, double *y, int mode) {
+  __shared__ double part[kSpmvWarps][6][32];
+  __shared__ double sh[kSpmvThreads / 32];
+  griddep_wait();
+  double *pcg = S.pcg;
+  if (mode == 1 && pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
+  const double boost = mode == 1 ? pcg[BDEM_PCG_BOOST] : 0.0;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nf = S.vstride;
+  const int ns = (int)((S.n_elem + 31) >> 5);
+  double acc_xy = 0.0, acc_yy = 0.0, acc_xx = 0.0;
+#pragma unroll 1
+  for (int sl = blockIdx.x; sl < ns; sl += gridDim.x) {
+    const int a0 = __ldg(S.slice_base + sl), a1 = __ldg(S.slice_base + sl + 1);
+    const int c0 = __ldg(S.shfl_jbase + sl), c1 = __ldg(S.shfl_jbase + sl + 1);
+    const int ki = (a1 - a0) >> 5, kj = (c1 - c0) >> 5;
+    const int own = __ldg(S.row_slot + (int64_t)sl * 32 + lane);
+    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    // i-role slots with hand-over (warp-uniform trip count: shuffles); the
+    // next slot's indices are in flight while this slot's data arrive
+    int o_n = -1, src_n = -1;
+    if (w < ki) {
+      o_n = __ldg(S.pos_oslot + a0 + 32 * w + lane);
+      src_n = __ldg(S.shfl_src + a0 + 32 * w + lane);
+    }
+#pragma unroll 1
+    for (int k = w; k < ki; k += kSpmvWarps) {
+      const int64_t b = a0 + 32 * k + lane;
+      const int o = o_n, src = src_n;
+      if (k + kSpmvWarps < ki) {
+        o_n = __ldg(S.pos_oslot + b + 32 * kSpmvWarps);
+        src_n = __ldg(S.shfl_src + b + 32 * kSpmvWarps);
+      }
+      double t[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      if (o >= 0) {
+        double xo[6];
+        load6_ro(x, o, nf, xo);
+        const Coef cv = load_coef<true>(S.scoef + cf_idx(b, 0));
+        const double nx = cv.al * ((cv.n[0] * xo[0] + cv.n[1] * xo[1]) + cv.n[2] * xo[2]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[c] -= nx * cv.n[c] + cv.be * xo[c];
+#pragma unroll
+        for (int qq = 0; qq < 3; ++qq)
+          acc[3 + qq] += (cv.C[3 * qq] * xo[3] + cv.C[3 * qq + 1] * xo[4]) + cv.C[3 * qq + 2] * xo[5];
+        if (own >= 0) {
+          // row j's product from this row's x (the j-role formula of slot_apply)
+          double xi[6];
+          load6_ro(x, own, nf, xi);
+          const double ni = cv.al * ((cv.n[0] * xi[0] + cv.n[1] * xi[1]) + cv.n[2] * xi[2]);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) t[c] = -(ni * cv.n[c] + cv.be * xi[c]);
+#pragma unroll
+          for (int qq = 0; qq < 3; ++qq)
+            t[3 + qq] = (cv.C[qq] * xi[3] + cv.C[3 + qq] * xi[4]) + cv.C[6 + qq] * xi[5];
+        }
+      }
+      const int from = src >= 0 ? src : lane;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        const double v = __shfl_sync(0xffffffffu, t[c], from);
+        if (src >= 0) acc[c] += v;
+      }
+    }
+    // remaining j-role bonds (lists without the handed-over ones)
+    SlotRef cur{0, -1, true};
+    if (w < kj) {
+      cur.o = __ldg(S.shfl_jslot + c0 + 32 * w + lane);
+      cur.b = __ldg(S.shfl_jpos + c0 + 32 * w + lane);
+    }
+#pragma unroll 1
+    for (int k = w; k < kj; k += kSpmvWarps) {
+      SlotRef nxt{0, -1, true};
+      if (k + kSpmvWarps < kj) {
+        const int64_t jk = c0 + 32 * (k + kSpmvWarps) + lane;
+        nxt.o = __ldg(S.shfl_jslot + jk);
+        nxt.b = __ldg(S.shfl_jpos + jk);
+      }
+      slot_apply(S, x, cur, acc);
+      cur = nxt;
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) part[w][q][lane] = acc[q];
+    __syncthreads();
+    spmv_tail<kSpmvWarps>(S, x, y, sl, w, lane, part, boost, acc_xy, acc_yy, acc_xx);
+    __syncthreads();
+  }
+  if (mode == 0) return;
+  spmv_pcg_epilogue<kSpmvThreads>(S, boost, acc_xy, acc_yy, acc_xx, sh);
+}
+
 // x += alpha p; r -= alpha Ap; z = M^-1 r; r.r, r.z (linalg.py:79-89)
 #ifndef BDEM_UPD_MINB
 #define BDEM_UPD_MINB 4
@@ -1070,7 +1174,7 @@ static int spmv_kernel() {
   if (g_spmv_kernel < 0) {
     const char *env = getenv("BDEM_SPMV_TILE");
     g_spmv_kernel = env ? atoi(env) : 0;
-    if (g_spmv_kernel < 0 || g_spmv_kernel > 3) g_spmv_kernel = 0;
+    if (g_spmv_kernel < 0 || g_spmv_kernel > 4) g_spmv_kernel = 0;
   }
   return g_spmv_kernel;
 }
@@ -1614,6 +1718,10 @@ static void launch_update_fused(unsigned int grid, cudaStream_t st, bool pdl,
 static void launch_spmv(const bdem_system_t &S, const double *x, double *y, int mode,
                         cudaStream_t st) {
   if (spmv_kernel() == 3 && launch_spmv_wave(S, x, y, mode, st)) return;
+  if (spmv_kernel() == 4 && S.shfl_src && S.shfl_jbase) {
+    k_spmv_shfl<<<spmv_grid(), kSpmvThreads, 0, st>>>(S, x, y, mode);
+    return;
+  }
   if (spmv_kernel() == 2 && launch_spmv_sym(S, x, y, mode, st)) return;
   if (launch_spmv_tile(S, x, y, mode, st)) return;
   const unsigned int g = spmv_grid();
@@ -1629,7 +1737,7 @@ extern "C" {
 int bdem_spmv_tile_slices(void) { return kTileTS; }
 int bdem_spmv_set_kernel(int kernel) {
   const int prev = spmv_kernel();
-  if (kernel >= 0 && kernel <= 3) g_spmv_kernel = kernel;
+  if (kernel >= 0 && kernel <= 4) g_spmv_kernel = kernel;
   return prev;
 }
 int bdem_pcg_set_fused(int on) {
@@ -1676,12 +1784,15 @@ int bdem_pcg_iterate(const bdem_system_t *sys, double *x, double *r, double *zv,
                      double *ap, int n_iter, void *stream) {
   if (!sys || n_iter < 0) return BDEM_ERR_ARG;
   cudaStream_t st = as_stream(stream);
-  const bool pdl = pdl_enabled() && spmv_kernel() == 0;
+  // PDL chain for the slot-parallel SpMV kernels (0, 4)
+  const bool shfl = spmv_kernel() == 4 && sys->shfl_src && sys->shfl_jbase;
+  auto spmv_k = shfl ? k_spmv_shfl : k_spmv;
+  const bool pdl = pdl_enabled() && (spmv_kernel() == 0 || shfl);
   const unsigned int fg = upd_fused_grid(*sys);
   if (fg > 0) {
     for (int it = 0; it < n_iter; ++it) {
       if (pdl)
-        launch_pdl(k_spmv, spmv_grid(), kSpmvThreads, st, *sys, (const double *)pv, ap, 1);
+        launch_pdl(spmv_k, spmv_grid(), kSpmvThreads, st, *sys, (const double *)pv, ap, 1);
       else
         launch_spmv(*sys, pv, ap, 1, st);
       launch_update_fused(fg, st, pdl, *sys, x, r, (const double *)ap, pv);
@@ -1690,7 +1801,7 @@ int bdem_pcg_iterate(const bdem_system_t *sys, double *x, double *r, double *zv,
   }
   for (int it = 0; it < n_iter; ++it) {
     if (pdl) {
-      launch_pdl(k_spmv, spmv_grid(), kSpmvThreads, st, *sys, (const double *)pv, ap, 1);
+      launch_pdl(spmv_k, spmv_grid(), kSpmvThreads, st, *sys, (const double *)pv, ap, 1);
       launch_pdl(k_pcg_update, kRedBlocks, kThreads, st, *sys, x, r, zv, (const double *)pv,
                  (const double *)ap);
       launch_pdl(k_pcg_pupdate, kRedBlocks, kThreads, st, *sys, pv, (const double *)zv);

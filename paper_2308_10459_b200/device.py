@@ -96,6 +96,8 @@ def row_order(el, mode: str | None = None) -> np.ndarray:
     cell = 2.0 * float(np.median(np.asarray(el.radius)))
     if mode == "strip":
         return strip_order(el.p, cell)
+    if mode.startswith("strip") and mode[5:].isdigit():    # e.g. strip8: 8-wide strips
+        return strip_order(el.p, cell, width=int(mode[5:]))
     return z_order(el.p, cell)
 
 
@@ -180,6 +182,49 @@ class SellLayout:
         jpos[jidx] = self.pos_of_bond[bnd]
         jslot[jidx] = slot[bi[bnd]]
         return jloc, jb_base.astype(np.int32), jpos, jslot, kc, float(inside.mean()) if inside.size else 0.0
+
+    def shfl_tables(self, bi, bj, slot):
+        """Tables of the warp-shuffle SpMV (bdem_spmv_set_kernel(4)).
+
+        A bond whose rows i, j (both free) lie in the same slice is handed to
+        row j at its i-role slot k through a warp shuffle from lane(i) to
+        lane(j); a receiving lane takes at most one bond per slot (the lowest
+        sending lane), the others stay in j-role lists of the usual SELL shape.
+        Returns (src int8 per position: sending lane for the receiving lane
+        pos & 31, -1 none), the reduced j-role lists (base, pos, slot) and the
+        handed-over fraction of the bonds."""
+        nb = bi.shape[0]
+        n = self.elem_row.shape[0]
+        ns = self.n_slices
+        src = np.full(max(self.n_pos, 1), -1, dtype=np.int8)
+        if nb == 0:
+            base, _, _ = self._slices(np.zeros(0, dtype=np.int64), n, ns)
+            return src, base.astype(np.int32), np.full(1, -1, np.int32), \
+                np.full(1, -1, np.int32), 0.0
+        ri, rj = self.elem_row[bi], self.elem_row[bj]
+        pos = self.pos_of_bond
+        k = (pos - self.slice_base[ri // 32]) // 32
+        cand = ((ri // 32) == (rj // 32)) & (slot[bi] >= 0) & (slot[bj] >= 0)
+        # receiving slot key (slice, k, lane_j); keep the lowest sending lane
+        key = (ri // 32) * (self.kmax + 1) * 32 + k * 32 + (rj % 32)
+        c = np.nonzero(cand)[0]
+        order = c[np.lexsort((ri[c] % 32, key[c]))]
+        first = np.ones(order.shape[0], dtype=bool)
+        first[1:] = key[order][1:] != key[order][:-1]
+        handed = np.zeros(nb, dtype=bool)
+        handed[order[first]] = True
+        h = np.nonzero(handed)[0]
+        recv_pos = self.slice_base[ri[h] // 32] + 32 * k[h] + (rj[h] % 32)
+        src[recv_pos] = (ri[h] % 32).astype(np.int8)
+        rest = np.nonzero(~handed)[0]
+        jb_base, rank_b, _ = self._slices(rj[rest], n, ns)
+        nj = int(jb_base[-1])
+        jidx = jb_base[rj[rest] // 32] + 32 * rank_b + (rj[rest] % 32)
+        jpos = np.full(max(nj, 1), -1, dtype=np.int32)
+        jslot = np.full(max(nj, 1), -1, dtype=np.int32)
+        jpos[jidx] = pos[rest]
+        jslot[jidx] = slot[bi[rest]]
+        return src, jb_base.astype(np.int32), jpos, jslot, float(handed.mean())
 
     def wave_tables(self, bi, bj, slot, ring_slices: int):
         """Tables of the dataflow SpMV: per j-role list entry the ring slot its
@@ -341,6 +386,10 @@ class DeviceSystem:
         self.sym_jloc = _t(np.append(jloc, -1), I32, dev)
         self.sym_jbase, self.sym_jpos = _t(jbase, I32, dev), _t(jpos_b, I32, dev)
         self.sym_jslot, self.sym_kc = _t(jslot_b, I32, dev), kc
+        src, sjb, sjp, sjs, self.shfl_handed = sell.shfl_tables(bi64, bj64, slot)
+        self.shfl_src = _t(src, torch.int8, dev)
+        self.shfl_jbase, self.shfl_jpos = _t(sjb, I32, dev), _t(np.append(sjp, -1), I32, dev)
+        self.shfl_jslot = _t(np.append(sjs, -1), I32, dev)
         ring = 4096
         jring, lag = sell.wave_tables(bi64, bj64, slot, ring)
         self.wave_jring, self.wave_lag, self.wave_ring_slices = _t(jring, I32, dev), lag, ring
@@ -399,6 +448,8 @@ class DeviceSystem:
         s.wave_jring, s.wave_lag = _ptr(self.wave_jring), self.wave_lag
         s.wave_ring_slices, s.wave_ring = self.wave_ring_slices, _ptr(self.wave_ring)
         s.wave_ypart, s.wave_flags = _ptr(self.wave_ypart), _ptr(self.wave_flags)
+        s.shfl_src, s.shfl_jbase = _ptr(self.shfl_src), _ptr(self.shfl_jbase)
+        s.shfl_jpos, s.shfl_jslot = _ptr(self.shfl_jpos), _ptr(self.shfl_jslot)
         s.stage, s.diag, s.minv = _ptr(self.stage), _ptr(self.diag), _ptr(self.minv)
         s.scoef = _ptr(self.scoef)
         s.red, s.scalars, s.pcg = _ptr(self.red), _ptr(self.scalars), _ptr(self.pcg_state)

@@ -624,14 +624,14 @@ def _assembled(spec, k_element=None):
     return dev
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4])
 @pytest.mark.parametrize("case", ["plate_z", "cube_random_q", "dense_overflow"])
 def test_tiled_spmv_matches_default(cuda_ok, monkeypatch, case, variant):
     """Same terms per row as k_spmv; with 8 warps per slice (k_spmv: 4) the
     slot partials associate differently, so the two agree to round-off."""
     from paper_2308_10459_b200 import configs as C
     if case == "plate_z":
-        monkeypatch.setenv("BDEM_ROW_ORDER", {1: "z", 2: "strip", 3: "id"}[variant])
+        monkeypatch.setenv("BDEM_ROW_ORDER", {1: "z", 2: "strip", 3: "id", 4: "strip"}[variant])
         spec = C.plate(nx=100, ny=60, epsilon=1e-6)
     elif case == "cube_random_q":
         spec = C.cube(n_side=9, seed=4, random_q=True)
@@ -652,12 +652,14 @@ def test_tiled_spmv_matches_default(cuda_ok, monkeypatch, case, variant):
         assert 0.0 < dev.sym_inside <= 1.0
     if variant == 3:
         assert 0 <= dev.wave_lag and 4 * (dev.wave_lag + 1) <= dev.wave_ring_slices
+    if variant == 4 and case == "plate_z":
+        assert dev.shfl_handed > 0.5            # most bonds handed over in-slice
     y0, y1 = _spmv_both(dev, 11, variant)
     assert np.all(np.isfinite(y0))
     np.testing.assert_allclose(y1, y0, rtol=1e-12, atol=1e-13 * np.abs(y0).max())
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4])
 def test_tiled_spmv_newton_solve_vs_golden(cuda_ok, variant):
     """The reference Newton solve (newton_solve.npz) through the SpMV variants."""
     import paper_2308_10459_b200._lib as L
