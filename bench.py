@@ -14,7 +14,13 @@ ranks) / max-over-ranks device time.  ``e2e`` repeats the measurement through
 the same public call with host buffers (``Scene(host_sync=True)``: host->device
 upload of the element and bond state before, device->host download after,
 every step).  Per-kernel durations (fused bond assembly, every SpMV) are
-taken live with CUDA events on the launching stream inside the timed region.
+taken with CUDA events on the launching stream around every launch of a
+replay of exactly the timed steps (the timed region itself runs the
+production path uninstrumented).  ``rot_zero_shortcut`` replays the timed
+steps once more with ``bdem_pcg_set_rot_skip(1)``: on this config the rotation
+half of every Newton system is exactly zero, the PCG kernels skip it, and the
+final state must equal the timed run's bit for bit; it is reported beside the
+full 6-DOF headline, not as it (SURVEY §9 / DESIGN §9).
 
 ``--impl reference`` times the reference's algorithm on the host cores: the
 CPU oracle (``oracle/cpu_oracle.py``, a restatement of the reference pinned to
@@ -55,6 +61,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 2M-block kernel leg")
+    ap.add_argument("--no-rot-leg", action="store_true",
+                    help="skip the rotation-free (bdem_pcg_set_rot_skip) leg")
     ap.add_argument("--c5-side", type=int, default=126)
     ap.add_argument("--crop", type=int, nargs=2, default=(100, 60),
                     help="plate crop for the CPU sample (nx ny)")
@@ -382,6 +390,7 @@ def run_ours(args):
         barrier()
     launches = lib.bdem_launch_count() - launches0
     ms = t0.elapsed_time(t1)
+    final = snapshot(scene)     # the rotation-free leg must reproduce it bit for bit
 
     # kernel timing: the timed region runs the production path uninstrumented;
     # the same steps are replayed from the snapshot with CUDA events around
@@ -415,6 +424,43 @@ def run_ours(args):
     e2e_ms = e0.elapsed_time(e1)
     h2d = dev.n * (3 + 4 + 3 + 4 + 3 + 4) * 8 + dev.nb * (5 * 8 + 1)
     d2h = h2d
+
+    # rotation-free leg (SURVEY 8(f)'s exact shortcut, reported separately):
+    # the same timed steps from the same snapshot with bdem_pcg_set_rot_skip(1)
+    # -- on this config the rotation half of every Newton system is exactly
+    # zero (identity orientations, centre-based contact), so the PCG kernels
+    # skip it; the headline `value` above runs the full 6-DOF path
+    rot = None
+    if not args.no_rot_leg:
+        prev = lib.bdem_pcg_set_rot_skip(1)
+        restore(scene, snap)
+        scene.host_sync = False
+        dev.upload_elements(scene.elements, scene.p_prev, scene.q_prev)
+        dev.upload_bond_state(scene.bonds)
+        rot_newton = rot_pcg = 0
+        barrier()
+        r0 = torch.cuda.Event(enable_timing=True)
+        r1 = torch.cuda.Event(enable_timing=True)
+        r0.record()
+        for _ in range(args.steps):
+            rep = stable_step(scene, cfg)
+            rot_newton += rep.solve.iterations
+            rot_pcg += rep.solve.pcg_total
+        r1.record()
+        barrier()
+        rot_ms = r0.elapsed_time(r1)
+        skipped = float(dev.pcg_state[L.PCG["ROTZERO"]].item()) == 1.0
+        lib.bdem_pcg_set_rot_skip(prev)
+        scene.sync_to_host()
+        same = all(np.array_equal(getattr(scene.elements, k), getattr(final["el"], k))
+                   for k in ("p", "q", "v", "qdot"))
+        rot = {"value": rot_newton / (rot_ms * 1e-3), "unit": UNIT,
+               "ms_per_step": rot_ms / args.steps, "newton_iterations": rot_newton,
+               "pcg_per_newton": rot_pcg / max(rot_newton, 1),
+               "rotation_half_skipped": skipped, "bit_identical_final_state": bool(same),
+               "note": "bdem_pcg_set_rot_skip(1): the rotation half of every Newton "
+                       "system is exactly zero on this config, so the PCG kernels skip it "
+                       "(exact; reported separately from the full 6-DOF headline)"}
 
     (ms_max, e2e_ms_max), (newton_all, e2e_newton_all) = reduce_across_ranks(
         [ms, e2e_ms], [stats["newton"], e2e_newton], world, "cuda")
@@ -461,6 +507,8 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
     }
+    if rot is not None:
+        line["rot_zero_shortcut"] = rot
     if not args.no_c5:
         line["c5_block"] = c5_leg(args.c5_side, peak)
     if not args.no_cpu_baseline and world == 1:

@@ -151,6 +151,7 @@ enum {
   BDEM_PCG_K = 11,      /* iterations of the current run (as double) */
   BDEM_PCG_MAXIT = 12,
   BDEM_PCG_STATE = 13,  /* 0 running, 1 converged, 2 breakdown, 3 max-iterations */
+  BDEM_PCG_ROTZERO = 14, /* 1: rotation half of the system identically zero (skipped) */
   BDEM_PCG_COUNT = 16
 };
 
@@ -369,6 +370,15 @@ int bdem_spmv_set_kernel(int kernel);
  * n_free <= BDEM_RED_BLOCKS * 512).  Returns the previous setting; any other
  * value only queries.  BDEM_FUSED_UPD=1 selects it at load time. */
 int bdem_pcg_set_fused(int on);
+/* Rotation-free PCG: when on and the rotation half of the right-hand side
+ * is identically zero at bdem_pcg_init (e.g. identity orientations with no
+ * rotational load, as on the BASELINE plate), the rotation halves of every
+ * PCG vector stay exactly zero (the reduced matrix has no position/rotation
+ * coupling), and the SpMV / update kernels skip them: 5 of the 14 SpMV
+ * coefficients and 3 of 6 vector components per row.  Bit-identical iterates
+ * (up to the sign of zeros).  Default off; BDEM_ROT_SKIP=1 selects it at load
+ * time.  Returns the previous setting; any other value only queries. */
+int bdem_pcg_set_rot_skip(int on);
 /* Slices per tile of the tiled SpMV and the int32 stride of sys->tile_hdr. */
 int bdem_spmv_tile_slices(void);
 int bdem_spmv_tile_hdr_ints(void);

@@ -26,7 +26,7 @@ PS = dict(E=0, GI=1, A=4, COUNT=10)
 SC = dict(F=0, GNORM2=1, CNORM2=2, MAXDEV=3, SLOPE=4, FT=5, NSING=6, EBOND=7, ECOL=8, EGRAV=9,
           EKIN=10, EPAIR=11, COUNT=32)
 PCG = dict(RZ=0, PAP=1, ALPHA=2, BETA=3, RR=4, BNORM=5, REL=6, TOL=7, BOOST=8, APNORM2=9,
-           PNORM2=10, K=11, MAXIT=12, STATE=13, COUNT=16)
+           PNORM2=10, K=11, MAXIT=12, STATE=13, ROTZERO=14, COUNT=16)
 PCG_RUNNING, PCG_CONVERGED, PCG_BREAKDOWN, PCG_MAXIT = 0, 1, 2, 3
 ABI_VERSION = 3
 RED_BLOCKS = 1184
@@ -104,6 +104,7 @@ SIGNATURES = {
     "bdem_select_flagged": (_int, [_p, _i64, _p, _p, C.POINTER(C.c_int64), _p]),
     "bdem_spmv_set_kernel": (_int, [_int]),
     "bdem_pcg_set_fused": (_int, [_int]),
+    "bdem_pcg_set_rot_skip": (_int, [_int]),
     "bdem_spmv_tile_slices": (_int, []),
     "bdem_spmv_sym_slices": (_int, []),
     "bdem_spmv_sym_kcap": (_int, []),

@@ -32,7 +32,8 @@ __device__ __forceinline__ void griddep_wait() {
 }
 enum { CNT_SPMV = 2, CNT_UPDATE = 3, CNT_INIT = 4 };
 // partial-sum columns of sys->red owned by PCG (disjoint from BDEM_SC_*)
-enum { RC_PAP = 20, RC_AP2 = 21, RC_PP2 = 22, RC_RR = 23, RC_RZ = 24, RC_IRR = 25, RC_IRZ = 26 };
+enum { RC_PAP = 20, RC_AP2 = 21, RC_PP2 = 22, RC_RR = 23, RC_RZ = 24, RC_IRR = 25, RC_IRZ = 26,
+       RC_IRN = 27 };
 
 // reduced vectors are 6 planes of stride vstride: component c of slot s at
 // x[c * vstride + s], so a warp touching 32 consecutive slots reads 256 contiguous
@@ -67,7 +68,7 @@ __device__ __forceinline__ void precond_row(const bdem_system_t &S, int64_t s, c
 
 // component c (= w, w + W, ...) of y for the 32 rows of slice sl:
 // y = D x + sum of the staged slot partials (fixed order) - pair couplings
-template <int W>
+template <int W, bool kRot = true>
 __device__ __forceinline__ void spmv_tail(const bdem_system_t &S, const double *x, double *y,
                                           int sl, int w, int lane, const double (*part)[6][32],
                                           double boost, double &acc_xy, double &acc_yy,
@@ -76,7 +77,9 @@ __device__ __forceinline__ void spmv_tail(const bdem_system_t &S, const double *
   const int64_t e = __ldg(S.row_elem + (int64_t)sl * 32 + lane);
   const int s = e >= 0 ? __ldg(S.slot + e) : -1;
   if (s < 0) return;
-  for (int c = w; c < 6; c += W) {
+  // kRot false: the rotation half of x is identically zero (see
+  // pcg_rot_active), so y's rotation half is zero and not formed
+  for (int c = w; c < (kRot ? 6 : 3); c += W) {
     const int base = c < 3 ? 0 : 3, rr = c - base;
     const double *dg = S.diag + (c < 3 ? 0 : 6 * nf);
     double xs[3], dgr[3];
@@ -193,9 +196,24 @@ __device__ __forceinline__ SlotRef slot_ref(const bdem_system_t &S, int64_t i0, 
   return r;
 }
 
+template <bool kRot = true>
 __device__ __forceinline__ void slot_apply(const bdem_system_t &S, const double *x,
                                            const SlotRef &r, double acc[6]) {
   if (r.o < 0) return;
+  if (!kRot) {
+    // position half only: 5 of the 14 coefficients, 3 of the 6 x components
+    const double *base = S.scoef + cf_idx(r.b, 0);
+    double xo[3], n[3];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) xo[t] = __ldg(x + t * S.vstride + r.o);
+#pragma unroll
+    for (int t = 0; t < 3; ++t) n[t] = __ldg(base + 32 * (BDEM_CF_N + t));
+    const double al = __ldg(base + 32 * BDEM_CF_ALPHA), be = __ldg(base + 32 * BDEM_CF_BETA);
+    const double nx = al * ((n[0] * xo[0] + n[1] * xo[1]) + n[2] * xo[2]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) acc[c] -= nx * n[c] + be * xo[c];
+    return;
+  }
   const int64_t nb = S.n_bond;
   const double *st = S.stage;
   double xo[6], n[3], C[9];
@@ -250,18 +268,12 @@ __device__ __forceinline__ SliceBounds slice_bounds(const bdem_system_t &S, int 
 // mode 0: plain y = A x;  mode 1: PCG step (y = A p + boost p, p.Ap, |Ap|^2,
 // |p|^2 and the breakdown test, linalg.py:69-77).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kSpmvThreads, BDEM_SPMV_MINB) k_spmv(bdem_system_t S, const double *x, double *y,
-                                                       int mode) {
-  __shared__ double part[kSpmvWarps][6][32];
-  __shared__ double sh[kSpmvThreads / 32];
-  griddep_wait();
-  double *pcg = S.pcg;
-  if (mode == 1 && pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
-  const double boost = mode == 1 ? pcg[BDEM_PCG_BOOST] : 0.0;
+template <bool kRot>
+__device__ __forceinline__ void spmv_slices(const bdem_system_t &S, const double *x, double *y,
+                                            double boost, double (*part)[6][32],
+                                            double &acc_xy, double &acc_yy, double &acc_xx) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t nf = S.vstride;
   const int ns = (int)((S.n_elem + 31) >> 5);
-  double acc_xy = 0.0, acc_yy = 0.0, acc_xx = 0.0;
 #if BDEM_SPMV_BLOCKED
   // contiguous slice ranges per CTA: neighbouring rows (and their x blocks)
   // are processed by the same SM, so gathers reuse L1/L2 lines
@@ -283,15 +295,42 @@ __global__ void __launch_bounds__(kSpmvThreads, BDEM_SPMV_MINB) k_spmv(bdem_syst
 #pragma unroll 1
     for (int k = w; k < kt; k += kSpmvWarps) {
       const SlotRef nxt = slot_ref(S, cb.i0, cb.ki, cb.j0, cb.kj, lane, k + kSpmvWarps);
-      slot_apply(S, x, cur, acc);
+      slot_apply<kRot>(S, x, cur, acc);
       cur = nxt;
     }
 #pragma unroll
     for (int q = 0; q < 6; ++q) part[w][q][lane] = acc[q];
     __syncthreads();
-    spmv_tail<kSpmvWarps>(S, x, y, sl, w, lane, part, boost, acc_xy, acc_yy, acc_xx);
+    spmv_tail<kSpmvWarps, kRot>(S, x, y, sl, w, lane, part, boost, acc_xy, acc_yy, acc_xx);
     __syncthreads();
   }
+}
+
+// Rotation-free PCG (bdem_pcg_set_rot_skip): when the rotation half of the
+// right-hand side is identically zero (pcg_init found no non-zero entry,
+// e.g. identity orientations with no rotational load: every shear and
+// bend/twist gradient vanishes exactly), the rotation halves of r, z, p, x
+// and Ap stay exactly zero through the whole solve (the reduced matrix has
+// no position/rotation coupling), so every PCG kernel skips them.  Each
+// skipped term is an exact zero, so iterates and scalars are bit-identical
+// to the full solve (up to the sign of zeros).
+__device__ __forceinline__ bool pcg_rot_active(const double *pcg) {
+  return pcg[BDEM_PCG_ROTZERO] == 0.0;
+}
+
+__global__ void __launch_bounds__(kSpmvThreads, BDEM_SPMV_MINB) k_spmv(bdem_system_t S, const double *x, double *y,
+                                                       int mode) {
+  __shared__ double part[kSpmvWarps][6][32];
+  __shared__ double sh[kSpmvThreads / 32];
+  griddep_wait();
+  double *pcg = S.pcg;
+  if (mode == 1 && pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
+  const double boost = mode == 1 ? pcg[BDEM_PCG_BOOST] : 0.0;
+  double acc_xy = 0.0, acc_yy = 0.0, acc_xx = 0.0;
+  if (mode == 0 || pcg_rot_active(pcg))
+    spmv_slices<true>(S, x, y, boost, part, acc_xy, acc_yy, acc_xx);
+  else
+    spmv_slices<false>(S, x, y, boost, part, acc_xy, acc_yy, acc_xx);
   if (mode == 0) return;
   spmv_pcg_epilogue<kSpmvThreads>(S, boost, acc_xy, acc_yy, acc_xx, sh);
 }
@@ -412,6 +451,7 @@ __global__ void __launch_bounds__(kThreads, BDEM_UPD_MINB) k_pcg_update(bdem_sys
   double *pcg = S.pcg;
   if (pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
   const double alpha = pcg[BDEM_PCG_ALPHA];
+  const int halves = pcg_rot_active(pcg) ? 2 : 1;
   double acc_rr = 0.0, acc_rz = 0.0;
   // two consecutive slots per thread with 16-byte loads (planes are 256-B
   // aligned, stride vstride); padding slots carry zeros and stay zero
@@ -428,6 +468,7 @@ __global__ void __launch_bounds__(kThreads, BDEM_UPD_MINB) k_pcg_update(bdem_sys
     // position half (components 0..2, P^-1) then rotation half (3..5, R^-1)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
+      if (h >= halves) break;
       double ra[3], rb[3], ma[6], mb[6], za[3], zb[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -489,7 +530,8 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(bdem_system_t S, doubl
   const double *pcg = S.pcg;
   if (pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
   const double beta = pcg[BDEM_PCG_BETA];
-  const int64_t n6 = 3 * S.vstride;  // double2 units over 6 planes
+  // double2 units over 6 planes (3 with the rotation half inactive)
+  const int64_t n6 = pcg_rot_active(pcg) ? 3 * S.vstride : (3 * S.vstride) / 2;
   double2 *p2 = reinterpret_cast<double2 *>(p);
   const double2 *z2 = reinterpret_cast<const double2 *>(zv);
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n6;
@@ -554,6 +596,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_pcg_update_fused(bdem_system_t 
   const double rz_old = pcg[BDEM_PCG_RZ], k_old = pcg[BDEM_PCG_K];
   const double bnorm = pcg[BDEM_PCG_BNORM], tol = pcg[BDEM_PCG_TOL];
   const double maxit = pcg[BDEM_PCG_MAXIT];
+  const int halves = pcg_rot_active(pcg) ? 2 : 1;
   const int64_t nf = S.vstride;
   const int64_t h2 = nf >> 1;
   const double2 *ap2 = reinterpret_cast<const double2 *>(ap);
@@ -569,6 +612,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_pcg_update_fused(bdem_system_t 
     if (t < h2) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
+        if (h >= halves) break;
         double ra[3], rb[3], ma[6], mb[6], za[3], zb[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -645,6 +689,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_pcg_update_fused(bdem_system_t 
     if (t >= h2) continue;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
+      if (h >= halves) break;
       double2 pv[3], xv[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -668,14 +713,16 @@ __global__ void __launch_bounds__(kThreads, 4) k_pcg_update_fused(bdem_system_t 
 __global__ void __launch_bounds__(kThreads) k_pcg_init(bdem_system_t S, const double *b,
                                                        double sign, double *x, double *r,
                                                        double *zv, double *p, double tol,
-                                                       double maxit, double boost) {
+                                                       double maxit, double boost,
+                                                       int rot_skip) {
   __shared__ double sh[kThreads / 32];
-  double acc_rr = 0.0, acc_rz = 0.0;
+  double acc_rr = 0.0, acc_rz = 0.0, acc_nz = 0.0;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < S.n_free;
        s += (int64_t)gridDim.x * blockDim.x) {
     double bs[6], zs[6];
     const double zero[6] = {0, 0, 0, 0, 0, 0};
     load6(b, s, S.vstride, bs);
+    if (bs[3] != 0.0 || bs[4] != 0.0 || bs[5] != 0.0) acc_nz = 1.0;
 #pragma unroll
     for (int c = 0; c < 6; ++c) {
       bs[c] = sign * bs[c];
@@ -693,11 +740,17 @@ __global__ void __launch_bounds__(kThreads) k_pcg_init(bdem_system_t S, const do
   if (threadIdx.x == 0) *red_slot(S.red, RC_IRR, blockIdx.x) = v;
   v = block_sum<kThreads>(acc_rz, sh);
   if (threadIdx.x == 0) *red_slot(S.red, RC_IRZ, blockIdx.x) = v;
+  v = block_sum<kThreads>(acc_nz, sh);
+  if (threadIdx.x == 0) *red_slot(S.red, RC_IRN, blockIdx.x) = v;
   if (!last_block(S.counter + CNT_INIT)) return;
   const double rr = sum_partials<kThreads>(S.red, RC_IRR, gridDim.x, sh);
   const double rz = sum_partials<kThreads>(S.red, RC_IRZ, gridDim.x, sh);
+  const double nz = sum_partials<kThreads>(S.red, RC_IRN, gridDim.x, sh);
   if (threadIdx.x == 0) {
     double *pcg = S.pcg;
+    // rotation half active unless the skip is enabled and b's rotation
+    // half is identically zero (see pcg_rot_active)
+    pcg[BDEM_PCG_ROTZERO] = (rot_skip && nz == 0.0) ? 1.0 : 0.0;
     pcg[BDEM_PCG_RZ] = rz;
     pcg[BDEM_PCG_BNORM] = sqrt(rr);
     pcg[BDEM_PCG_RR] = rr;
@@ -1662,6 +1715,14 @@ static unsigned int spmv_grid() {
 // there are not enough co-resident blocks for the virtual layout, or more
 // slot pairs than virtual threads.
 static constexpr size_t kFusedSmem = sizeof(double2) * kFusedMaxV * 6 * kThreads;
+static int g_rot_skip = -1;
+static int rot_skip_on() {
+  if (g_rot_skip < 0) {
+    const char *env = getenv("BDEM_ROT_SKIP");
+    g_rot_skip = env ? (atoi(env) != 0) : 0;
+  }
+  return g_rot_skip;
+}
 static int g_fused_on = -1;
 static int fused_on() {
   if (g_fused_on < 0) {
@@ -1740,6 +1801,11 @@ int bdem_spmv_set_kernel(int kernel) {
   if (kernel >= 0 && kernel <= 4) g_spmv_kernel = kernel;
   return prev;
 }
+int bdem_pcg_set_rot_skip(int on) {
+  const int prev = rot_skip_on();
+  if (on == 0 || on == 1) g_rot_skip = on;
+  return prev;
+}
 int bdem_pcg_set_fused(int on) {
   const int prev = fused_on();
   if (on == 0 || on == 1) g_fused_on = on;
@@ -1776,7 +1842,8 @@ int bdem_pcg_init(const bdem_system_t *sys, const double *b, double sign, double
                   void *stream) {
   if (!sys) return BDEM_ERR_ARG;
   k_pcg_init<<<kRedBlocks, kThreads, 0, as_stream(stream)>>>(*sys, b, sign, x, r, zv, pv, tol,
-                                                              (double)max_iter, boost);
+                                                              (double)max_iter, boost,
+                                                              rot_skip_on());
   return launch_status();
 }
 

@@ -696,3 +696,39 @@ def test_fused_pcg_update_bit_identical(cuda_ok):
     assert s0[13] in (1, 3) and s0[11] > 50   # stopped (converged / max-it) after many iterations
     assert np.array_equal(s0, s1)
     assert np.array_equal(y0, y1) and np.array_equal(p0, p1)
+
+
+@pytest.mark.parametrize("case", ["plate", "rope"])
+def test_rot_skip_bit_identical(cuda_ok, case):
+    """Rotation-free PCG (bdem_pcg_set_rot_skip): on the plate (identity
+    orientations, centre-based contact: the rotation half of every Newton
+    right-hand side is exactly zero) the skipped solve gives bit-identical
+    trajectories; on the twisted rope the rotation half is non-zero, the
+    flag stays off and the results are the same path."""
+    from paper_2308_10459_b200 import SolverConfig, stable_step
+    from paper_2308_10459_b200 import _lib as L
+    from paper_2308_10459_b200 import configs as C
+    from paper_2308_10459_b200.scene import Scene
+    lib = L.load()
+    eps = 1e-6 if case == "plate" else 1e-5
+    out = []
+    for skip in (0, 1):
+        prev = lib.bdem_pcg_set_rot_skip(skip)
+        try:
+            # a fresh spec per run: the scene steps the spec's arrays in place
+            spec = C.plate(nx=60, ny=36, epsilon=1e-6) if case == "plate" else C.rope(n=200)
+            scene = Scene.from_spec(spec)
+            recs, flags = [], []
+            for _ in range(4):
+                rep = stable_step(scene, SolverConfig(epsilon=eps, max_iterations=200))
+                recs.append((rep.committed, rep.solve.iterations, rep.solve.pcg_total))
+                flags.append(float(scene.device.pcg_state[L.PCG["ROTZERO"]].item()))
+        finally:
+            lib.bdem_pcg_set_rot_skip(prev)
+        out.append((recs, flags, scene.elements.p.copy(), scene.elements.q.copy(),
+                    scene.elements.v.copy()))
+    (r0, f0, p0, q0, v0), (r1, f1, p1, q1, v1) = out
+    assert r0 == r1 and sum(r[2] for r in r0) > 0
+    assert np.array_equal(p0, p1) and np.array_equal(q0, q1) and np.array_equal(v0, v1)
+    assert all(f == 0.0 for f in f0)
+    assert all(f == (1.0 if case == "plate" else 0.0) for f in f1)
