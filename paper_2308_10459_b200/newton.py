@@ -177,6 +177,7 @@ class GPUProblem:
             chunk = chunk0
             tm = self.timer
             k_before = 0
+            hist = []
             while True:
                 if tm is None:
                     d.call("bdem_pcg_iterate", s, *ptrs, d.ap.data_ptr(), int(chunk), st)
@@ -197,7 +198,7 @@ class GPUProblem:
                     tm.drop_last("spmv", chunk - min(worked, chunk))
                     k_before = k_now
                 if state == L.PCG_RUNNING:
-                    chunk = min(chunk * 2, chunk_max)
+                    chunk = self._next_chunk(chunk, chunk_max, h, hist)
                     continue
                 break
             k = int(h[L.PCG["K"]])
@@ -209,6 +210,25 @@ class GPUProblem:
                     return PCGResult(k, False, rel, restarts)
                 continue
             return PCGResult(k, state == L.PCG_CONVERGED, rel, restarts)
+
+    @staticmethod
+    def _next_chunk(chunk, chunk_max, h, hist):
+        """Iterations to enqueue before the next read-back.  Kernels past
+        convergence exit at once, so a chunk only trades early-exit launches
+        against read-back bubbles; once two read-backs show the residual's
+        geometric rate, the chunk is sized to the iterations it predicts
+        (plus one), else it doubles up to ``chunk_max``."""
+        k, rel, tol = float(h[L.PCG["K"]]), float(h[L.PCG["REL"]]), float(h[L.PCG["TOL"]])
+        hist.append((k, rel))
+        if len(hist) >= 2:
+            (k0, r0), (k1, r1) = hist[-2], hist[-1]
+            if k1 > k0 and 0.0 < r1 < r0 and tol > 0.0:
+                rate = (r1 / r0) ** (1.0 / (k1 - k0))
+                if rate < 1.0:
+                    need = math.log(tol / r1) / math.log(rate)
+                    if math.isfinite(need):
+                        return int(min(max(math.ceil(need) + 1, 4), 4 * chunk_max))
+        return min(chunk * 2, chunk_max)
 
     def dot(self, a, b, n):
         d = self.dev
