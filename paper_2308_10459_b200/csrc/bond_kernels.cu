@@ -369,14 +369,14 @@ __global__ void __launch_bounds__(kThreads) k_bond_update(bdem_system_t S, const
   const double mb = hypot(kt[1], kt[2]);
   const double r0 = g[BDEM_BG_RADIUS * nb + b];
   const double section = bs[BDEM_BS_DAMAGE * nb + b] * g[BDEM_BG_SECTION * nb + b];
-  const double sigma = fn / section + (mb * r0) / g[BDEM_BG_SECOND * nb + b];
-  const double tau = (mt * r0) / g[BDEM_BG_POLAR * nb + b];
+  const double sigma = div_nz(fn, section) + div_nz(mb * r0, g[BDEM_BG_SECOND * nb + b]);
+  const double tau = div_nz(mt * r0, g[BDEM_BG_POLAR * nb + b]);
   bs[BDEM_BS_SIGMA * nb + b] = sigma;
   bs[BDEM_BS_TAU * nb + b] = tau;
   bool broke = false;
   int8_t new_status = status;
   if (plastic_on) {
-    const double strain = (len - l0) / l0;
+    const double strain = div_nz(len - l0, l0);
     const double sy = youngs * eps_y;
     const double vm = sqrt(sigma * sigma + 3.0 * (tau * tau));
     if (vm > sy) {

@@ -19,10 +19,10 @@ __device__ inline void collider_eval(const bdem_collider_t &C, const double p[3]
     g = r - C.a[3];
     double n[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) { n[c] = d[c] / rs; dg[c] = n[c]; }
+    for (int c = 0; c < 3; ++c) { n[c] = div_nz(d[c], rs); dg[c] = n[c]; }
     const int pr[6] = {0, 0, 0, 1, 1, 2}, pc[6] = {0, 1, 2, 1, 2, 2};
 #pragma unroll
-    for (int t = 0; t < 6; ++t) H[t] = ((pr[t] == pc[t] ? 1.0 : 0.0) - n[pr[t]] * n[pc[t]]) / rs;
+    for (int t = 0; t < 6; ++t) H[t] = div_nz((pr[t] == pc[t] ? 1.0 : 0.0) - n[pr[t]] * n[pc[t]], rs);
   } else {  // box
     double loc[3], d[3], pos[3], sign[3];
 #pragma unroll
@@ -39,12 +39,12 @@ __device__ inline void collider_eval(const bdem_collider_t &C, const double p[3]
       const double ons = fmax(on, 1e-300);
       double n[3];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) { n[c] = sign[c] * pos[c] / ons; dg[c] = n[c]; }
+      for (int c = 0; c < 3; ++c) { n[c] = div_nz(sign[c] * pos[c], ons); dg[c] = n[c]; }
       const int pr[6] = {0, 0, 0, 1, 1, 2}, pc[6] = {0, 1, 2, 1, 2, 2};
 #pragma unroll
       for (int t = 0; t < 6; ++t) {
         const double act = (pr[t] == pc[t] && pos[pr[t]] > 0.0) ? 1.0 : 0.0;
-        H[t] = (act - n[pr[t]] * n[pc[t]]) / ons;
+        H[t] = div_nz(act - n[pr[t]] * n[pc[t]], ons);
       }
     } else {
       int ax = 0;

@@ -397,9 +397,9 @@ __global__ void k_finish_step(bdem_system_t S, const double *p, const double *q,
   load_p(pc, e, pce);
   load_q(qc, e, qce);
 #pragma unroll
-  for (int c = 0; c < 3; ++c) v[3 * e + c] = (pe[c] - pce[c]) / dt;
+  for (int c = 0; c < 3; ++c) v[3 * e + c] = div_nz(pe[c] - pce[c], dt);
 #pragma unroll
-  for (int c = 0; c < 4; ++c) w[c] = (qe[c] - qce[c]) / dt;
+  for (int c = 0; c < 4; ++c) w[c] = div_nz(qe[c] - qce[c], dt);
   const double qw = ((qe[0] * w[0] + qe[1] * w[1]) + qe[2] * w[2]) + qe[3] * w[3];
 #pragma unroll
   for (int c = 0; c < 4; ++c) out[c] = w[c] - qw * qe[c];

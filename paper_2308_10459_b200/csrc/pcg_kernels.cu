@@ -797,7 +797,7 @@ __global__ void __launch_bounds__(kThreads) k_pair(bdem_system_t S, const double
     } else {
       const double l = fmax(len, 1e-300);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) n[c] = d[c] / l;
+      for (int c = 0; c < 3; ++c) n[c] = div_nz(d[c], l);
     }
     const bool touch = depth > 0.0;
     double *ps = S.pstage;
