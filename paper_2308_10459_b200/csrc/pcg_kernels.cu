@@ -443,6 +443,9 @@ __global__ void __launch_bounds__(kSpmvThreads, BDEM_SHFL_MINB)
 #ifndef BDEM_UPD_MINB
 #define BDEM_UPD_MINB 4
 #endif
+#ifndef BDEM_UPD_STREAM
+#define BDEM_UPD_STREAM 1
+#endif
 __global__ void __launch_bounds__(kThreads, BDEM_UPD_MINB) k_pcg_update(bdem_system_t S, double *x, double *r,
                                                          double *zv, const double *p,
                                                          const double *ap) {
@@ -473,15 +476,30 @@ __global__ void __launch_bounds__(kThreads, BDEM_UPD_MINB) k_pcg_update(bdem_sys
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const int64_t k = (3 * h + c) * h2 + t;
+#if BDEM_UPD_STREAM
+        // x, r, Ap and M^-1 are next touched an SpMV later (0.5 GB of
+        // coefficients streamed in between): evict-first loads / stores keep
+        // them from displacing the SpMV's L2 working set
+        const double2 xv = __ldcs(x2 + k), rv = __ldcs(r2 + k), pv = p2[k], av = __ldcs(ap2 + k);
+        __stcs(x2 + k, make_double2(xv.x + alpha * pv.x, xv.y + alpha * pv.y));
+        ra[c] = rv.x - alpha * av.x;
+        rb[c] = rv.y - alpha * av.y;
+        __stcs(r2 + k, make_double2(ra[c], rb[c]));
+#else
         const double2 xv = x2[k], rv = r2[k], pv = p2[k], av = ap2[k];
         x2[k] = make_double2(xv.x + alpha * pv.x, xv.y + alpha * pv.y);
         ra[c] = rv.x - alpha * av.x;
         rb[c] = rv.y - alpha * av.y;
         r2[k] = make_double2(ra[c], rb[c]);
+#endif
       }
 #pragma unroll
       for (int tt = 0; tt < 6; ++tt) {
+#if BDEM_UPD_STREAM
+        const double2 m = __ldcs(mi2 + (6 * h + tt) * h2 + t);
+#else
         const double2 m = mi2[(6 * h + tt) * h2 + t];
+#endif
         ma[tt] = m.x;
         mb[tt] = m.y;
       }
@@ -536,7 +554,11 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(bdem_system_t S, doubl
   const double2 *z2 = reinterpret_cast<const double2 *>(zv);
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n6;
        k += (int64_t)gridDim.x * blockDim.x) {
+#if BDEM_UPD_STREAM
+    const double2 zz = __ldcs(z2 + k), pp = p2[k];   // last use of z this iteration
+#else
     const double2 zz = z2[k], pp = p2[k];
+#endif
     p2[k] = make_double2(zz.x + beta * pp.x, zz.y + beta * pp.y);
   }
 }
