@@ -23,6 +23,34 @@ namespace bdem {
 
 enum { PCG_RUNNING = 0, PCG_CONVERGED = 1, PCG_BREAKDOWN = 2, PCG_MAXIT = 3 };
 
+// Diagnostic builds only (-DBDEM_TIMELINE=1, not the shipped library): every
+// PCG kernel stamps %globaltimer at its first CTA's arrival, its first CTA's
+// release from griddepcontrol.wait and its last CTA's exit, per iteration,
+// so the gaps at the kernel boundaries of the PDL chain can be read back
+// (bdem_timeline_read).  Slot = (kernel, pcg K & 1023).
+#ifndef BDEM_TIMELINE
+#define BDEM_TIMELINE 0
+#endif
+#if BDEM_TIMELINE
+__device__ unsigned long long g_tl[3 * 1024 * 3];
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL_ARRIVE(kid, it) \
+  if (threadIdx.x == 0) atomicMin(&g_tl[((kid) * 1024 + ((it) & 1023)) * 3 + 0], tl_now());
+#define TL_RELEASE(kid, it) \
+  if (threadIdx.x == 0) atomicMin(&g_tl[((kid) * 1024 + ((it) & 1023)) * 3 + 1], tl_now());
+#define TL_EXIT(kid, it)  \
+  __syncthreads();        \
+  if (threadIdx.x == 0) atomicMax(&g_tl[((kid) * 1024 + ((it) & 1023)) * 3 + 2], tl_now());
+#else
+#define TL_ARRIVE(kid, it)
+#define TL_RELEASE(kid, it)
+#define TL_EXIT(kid, it)
+#endif
+
 // Programmatic dependent launch: the PCG kernels are launched with
 // programmatic stream serialisation, so a kernel's CTAs are scheduled as the
 // previous kernel's CTAs retire; each waits here until the previous grid has
@@ -344,9 +372,19 @@ __global__ void __launch_bounds__(kSpmvThreads, BDEM_SPMV_MINB) k_spmv(bdem_syst
                                                        int mode) {
   __shared__ double part[kSpmvWarps][6][32];
   __shared__ double sh[kSpmvThreads / 32];
+#if BDEM_TIMELINE
+  const unsigned long long t_arrive = tl_now();
+#endif
   griddep_wait();
   double *pcg = S.pcg;
   if (mode == 1 && pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
+#if BDEM_TIMELINE
+  const int tl_it = (int)pcg[BDEM_PCG_K];
+  if (mode == 1 && threadIdx.x == 0) {
+    atomicMin(&g_tl[(0 * 1024 + (tl_it & 1023)) * 3 + 0], t_arrive);
+    TL_RELEASE(0, tl_it)
+  }
+#endif
   const double boost = mode == 1 ? pcg[BDEM_PCG_BOOST] : 0.0;
   double acc_xy = 0.0, acc_yy = 0.0, acc_xx = 0.0;
   if (mode == 0 || pcg_rot_active(pcg))
@@ -355,6 +393,7 @@ __global__ void __launch_bounds__(kSpmvThreads, BDEM_SPMV_MINB) k_spmv(bdem_syst
     spmv_slices<false>(S, x, y, boost, part, acc_xy, acc_yy, acc_xx);
   if (mode == 0) return;
   spmv_pcg_epilogue<kSpmvThreads>(S, boost, acc_xy, acc_yy, acc_xx, sh);
+  TL_EXIT(0, tl_it)
 }
 
 // ---------------------------------------------------------------------------
@@ -472,9 +511,19 @@ __global__ void __launch_bounds__(kThreads, BDEM_UPD_MINB) k_pcg_update(bdem_sys
                                                          double *zv, const double *p,
                                                          const double *ap) {
   __shared__ double sh[kThreads / 32];
+#if BDEM_TIMELINE
+  const unsigned long long t_arrive = tl_now();
+#endif
   griddep_wait();
   double *pcg = S.pcg;
   if (pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
+#if BDEM_TIMELINE
+  const int tl_it = (int)pcg[BDEM_PCG_K];
+  if (threadIdx.x == 0) {
+    atomicMin(&g_tl[(1 * 1024 + (tl_it & 1023)) * 3 + 0], t_arrive);
+    TL_RELEASE(1, tl_it)
+  }
+#endif
   const double alpha = pcg[BDEM_PCG_ALPHA];
   const int halves = pcg_rot_active(pcg) ? 2 : 1;
   double acc_rr = 0.0, acc_rz = 0.0;
@@ -561,14 +610,25 @@ __global__ void __launch_bounds__(kThreads, BDEM_UPD_MINB) k_pcg_update(bdem_sys
       if (k >= pcg[BDEM_PCG_MAXIT]) pcg[BDEM_PCG_STATE] = PCG_MAXIT;
     }
   }
+  TL_EXIT(1, tl_it)
 }
 
 // p = z + beta p (linalg.py:91)
 __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(bdem_system_t S, double *p,
                                                           const double *zv) {
+#if BDEM_TIMELINE
+  const unsigned long long t_arrive = tl_now();
+#endif
   griddep_wait();
   const double *pcg = S.pcg;
   if (pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
+#if BDEM_TIMELINE
+  const int tl_it = (int)pcg[BDEM_PCG_K];
+  if (threadIdx.x == 0) {
+    atomicMin(&g_tl[(2 * 1024 + (tl_it & 1023)) * 3 + 0], t_arrive);
+    TL_RELEASE(2, tl_it)
+  }
+#endif
   const double beta = pcg[BDEM_PCG_BETA];
   // double2 units over 6 planes (3 with the rotation half inactive)
   const int64_t n6 = pcg_rot_active(pcg) ? 3 * S.vstride : (3 * S.vstride) / 2;
@@ -583,6 +643,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(bdem_system_t S, doubl
 #endif
     p2[k] = make_double2(zz.x + beta * pp.x, zz.y + beta * pp.y);
   }
+  TL_EXIT(2, tl_it)
 }
 
 // ---------------------------------------------------------------------------
@@ -661,14 +722,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_pcg_update_fused(bdem_system_t 
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const int64_t k = (3 * h + c) * h2 + t;
-          const double2 rv = r2[k], av = ap2[k];
+          const double2 rv = __ldcs(r2 + k), av = __ldcs(ap2 + k);
           ra[c] = rv.x - alpha * av.x;
           rb[c] = rv.y - alpha * av.y;
-          r2[k] = make_double2(ra[c], rb[c]);
+          __stcs(r2 + k, make_double2(ra[c], rb[c]));
         }
 #pragma unroll
         for (int tt = 0; tt < 6; ++tt) {
-          const double2 m = mi2[(6 * h + tt) * h2 + t];
+          const double2 m = __ldcs(mi2 + (6 * h + tt) * h2 + t);
           ma[tt] = m.x;
           mb[tt] = m.y;
         }
@@ -738,12 +799,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_pcg_update_fused(bdem_system_t 
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         pv[c] = p2[(3 * h + c) * h2 + t];
-        xv[c] = x2[(3 * h + c) * h2 + t];
+        xv[c] = __ldcs(x2 + (3 * h + c) * h2 + t);
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const int64_t k = (3 * h + c) * h2 + t;
-        x2[k] = make_double2(xv[c].x + alpha * pv[c].x, xv[c].y + alpha * pv[c].y);
+        __stcs(x2 + k, make_double2(xv[c].x + alpha * pv[c].x, xv[c].y + alpha * pv[c].y));
         if (running) {
           const double2 zz = zsh[(v * 6 + 3 * h + c) * kThreads + threadIdx.x];
           p2[k] = make_double2(zz.x + beta * pv[c].x, zz.y + beta * pv[c].y);
@@ -1845,6 +1906,22 @@ int bdem_spmv_set_kernel(int kernel) {
   if (kernel >= 0 && kernel <= 4) g_spmv_kernel = kernel;
   return prev;
 }
+#if BDEM_TIMELINE
+// diagnostic builds: reset / read the PCG kernel timeline (3 x 1024 x 3 u64)
+int bdem_timeline_reset(void) {
+  static unsigned long long init[3 * 1024 * 3];
+  for (int k = 0; k < 3 * 1024; ++k) {
+    init[3 * k] = ~0ull;
+    init[3 * k + 1] = ~0ull;
+    init[3 * k + 2] = 0ull;
+  }
+  return cudaMemcpyToSymbol(g_tl, init, sizeof(init)) == cudaSuccess ? 0 : 1;
+}
+int bdem_timeline_read(unsigned long long *out) {
+  return cudaMemcpyFromSymbol(out, g_tl, sizeof(unsigned long long) * 3 * 1024 * 3) ==
+                 cudaSuccess ? 0 : 1;
+}
+#endif
 int bdem_pcg_set_rot_skip(int on) {
   const int prev = rot_skip_on();
   if (on == 0 || on == 1) g_rot_skip = on;
