@@ -71,6 +71,33 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
   return s;
 }
 
+// Two / three block sums in one shared-memory round (2 barriers instead of
+// 2 per value); each value is reduced exactly as block_sum does (same
+// butterfly, same warp order), so the results are bit-identical to it.
+// `sh` holds K * NT / 32 doubles.  Results valid in thread 0.
+template <int NT, int K>
+__device__ __forceinline__ void block_sum_k(double (&v)[K], double *sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0)
+#pragma unroll
+    for (int k = 0; k < K; ++k) sh[k * (NT / 32) + w] = v[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < NT / 32; ++q) s += sh[k * (NT / 32) + q];
+      v[k] = s;
+    }
+  }
+}
+
 template <int NT>
 __device__ __forceinline__ double block_max(double v, double *sh) {
 #pragma unroll

@@ -170,33 +170,41 @@ __device__ __forceinline__ void spmv_tail(const bdem_system_t &S, const double *
 }
 
 // PCG-mode epilogue shared by the SpMV kernels: per-block partials of p.Ap,
-// |Ap|^2, |p|^2; the last block sets alpha or flags breakdown (linalg.py:69-77)
+// |Ap|^2, |p|^2 (one shared-memory round); the last block sets alpha, or
+// flags breakdown and only then sums |Ap|^2 and |p|^2 for the restart boost
+// (linalg.py:69-77).  Same partials and fixed-order sums as before.
 template <int NT>
 __device__ __forceinline__ void spmv_pcg_epilogue(const bdem_system_t &S, double boost,
                                                   double acc_xy, double acc_yy, double acc_xx,
                                                   double *sh) {
   double *pcg = S.pcg;
-  double v = block_sum<NT>(acc_xy, sh);
-  if (threadIdx.x == 0) *red_slot(S.red, RC_PAP, blockIdx.x) = v;
-  v = block_sum<NT>(acc_yy, sh);
-  if (threadIdx.x == 0) *red_slot(S.red, RC_AP2, blockIdx.x) = v;
-  v = block_sum<NT>(acc_xx, sh);
-  if (threadIdx.x == 0) *red_slot(S.red, RC_PP2, blockIdx.x) = v;
+  __shared__ double sh3[3 * (NT / 32)];
+  __shared__ double pap_sh;
+  double v3[3] = {acc_xy, acc_yy, acc_xx};
+  block_sum_k<NT, 3>(v3, sh3);
+  if (threadIdx.x == 0) {
+    *red_slot(S.red, RC_PAP, blockIdx.x) = v3[0];
+    *red_slot(S.red, RC_AP2, blockIdx.x) = v3[1];
+    *red_slot(S.red, RC_PP2, blockIdx.x) = v3[2];
+  }
   if (!last_block(S.counter + CNT_SPMV)) return;
   const double pap = sum_partials<NT>(S.red, RC_PAP, gridDim.x, sh);
+  if (threadIdx.x == 0) {
+    pap_sh = pap;
+    pcg[BDEM_PCG_PAP] = pap;
+    if (pap > 0.0) pcg[BDEM_PCG_ALPHA] = pcg[BDEM_PCG_RZ] / pap;
+  }
+  __syncthreads();
+  if (pap_sh > 0.0) return;
+  // breakdown: boost for the restart (linalg.py:74-77)
   const double ap2 = sum_partials<NT>(S.red, RC_AP2, gridDim.x, sh);
   const double pp2 = sum_partials<NT>(S.red, RC_PP2, gridDim.x, sh);
   if (threadIdx.x == 0) {
-    pcg[BDEM_PCG_PAP] = pap;
     pcg[BDEM_PCG_APNORM2] = ap2;
     pcg[BDEM_PCG_PNORM2] = pp2;
-    if (pap <= 0.0) {  // breakdown: boost for the restart (linalg.py:74-77)
-      const double sc = sqrt(ap2) / fmax(sqrt(pp2), 1e-300);
-      pcg[BDEM_PCG_BOOST] = fmax(boost * 100.0, 1e-10 * fmax(sc, 1.0));
-      pcg[BDEM_PCG_STATE] = PCG_BREAKDOWN;
-    } else {
-      pcg[BDEM_PCG_ALPHA] = pcg[BDEM_PCG_RZ] / pap;
-    }
+    const double sc = sqrt(ap2) / fmax(sqrt(pp2), 1e-300);
+    pcg[BDEM_PCG_BOOST] = fmax(boost * 100.0, 1e-10 * fmax(sc, 1.0));
+    pcg[BDEM_PCG_STATE] = PCG_BREAKDOWN;
   }
 }
 
@@ -589,10 +597,13 @@ __global__ void __launch_bounds__(kThreads, BDEM_UPD_MINB) k_pcg_update(bdem_sys
       }
     }
   }
-  double v = block_sum<kThreads>(acc_rr, sh);
-  if (threadIdx.x == 0) *red_slot(S.red, RC_RR, blockIdx.x) = v;
-  v = block_sum<kThreads>(acc_rz, sh);
-  if (threadIdx.x == 0) *red_slot(S.red, RC_RZ, blockIdx.x) = v;
+  __shared__ double sh2[2 * (kThreads / 32)];
+  double v2[2] = {acc_rr, acc_rz};
+  block_sum_k<kThreads, 2>(v2, sh2);
+  if (threadIdx.x == 0) {
+    *red_slot(S.red, RC_RR, blockIdx.x) = v2[0];
+    *red_slot(S.red, RC_RZ, blockIdx.x) = v2[1];
+  }
   if (!last_block(S.counter + CNT_UPDATE)) return;
   const double rr = sum_partials<kThreads>(S.red, RC_RR, gridDim.x, sh);
   const double rz_new = sum_partials<kThreads>(S.red, RC_RZ, gridDim.x, sh);
