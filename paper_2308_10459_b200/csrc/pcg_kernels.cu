@@ -124,9 +124,11 @@ __device__ __forceinline__ void spmv_tail(const bdem_system_t &S, const double *
                                           double boost, double &acc_xy, double &acc_yy,
                                           double &acc_xx) {
   const int64_t nf = S.vstride;
-  const int64_t e = __ldg(S.row_elem + (int64_t)sl * 32 + lane);
-  const int s = e >= 0 ? __ldg(S.slot + e) : -1;
+  // the row's free slot in one load (row_slot = slot[row_elem]); the element
+  // id only for the contact-pair terms
+  const int s = __ldg(S.row_slot + (int64_t)sl * 32 + lane);
   if (s < 0) return;
+  const int64_t e = S.n_pair > 0 ? __ldg(S.row_elem + (int64_t)sl * 32 + lane) : -1;
   // kRot false: the rotation half of x is identically zero (see
   // pcg_rot_active), so y's rotation half is zero and not formed
   for (int c = w; c < (kRot ? 6 : 3); c += W) {
