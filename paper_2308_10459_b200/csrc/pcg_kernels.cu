@@ -122,11 +122,10 @@ template <int W, bool kRot = true>
 __device__ __forceinline__ void spmv_tail(const bdem_system_t &S, const double *x, double *y,
                                           int sl, int w, int lane, const double (*part)[6][32],
                                           double boost, double &acc_xy, double &acc_yy,
-                                          double &acc_xx) {
+                                          double &acc_xx, int s) {
   const int64_t nf = S.vstride;
-  // the row's free slot in one load (row_slot = slot[row_elem]); the element
-  // id only for the contact-pair terms
-  const int s = __ldg(S.row_slot + (int64_t)sl * 32 + lane);
+  // s = the row's free slot (row_slot = slot[row_elem], loaded by the caller
+  // at the start of the slice); the element id only for the contact pairs
   if (s < 0) return;
   const int64_t e = S.n_pair > 0 ? __ldg(S.row_elem + (int64_t)sl * 32 + lane) : -1;
   // kRot false: the rotation half of x is identically zero (see
@@ -347,6 +346,7 @@ __device__ __forceinline__ void spmv_slices(const bdem_system_t &S, const double
 #pragma unroll 1
   for (int sl = s_begin; sl < s_end; sl += step) {
     const SliceBounds cb = slice_bounds(S, sl, ns);
+    const int s_row = __ldg(S.row_slot + (int64_t)sl * 32 + lane);
     double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     // software pipeline on the (cheap, integer) slot indices: the next slot's
     // index loads are in flight while this slot's coefficients arrive
@@ -361,7 +361,8 @@ __device__ __forceinline__ void spmv_slices(const bdem_system_t &S, const double
 #pragma unroll
     for (int q = 0; q < 6; ++q) part[w][q][lane] = acc[q];
     __syncthreads();
-    spmv_tail<kSpmvWarps, kRot>(S, x, y, sl, w, lane, part, boost, acc_xy, acc_yy, acc_xx);
+    spmv_tail<kSpmvWarps, kRot>(S, x, y, sl, w, lane, part, boost, acc_xy, acc_yy, acc_xx,
+                                s_row);
     __syncthreads();
   }
 }
@@ -503,7 +504,7 @@ __global__ void __launch_bounds__(kSpmvThreads, BDEM_SHFL_MINB)
 #pragma unroll
     for (int q = 0; q < 6; ++q) part[w][q][lane] = acc[q];
     __syncthreads();
-    spmv_tail<kSpmvWarps>(S, x, y, sl, w, lane, part, boost, acc_xy, acc_yy, acc_xx);
+    spmv_tail<kSpmvWarps>(S, x, y, sl, w, lane, part, boost, acc_xy, acc_yy, acc_xx, own);
     __syncthreads();
   }
   if (mode == 0) return;
