@@ -20,8 +20,19 @@ __all__ = [
     "Scene", "SolveResult", "SolverConfig", "SphereCollider", "StepReport", "broad_phase",
     "energy_terms", "label_components", "minimize_second_order", "relative_tolerance",
     "stable_step", "stretch_driver", "twist_driver", "update_bond_states",
-    "BROKEN", "INTACT", "WEAKENED",
+    "rotation_free_pcg", "BROKEN", "INTACT", "WEAKENED",
 ]
+
+
+def rotation_free_pcg(enabled: bool = True) -> bool:
+    """Switch the exact rotation-free PCG on or off (process-wide); returns
+    the previous setting.  When on, a Newton system whose right-hand side has
+    an identically zero rotation half (identity orientations and no
+    rotational load, e.g. the BASELINE plate) is solved on its position half
+    only: the rotation halves of every PCG vector stay exactly zero, so the
+    iterates are bit-identical to the full solve."""
+    from . import _lib
+    return bool(_lib.load().bdem_pcg_set_rot_skip(1 if enabled else 0))
 
 
 def __getattr__(name):

@@ -103,3 +103,14 @@ def test_graft_entry_build(lib):
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     entry = importlib.import_module("__graft_entry__")
     entry.build()
+
+
+def test_rotation_free_pcg_switch(lib):
+    """Host-only: the process-wide switch round-trips through the C ABI."""
+    import paper_2308_10459_b200 as P
+    prev = P.rotation_free_pcg(True)
+    try:
+        assert P.rotation_free_pcg(True) is True
+    finally:
+        P.rotation_free_pcg(prev)
+    assert lib.bdem_pcg_set_rot_skip(-1) == int(prev)
