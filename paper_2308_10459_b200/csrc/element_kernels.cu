@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_element_assemble(bdem_system_t 
     double ebond = 0.0;
     const int sl = (int)(row >> 5), lane = (int)(row & 31);
     // bonds with i == e: this element's SELL row (padding stages zeros)
+#pragma unroll 2
     for (int64_t b = S.slice_base[sl] + lane; b < S.slice_base[sl + 1]; b += 32) {
       double n[3], apos[6];
       const double kc = stage_stretch(st, S.scoef, nb, b, n, apos);
@@ -82,6 +83,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_element_assemble(bdem_system_t 
       ebond += st[BDEM_ST_E * nb + b];
     }
     // bonds with j == e (ascending bond id)
+#pragma unroll 2
     for (int64_t k = S.jslice_base[sl] + lane; k < S.jslice_base[sl + 1]; k += 32) {
       const int64_t b = S.jpos[k];
       if (b < 0) continue;
