@@ -329,7 +329,7 @@ __device__ __forceinline__ SliceBounds slice_bounds(const bdem_system_t &S, int 
 // ---------------------------------------------------------------------------
 template <bool kRot>
 __device__ __forceinline__ void spmv_slices(const bdem_system_t &S, const double *x, double *y,
-                                            double boost, double (*part)[6][32],
+                                            double boost, double (*part2)[kSpmvWarps][6][32],
                                             double &acc_xy, double &acc_yy, double &acc_xx) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ns = (int)((S.n_elem + 31) >> 5);
@@ -343,8 +343,13 @@ __device__ __forceinline__ void spmv_slices(const bdem_system_t &S, const double
 #else
   const int s_begin = blockIdx.x, s_end = ns, step = gridDim.x;
 #endif
+  int buf = 0;
 #pragma unroll 1
-  for (int sl = s_begin; sl < s_end; sl += step) {
+  for (int sl = s_begin; sl < s_end; sl += step, buf ^= 1) {
+    // partial products alternate between two buffers, so one barrier per
+    // slice suffices: a warp may start the next slice while others still
+    // read this slice's partials in the tail
+    double (*part)[6][32] = part2[buf];
     const SliceBounds cb = slice_bounds(S, sl, ns);
     const int s_row = __ldg(S.row_slot + (int64_t)sl * 32 + lane);
     double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
@@ -363,7 +368,6 @@ __device__ __forceinline__ void spmv_slices(const bdem_system_t &S, const double
     __syncthreads();
     spmv_tail<kSpmvWarps, kRot>(S, x, y, sl, w, lane, part, boost, acc_xy, acc_yy, acc_xx,
                                 s_row);
-    __syncthreads();
   }
 }
 
@@ -381,7 +385,7 @@ __device__ __forceinline__ bool pcg_rot_active(const double *pcg) {
 
 __global__ void __launch_bounds__(kSpmvThreads, BDEM_SPMV_MINB) k_spmv(bdem_system_t S, const double *x, double *y,
                                                        int mode) {
-  __shared__ double part[kSpmvWarps][6][32];
+  __shared__ double part[2][kSpmvWarps][6][32];
   __shared__ double sh[kSpmvThreads / 32];
 #if BDEM_TIMELINE
   const unsigned long long t_arrive = tl_now();
