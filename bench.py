@@ -313,7 +313,17 @@ def assembly_bytes(dev):
 # Chip-wide L2-slice (LTS) throughput cap per SM clock, measured on the
 # GB300 (B300_MICROARCH.md "LTS throughput cap ~6300 B/cyc full-chip"); the
 # SpMV's gathers re-read coefficients and x from L2, so this is its real bound.
-L2_BYTES_PER_CLK = 6300.0
+def _l2_bytes_per_clk():
+    """Measured L2 read throughput of this B200 (profiles/l2_peak.json,
+    scratch/l2bw); the B300 figure of B300_MICROARCH.md if absent."""
+    try:
+        with open(os.path.join(REPO, "profiles", "l2_peak.json")) as fh:
+            return float(json.load(fh)["l2_read_bytes_per_clk"]), "measured (profiles/l2_peak.json)"
+    except Exception:
+        return 6300.0, "B300_MICROARCH.md estimate"
+
+
+L2_BYTES_PER_CLK, L2_CAP_SOURCE = _l2_bytes_per_clk()
 
 
 def l2_roofline(ncu, spmv_ms, clocks):
@@ -326,7 +336,8 @@ def l2_roofline(ncu, spmv_ms, clocks):
     achieved = 32.0 * sectors / (spmv_ms * 1e-3) / 1e9
     cap = L2_BYTES_PER_CLK * mhz * 1e6 / 1e9
     return {"bytes_per_launch": 32.0 * sectors, "achieved": achieved, "cap": cap, "unit": "GB/s",
-            "frac": achieved / cap, "source": "ncu lts__t_sectors.sum x 32 B (profiles/ncu_traffic.json)"}
+            "frac": achieved / cap, "source": "ncu lts__t_sectors.sum x 32 B (profiles/ncu_traffic.json)",
+            "cap_source": f"{L2_BYTES_PER_CLK:.0f} B/clk x sampled SM clock, {L2_CAP_SOURCE}"}
 
 
 def load_ncu_traffic():
