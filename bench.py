@@ -475,6 +475,15 @@ def run_ours(args):
 
     (ms_max, e2e_ms_max), (newton_all, e2e_newton_all) = reduce_across_ranks(
         [ms, e2e_ms], [stats["newton"], e2e_newton], world, "cuda")
+    if rot is not None and world > 1:
+        # whole-job figure like the headline: all ranks' Newton iterations
+        # over the slowest rank's time
+        (rot_ms_max,), (rot_newton_all, same_all) = reduce_across_ranks(
+            [rot["ms_per_step"] * args.steps], [rot["newton_iterations"],
+                                                float(rot["bit_identical_final_state"])],
+            world, "cuda")
+        rot["value"] = rot_newton_all / (rot_ms_max * 1e-3)
+        rot["bit_identical_final_state"] = bool(same_all == world)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
