@@ -222,10 +222,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_element_assemble(bdem_system_t 
 }
 
 // fixed-order finish of per-block partials -> scalars
+// one block per column (grid = ncol): each column is reduced exactly as
+// before (same per-thread strided partial sums, same block_sum order)
 __global__ void __launch_bounds__(kThreads) k_reduce_finish(bdem_system_t S, int col0, int ncol,
                                                             int nblocks) {
   __shared__ double sh[kThreads / 32];
-  for (int c = col0; c < col0 + ncol; ++c) {
+  for (int c = col0 + blockIdx.x; c < col0 + ncol; c += gridDim.x) {
     double v;
     if (c == BDEM_SC_MAXDEV) {
       double m = 0.0;
@@ -440,7 +442,8 @@ int bdem_element_assemble(const bdem_system_t *sys, const double *p, const doubl
 int bdem_reduce_finish(const bdem_system_t *sys, int col0, int ncol, int nblocks,
                        void *stream) {
   if (!sys || col0 < 0 || col0 + ncol > BDEM_SC_COUNT || nblocks > kRedBlocks) return BDEM_ERR_ARG;
-  k_reduce_finish<<<1, kThreads, 0, as_stream(stream)>>>(*sys, col0, ncol, nblocks);
+  k_reduce_finish<<<ncol > 0 ? ncol : 1, kThreads, 0, as_stream(stream)>>>(*sys, col0, ncol,
+                                                                           nblocks);
   return launch_status();
 }
 
