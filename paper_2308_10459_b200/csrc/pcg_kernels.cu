@@ -315,15 +315,19 @@ __device__ __forceinline__ SliceBounds slice_bounds(const bdem_system_t &S, int 
 }
 
 // ---------------------------------------------------------------------------
-// SpMV, slot-parallel form.  One CTA walks 32-element slices; in each slice
-// warp w handles slot w of the slice's i-role then j-role lists (lane =
-// element), so each thread issues one independent set of loads: 15
-// coefficient planes (contiguous 256-byte warp segments) and the
-// neighbour's x block.  The next slice's bounds and slot indices are
-// prefetched while the current slice's data is in flight, and warps 0..5
-// prefetch their diagonal row and x before the barrier, so a slice costs
-// about one memory latency.  Partial products meet in shared memory; warp c
-// forms component c of y = D x + sum_slots in a fixed order (deterministic).
+// SpMV, slot-parallel form.  One CTA of 4 warps walks 32-element slices
+// (strided over the grid); in each slice warp w handles slots w, w+4, ... of
+// the slice's i-role then j-role lists (lane = element), so each thread
+// issues one independent set of loads per slot: 14 coefficient planes
+// (contiguous 256-byte warp segments, AoSoA-32) and the neighbour's x block
+// (evict-last L2 policy: each block is gathered ~12 times).  The next slot's
+// indices are loaded while the current slot's data is in flight; the row's
+// free slot comes from row_slot in one load.  Partial products meet in a
+// double-buffered shared-memory array (one barrier per slice); warp c forms
+// component c (and c + 4) of y = D x + sum of the warp partials in a fixed
+// order (deterministic).  The kernel is memory-latency bound at the
+// 64-register / 8-CTA point; every variant that keeps more loads in flight
+// spilled (profiles/r01/README.md).
 // mode 0: plain y = A x;  mode 1: PCG step (y = A p + boost p, p.Ap, |Ap|^2,
 // |p|^2 and the breakdown test, linalg.py:69-77).
 // ---------------------------------------------------------------------------
