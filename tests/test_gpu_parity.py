@@ -732,3 +732,36 @@ def test_rot_skip_bit_identical(cuda_ok, case):
     assert np.array_equal(p0, p1) and np.array_equal(q0, q1) and np.array_equal(v0, v1)
     assert all(f == 0.0 for f in f0)
     assert all(f == (1.0 if case == "plate" else 0.0) for f in f1)
+
+
+def test_rot_skip_with_fracture_and_fused_update(cuda_ok):
+    """Rotation-free PCG together with the fused update kernel on the
+    identity-q cube crushed by a descending plane (bonds break): the same
+    trajectory, fracture events and Newton/PCG counts, bit for bit, as the
+    default path."""
+    from paper_2308_10459_b200 import SolverConfig, stable_step
+    from paper_2308_10459_b200 import _lib as L
+    from paper_2308_10459_b200 import configs as C
+    from paper_2308_10459_b200.scene import Scene
+    lib = L.load()
+    out = []
+    for skip, fused in ((0, 0), (1, 1)):
+        prev_s = lib.bdem_pcg_set_rot_skip(skip)
+        prev_f = lib.bdem_pcg_set_fused(fused)
+        try:
+            spec = C.cube(n_side=6, random_q=False, seed=3, youngs=3e8, k_contact=1e9, speed=2.0,
+                          dt=1e-4)
+            scene = Scene.from_spec(spec)
+            recs, events = [], []
+            for _ in range(6):
+                scene.colliders = spec.collider_schedule(scene.time + scene.dt)
+                rep = stable_step(scene, SolverConfig(epsilon=1e-6, max_iterations=300))
+                recs.append((rep.committed, rep.solve.iterations, rep.solve.pcg_total))
+                events.append([b for (b, _, _) in rep.broken])
+        finally:
+            lib.bdem_pcg_set_rot_skip(prev_s)
+            lib.bdem_pcg_set_fused(prev_f)
+        out.append((recs, events, scene.elements.p.copy(), scene.elements.q.copy()))
+    (r0, e0, p0, q0), (r1, e1, p1, q1) = out
+    assert r0 == r1 and e0 == e1
+    assert np.array_equal(p0, p1) and np.array_equal(q0, q1)
