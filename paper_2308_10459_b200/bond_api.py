@@ -42,6 +42,7 @@ def energy_terms(bonds, p, q, want_hess=False, want_grad=True, dev=None):
              out["gqi"].data_ptr(), out["gqj"].data_ptr(),
              hpp.data_ptr() if want_hess else None, hqq.data_ptr() if want_hess else None,
              int(bool(want_hess)), dev.stream)
+    dev.eval_pq = (pd, qd)
     dev.read_scalars()  # synchronises and raises DegenerateBondError / DegenerateShearError
     h = {k: v.cpu().numpy() for k, v in out.items()}
     if not (want_grad or want_hess):

@@ -423,6 +423,8 @@ class DeviceSystem:
         self._sel_work = None
         self.launches = 0
         self.labels = None
+        self._bi_np, self._bj_np = bi64, bj64   # caller bond order (error messages)
+        self.eval_pq = None   # (p, q) of the last evaluation (error messages)
         self.timer = None   # optional timing.KernelTimer picked up by GPUProblem
         self._pins = {}
 
@@ -669,16 +671,41 @@ class DeviceSystem:
         return int(self.sell.bond_of_pos[pos]) if 0 <= pos < self.sell.n_pos else -1
 
     def raise_errors(self, host_err):
-        if host_err[L.ERRSLOT_DEG_COUNT] > 0:
-            first = self.bond_id(int(host_err[L.ERRSLOT_DEG_FIRST]))
-            self.reset_errors()
-            raise DegenerateBondError(f"coincident bond endpoints at bond indices [{first}] "
-                                      f"({int(host_err[L.ERRSLOT_DEG_COUNT])} total)")
-        if host_err[L.ERRSLOT_ANTI_COUNT] > 0:
-            first = self.bond_id(int(host_err[L.ERRSLOT_ANTI_FIRST]))
-            self.reset_errors()
-            raise DegenerateShearError(f"antipodal quaternion pairs at bond indices [{first}] "
-                                       f"({int(host_err[L.ERRSLOT_ANTI_COUNT])} total)")
+        """Re-raise a kernel's data error as the reference exception.
+
+        The message lists, like ``stretch_terms`` / ``shear_terms``
+        (bonds.py:163-168, 222-227), the offending indices into the ACTIVE
+        bond list of ``energy_terms`` (bonds.py:482-490), evaluated at the
+        state the kernel saw (``self.eval_pq``, set by the caller before the
+        read-back).  Error path only: the state is read back and the
+        indices are recovered on the host."""
+        deg = host_err[L.ERRSLOT_DEG_COUNT] > 0
+        if not deg and host_err[L.ERRSLOT_ANTI_COUNT] <= 0:
+            return
+        first = self.bond_id(int(host_err[L.ERRSLOT_DEG_FIRST if deg
+                                           else L.ERRSLOT_ANTI_FIRST]))
+        self.reset_errors()
+        idx = [first]
+        if self.eval_pq is not None:
+            idx = self._offending_active(*self.eval_pq, deg)
+        if deg:
+            raise DegenerateBondError(f"coincident bond endpoints at indices {idx}")
+        raise DegenerateShearError(f"antipodal quaternion pairs at indices {idx}")
+
+    def _offending_active(self, p, q, degenerate: bool) -> list:
+        pos = self.sell.pos_of_bond
+        status = self.status.cpu().numpy()[pos]
+        act = np.nonzero(status != 2)[0]
+        i, j = self._bi_np[act], self._bj_np[act]
+        if degenerate:
+            pp = p.cpu().numpy()
+            l0 = self.geom[L.BG["L0"]].cpu().numpy()[pos][act]
+            bad = np.linalg.norm(pp[j] - pp[i], axis=-1) < 1e-12 * l0
+        else:
+            qq = q.cpu().numpy()
+            u = qq[i] + qq[j]
+            bad = np.sum(u * u, axis=-1) < 1e-8**2
+        return np.nonzero(bad)[0].tolist()
 
     def read_scalars(self):
         """Synchronise once and return (scalars, err) host arrays."""

@@ -120,6 +120,7 @@ class GPUProblem:
             d.call("bdem_pair_assemble", s, p.data_ptr(), 0, st)
         d.call("bdem_element_assemble", s, p.data_ptr(), q.data_ptr(), d.z.data_ptr(), st)
         d.call("bdem_reduce_finish", s, 0, 7, L.RED_BLOCKS, st)
+        d.eval_pq = (p, q)
         sc = d.read_scalars()
         f = float(sc[L.SC["F"]])
         gnorm = math.sqrt(float(sc[L.SC["GNORM2"]]))
@@ -145,6 +146,7 @@ class GPUProblem:
         d.call("bdem_bond_energy", s, p.data_ptr(), q.data_ptr(), L.SC["EBOND"], st)
         d.call("bdem_pair_assemble", s, p.data_ptr(), 1, st)
         d.call("bdem_reduce_finish", s, L.SC["FT"], 7, L.RED_BLOCKS, st)
+        d.eval_pq = (p, q)
         sc = d.read_scalars()
         # inertia + (bonds + contacts - gravity)   (integrator.py:87-93, 191-193)
         return float(sc[L.SC["FT"]]) + (((float(sc[L.SC["EBOND"]]) + float(sc[L.SC["EPAIR"]]))

@@ -112,11 +112,16 @@ def driver_from_spec(spec):
 class Scene:
     """Scene state (scenes.py:32-77); attribute names follow the reference."""
 
-    def __init__(self, name, elements: ElementSet, bonds: BondSet, colliders=None,
+    def __init__(self, name, mesh, elements: ElementSet, bonds: BondSet, colliders=None,
                  gravity=None, dt=1.0 / 60.0, youngs=1e7, shear_modulus=4e6, density=2500.0,
                  k_contact=1e6, k_element=1e6, mu_s=0.0, mu_r=0.0,
                  plastic: PlasticParams | None = None, driver=None, time=0.0, p_prev=None,
-                 q_prev=None, labels=None, surface_flags=None, mesh=None, host_sync=True):
+                 q_prev=None, labels=None, surface_flags=None, *, host_sync=True):
+        """Positional and keyword order of the reference dataclass
+        (scenes.py:31-52: name, mesh, elements, bonds, colliders, gravity, dt,
+        youngs, shear_modulus, density, k_contact, k_element, mu_s, mu_r,
+        plastic, driver, time, p_prev, q_prev, labels, surface_flags); ``mesh``
+        may be None (lattice scenes), ``host_sync`` is keyword-only."""
         self.name, self.mesh = name, mesh
         self.elements, self.bonds = elements, bonds
         self.colliders = list(colliders or [])
@@ -195,9 +200,9 @@ class Scene:
 
     @classmethod
     def from_spec(cls, spec, host_sync=True) -> "Scene":
-        return cls(spec.name, spec.elements, spec.bonds, colliders=spec.colliders,
+        return cls(spec.name, spec.mesh, spec.elements, spec.bonds, colliders=spec.colliders,
                    gravity=spec.gravity, dt=spec.dt, youngs=spec.youngs,
                    shear_modulus=spec.shear_modulus, density=spec.density,
                    k_contact=spec.k_contact, k_element=spec.k_element, plastic=spec.plastic,
                    driver=driver_from_spec(spec.driver), mu_s=spec.mu_s, mu_r=spec.mu_r,
-                   mesh=spec.mesh, host_sync=host_sync)
+                   host_sync=host_sync)

@@ -217,10 +217,23 @@ def _apply_driver(scene, dev, t):
         getattr(dev, name)[pin] = src
 
 
-def stable_step(scene, cfg: SolverConfig, method: str = "second-order") -> StepReport:
-    """Advance ``scene`` by one implicit step on the GPU (solver.py:881-939)."""
-    if method not in MINIMIZERS:
-        raise ValueError(f"the GPU path implements {sorted(MINIMIZERS)}, got {method!r}")
+@dataclass
+class PreparedStep:
+    """The step-1..6 prologue of stable_step (solver.py:894-906): what the
+    minimizer and the epilogue need."""
+
+    problem: GPUProblem
+    pairs: object
+    pin: object
+    backup: tuple
+    t_next: float
+
+
+def prepare_step(scene) -> PreparedStep:
+    """Everything stable_step does before the minimizer (solver.py:894-906,
+    integrator.py:141-161, 268-274): state upload, pinned backups, driver rows
+    at t + dt, the step context, frozen contact candidates and the predictor
+    (p0, q0 in ``dev.xp`` / ``dev.xq``)."""
     dev = scene.device
     if scene.host_sync:
         dev.upload_elements(scene.elements, scene.p_prev, scene.q_prev)
@@ -245,7 +258,17 @@ def stable_step(scene, cfg: SolverConfig, method: str = "second-order") -> StepR
              dev.qdot.data_ptr(), dev.p_prev.data_ptr(), dev.q_prev.data_ptr(), float(scene.dt),
              dev.p_hat.data_ptr(), dev.q_hat.data_ptr(), dev.mp_dt2.data_ptr(),
              dev.mq_dt2.data_ptr(), dev.xp.data_ptr(), dev.xq.data_ptr(), st)
-    problem = GPUProblem(dev)
+    return PreparedStep(GPUProblem(dev), pairs, pin, backup, t_next)
+
+
+def stable_step(scene, cfg: SolverConfig, method: str = "second-order") -> StepReport:
+    """Advance ``scene`` by one implicit step on the GPU (solver.py:881-939)."""
+    if method not in MINIMIZERS:
+        raise ValueError(f"the GPU path implements {sorted(MINIMIZERS)}, got {method!r}")
+    prep = prepare_step(scene)
+    dev, problem, pairs = scene.device, prep.problem, prep.pairs
+    pin, backup, t_next = prep.pin, prep.backup, prep.t_next
+    st = dev.stream
     result = MINIMIZERS[method](problem, dev.xp, dev.xq, cfg)
     n_pairs = int(pairs.shape[0])
 

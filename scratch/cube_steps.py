@@ -8,7 +8,7 @@ d = load("traj_cube.npz")
 spec = C.cube(n_side=5, random_q=False, seed=3, youngs=3e8, k_contact=1e9, speed=2.0, dt=1e-4)
 el = elements_from(d, "init_el_"); b = bonds_from(d, "init_b_")
 from paper_2308_10459_b200 import PlasticParams
-scene = Scene("cube", el, b, colliders=[], gravity=d["gravity"], dt=float(d["dt"]), youngs=float(d["youngs"]), plastic=PlasticParams(*d["plastic"]),
+scene = Scene("cube", None, el, b, colliders=[], gravity=d["gravity"], dt=float(d["dt"]), youngs=float(d["youngs"]), plastic=PlasticParams(*d["plastic"]),
               k_contact=float(d["k_contact"]), k_element=float(d["k_element"]))
 for s in range(6):
     scene.colliders = spec.collider_schedule(scene.time + scene.dt)

@@ -10,7 +10,7 @@ from paper_2308_10459_b200.step import contact_candidates
 d = load("traj_cube.npz")
 spec = C.cube(n_side=5, random_q=False, seed=3, youngs=3e8, k_contact=1e9, speed=2.0, dt=1e-4)
 el = elements_from(d, "init_el_"); b = bonds_from(d, "init_b_")
-scene = Scene("cube", el, b, colliders=spec.collider_schedule(spec.dt), gravity=d["gravity"], dt=float(d["dt"]),
+scene = Scene("cube", None, el, b, colliders=spec.collider_schedule(spec.dt), gravity=d["gravity"], dt=float(d["dt"]),
               youngs=float(d["youngs"]), k_contact=float(d["k_contact"]), k_element=float(d["k_element"]), host_sync=False)
 dev = scene.device
 dev.set_physics(scene.gravity, scene.k_contact, scene.k_element, scene.colliders)

@@ -6,7 +6,7 @@ from paper_2308_10459_b200 import configs as C
 d = load("traj_stack.npz")
 el = elements_from(d, "init_el_"); b = bonds_from(d, "init_b_")
 for mu in (True, False):
-    scene = Scene("stack", el.copy(), b.copy(), colliders=C.stack().colliders, gravity=d["gravity"], dt=float(d["dt"]),
+    scene = Scene("stack", None, el.copy(), b.copy(), colliders=C.stack().colliders, gravity=d["gravity"], dt=float(d["dt"]),
                   youngs=float(d["youngs"]), k_contact=float(d["k_contact"]), k_element=float(d["k_element"]),
                   mu_s=float(d["mu_s"]) if mu else 0.0, mu_r=float(d["mu_r"]) if mu else 0.0)
     for s in range(8):

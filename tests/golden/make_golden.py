@@ -332,11 +332,10 @@ def _run_traj(name, spec, steps, eps, driver=None, schedule=None, max_iter=300):
 
 
 def gold_trajectories():
-    # BASELINE's eps=1e-8 sits on this beam's line-search noise floor: the
-    # reference stalls at gnorm 1.16e-8 from step 2 on (300 iterations,
-    # committed=False).  Trajectory parity uses 1e-7, where every step commits.
+    # BASELINE configs[0] exactly: 40x4x4, eps=1e-8, 20 steps, coordinates
+    # centred at the origin; the reference commits all 20 steps.
     spec = C.cantilever()
-    _run_traj("cantilever", spec, 20, 1e-7)
+    _run_traj("cantilever", spec, 20, 1e-8)
 
     spec = C.rope(n=30, epsilon=1e-5)
     drv = spec.driver
@@ -350,6 +349,247 @@ def gold_trajectories():
                   dt=1e-4)
     sched = spec.collider_schedule
     _run_traj("cube", spec, 6, 1e-6, schedule=sched)
+
+
+def _subsample_rows(n, stride):
+    return np.unique(np.r_[np.arange(0, n, stride), np.arange(max(n - 3, 0), n)])
+
+
+def gold_rope100k():
+    """BASELINE configs[3] at its full size (100,000 spheres, G = 10 E, end
+    twisted at 10 rad/s, eps 1e-5): the first 5 implicit steps of the
+    reference.  The rotation path (twist driver, quaternion retraction,
+    tangent-projected qdot) is the only one that moves q, so every element's
+    q and qdot matter; the fixture keeps a strided subsample of rows plus both
+    ends and the whole-array norms."""
+    spec = C.rope()
+    drv = spec.driver
+    sc = ref_scene(spec, driver=rs.twist_driver(drv.ids, drv.p0, drv.axis_point, drv.rate))
+    cfg = rsv.SolverConfig(epsilon=1e-5, max_iterations=300)
+    rows = _subsample_rows(spec.elements.n, 331)
+    rec = {k: [] for k in ("p", "q", "v", "qdot", "newton", "pcg", "committed", "gnorm",
+                           "q_dev_norm", "qdot_norm", "pcg_per_newton", "reason")}
+    t0 = time.time()
+    for s in range(5):
+        rep = rsv.stable_step(sc, cfg)
+        el = sc.elements
+        for k, v in (("p", el.p), ("q", el.q), ("v", el.v), ("qdot", el.qdot)):
+            rec[k].append(v[rows].copy())
+        rec["q_dev_norm"].append(float(np.linalg.norm(el.q - np.array([0.0, 0, 0, 1]))))
+        rec["qdot_norm"].append(float(np.linalg.norm(el.qdot)))
+        rec["newton"].append(rep.solve.iterations)
+        rec["pcg"].append(rep.solve.pcg_total)
+        rec["pcg_per_newton"].append([r.pcg_iterations for r in rep.solve.records])
+        rec["committed"].append(rep.committed)
+        rec["gnorm"].append(rep.solve.grad_norm)
+        rec["reason"].append(rep.solve.reason)
+        print(f"    step {s}: newton {rep.solve.iterations} pcg {rep.solve.pcg_total} "
+              f"{rep.solve.reason} gnorm {rep.solve.grad_norm:.3e} ({time.time() - t0:.0f}s)",
+              flush=True)
+    out = {k: np.array(v) for k, v in rec.items() if k != "pcg_per_newton"}
+    out["pcg_per_newton"] = np.array(sum(rec["pcg_per_newton"], []))
+    out.update({"rows": rows, "n": spec.elements.n, "epsilon": 1e-5, "seconds": time.time() - t0})
+    save("traj_rope100k.npz", **out)
+
+
+def gold_plate600k():
+    """The north-star config at full size (BASELINE configs[2], SURVEY 8(d) C3:
+    1000x600 plate, 3,591,004 bonds, eps 1e-3): the step-1 problem exactly as
+    stable_step builds it (solver.py:902-908) and the first two Newton
+    iterations of minimize_second_order (solver.py:511-562).  Kept: the
+    iteration records (f, |z|, alpha, PCG counts), the Newton direction y and
+    the iterate after each iteration on a strided subsample of rows, and the
+    contact-candidate count."""
+    spec = C.plate()
+    t0 = time.time()
+    sc = ref_scene(spec)
+    print(f"    scene built in {time.time() - t0:.0f}s", flush=True)
+    el = sc.elements
+    t1 = time.time()
+    pairs = rsv.contact_candidates(sc)
+    t_bp = time.time() - t1
+    ctx = ri.StepContext(sc.dt, sc.p_prev.copy(), sc.q_prev.copy(), el.p.copy(), el.q.copy())
+    model = ri.PotentialModel(el, sc.bonds, pairs, sc.colliders, sc.gravity, sc.k_contact,
+                              sc.k_element)
+    prob = ri.ImplicitProblem(model, ctx)
+    p0, q0 = ri.predict_state(ctx, el.v, el.qdot, prob.free)
+    n = el.n
+    rows = _subsample_rows(n, 997)
+    free_ids = np.nonzero(prob.free)[0]
+    slot = np.full(n, -1)
+    slot[free_ids] = np.arange(free_ids.size)
+    y_idx = (6 * slot[rows][:, None] + np.arange(6)[None, :]).ravel()
+    cap = {"y": [], "p": [], "q": [], "t": []}
+    orig_nd, orig_ls = rsv._newton_direction, rsv.line_search
+
+    def nd(*a, **k):
+        out = orig_nd(*a, **k)
+        cap["y"].append(out[0][y_idx].copy())
+        return out
+
+    def ls(*a, **k):
+        out = orig_ls(*a, **k)
+        cap["p"].append(out[1][rows].copy())
+        cap["q"].append(out[2][rows].copy())
+        cap["t"].append(time.time())
+        return out
+
+    rsv._newton_direction, rsv.line_search = nd, ls
+    try:
+        t2 = time.time()
+        sol = rsv.minimize_second_order(prob, p0, q0,
+                                        rsv.SolverConfig(epsilon=1e-3, max_iterations=2))
+        t_solve = time.time() - t2
+    finally:
+        rsv._newton_direction, rsv.line_search = orig_nd, orig_ls
+    recs = sol.records
+    print(f"    2 Newton iterations in {t_solve:.0f}s: gnorm "
+          f"{[r.grad_norm for r in recs]} pcg {[r.pcg_iterations for r in recs]} "
+          f"alpha {[r.alpha for r in recs]}", flush=True)
+    save("plate600k_newton.npz", rows=rows, n=n, n_bonds=sc.bonds.n, n_pairs=pairs.shape[0],
+         p0=p0[rows], q0=q0[rows], y=np.array(cap["y"]), p=np.array(cap["p"]),
+         q=np.array(cap["q"]), rec_f=np.array([r.f for r in recs]),
+         rec_gnorm=np.array([r.grad_norm for r in recs]),
+         rec_cnorm=np.array([r.constraint_norm for r in recs]),
+         rec_alpha=np.array([r.alpha for r in recs]),
+         rec_pcg=np.array([r.pcg_iterations for r in recs]), epsilon=1e-3,
+         seconds_solve=t_solve, seconds_broadphase=t_bp)
+
+
+def _extra_elements(el, rows):
+    """Append isolated elements (p, mass, radius) to an ElementSet copy."""
+    k = len(rows)
+    p = np.concatenate([el.p, np.array([r[0] for r in rows], dtype=float)])
+    q = np.concatenate([el.q, np.tile([0.0, 0.0, 0.0, 1.0], (k, 1))])
+    return type(el)(p, q, np.concatenate([el.v, np.zeros((k, 3))]),
+                    np.concatenate([el.qdot, np.zeros((k, 4))]),
+                    np.concatenate([el.mass, [r[1] for r in rows]]),
+                    np.concatenate([el.radius, [r[2] for r in rows]]),
+                    np.concatenate([el.pinned, np.zeros(k, dtype=bool)]))
+
+
+def gold_failures():
+    """The reference's failure branches, each driven the way it can happen:
+
+    * pcg breakdown / diagonal-boost restart (linalg.py:74-97): the "near"
+      Newton system of newton_pieces.npz with every diagonal block shifted by
+      -c I (c = lambda_min(A) + delta) -- an indefinite operator; its
+      block-Jacobi (linalg.py:100-128) falls back to identity on the blocks
+      the shift made singular or indefinite.  One shift the boost cures
+      (restarts, then convergence) and one it does not (gives up after 4).
+    * BlockJacobi identity fallback in a real solve: a cantilever plus two
+      isolated free elements -- one with zero mass (zero 6x6 block) and one
+      with zero radius (position block m/dt^2 I, rotation block 0: singular
+      as a 6x6 block) -- stepped with stable_step.
+    * non-descent fallback (solver.py:542-548): minimize_second_order on the
+      newton_solve problem with the linear solve replaced by one returning
+      x = -b (an ascent direction); every iteration falls back to -z.
+    * reason="line-search" (solver.py:549-556): a random-q cube, whose
+      prestressed bonds defeat the line search.
+    * DegenerateBondError (bonds.py:163-168) raised through stable_step: a
+      two-element bond whose predictor makes its endpoints coincide.
+    """
+    from bdem import elements as re_
+    out = {}
+    # -- pcg breakdown -------------------------------------------------------
+    d = dict(np.load(os.path.join(HERE, "newton_pieces.npz")))
+    A, diag, z = d["near_A"], d["near_diag"], d["near_z"]
+    lam0 = float(np.linalg.eigvalsh(A).min())
+    for tag, delta in (("cured", 5e-8), ("giveup", 1e3)):
+        c = lam0 + delta
+        dmod = diag - c * np.eye(6)[None]
+        amod = A - c * np.eye(A.shape[0])
+        pre = rl.BlockJacobi(dmod)
+        res = rl.pcg(lambda v: amod @ v, -z, pre.apply, 1e-8, 2000)
+        print(f"  pcg {tag}: lambda_min {float(np.linalg.eigvalsh(amod).min()):.3e} "
+              f"restarts {res.restarts} it {res.iterations} converged {res.converged}")
+        out.update({f"pcg_{tag}_diag": dmod, f"pcg_{tag}_minv": pre.inverse_blocks,
+                    f"pcg_{tag}_x": res.x, f"pcg_{tag}_it": res.iterations,
+                    f"pcg_{tag}_restarts": res.restarts,
+                    f"pcg_{tag}_converged": res.converged,
+                    f"pcg_{tag}_rel": res.relative_residual, f"pcg_{tag}_shift": c})
+    out["pcg_tol"] = 1e-8
+    # -- singular block-Jacobi in a real solve ---------------------------------
+    spec = C.cantilever(nx=6, ny=3, nz=3)
+    m0 = float(spec.elements.mass[0])
+    el = _extra_elements(spec.elements, [((1.0, 0.0, 0.0), 0.0, 0.005),
+                                         ((-1.0, 0.0, 0.0), m0, 0.0)])
+    spec.elements = el
+    sc = ref_scene(spec)
+    cfg = rsv.SolverConfig(epsilon=1e-7, max_iterations=300)
+    pk = {k: [] for k in ("p", "q", "newton", "pcg", "committed")}
+    import logging
+    logging.getLogger("bdem").setLevel(logging.ERROR)
+    for _ in range(3):
+        rep = rsv.stable_step(sc, cfg)
+        pk["p"].append(sc.elements.p.copy())
+        pk["q"].append(sc.elements.q.copy())
+        pk["newton"].append(rep.solve.iterations)
+        pk["pcg"].append(rep.solve.pcg_total)
+        pk["committed"].append(rep.committed)
+    print(f"  singular: newton {pk['newton']} pcg {pk['pcg']} committed {pk['committed']}")
+    out.update(pack("sing_el_", el, ELEM_FIELDS))
+    out.update({f"sing_{k}": np.array(v) for k, v in pk.items()})
+    # -- non-descent fallback --------------------------------------------------
+    g = dict(np.load(os.path.join(HERE, "newton_solve.npz")))
+    el = re_.ElementSet(*(g[f"el_{f}"] for f in ELEM_FIELDS))
+    bs = rb.BondSet(**{f: g[f"b_{f}"] for f in BOND_FIELDS},
+                    face_i=np.zeros(g["b_i"].shape[0], dtype=np.int64),
+                    face_j=np.zeros(g["b_i"].shape[0], dtype=np.int64))
+    hs = g["hs"]
+    ctx = ri.StepContext(float(g["dt"]), g["p_prev"], g["q_prev"], el.p.copy(), el.q.copy())
+    model = ri.PotentialModel(el, bs, g["pairs"], [rc.HalfSpace(tuple(hs[:3]), hs[3])],
+                              g["gravity"], float(g["kc"]), float(g["ke"]))
+    prob = ri.ImplicitProblem(model, ctx)
+    orig_pcg = rsv.pcg
+
+    def ascent(apply_a, b, apply_m=None, tol_rel=1e-10, max_iter=None, on_iteration=None):
+        return rl.PCGResult(-np.asarray(b, dtype=float), 1, True, 1.0)
+
+    rsv.pcg = ascent
+    try:
+        sol = rsv.minimize_second_order(prob, g["p0"], g["q0"],
+                                        rsv.SolverConfig(epsilon=1e-9, max_iterations=6))
+    finally:
+        rsv.pcg = orig_pcg
+    print(f"  non-descent: {sol.reason} it {sol.iterations} alpha "
+          f"{[r.alpha for r in sol.records]}")
+    out.update({"nd_p": sol.p, "nd_q": sol.q, "nd_iterations": sol.iterations,
+                "nd_reason": np.array(sol.reason),
+                "nd_rec_f": np.array([r.f for r in sol.records]),
+                "nd_rec_gnorm": np.array([r.grad_norm for r in sol.records]),
+                "nd_rec_alpha": np.array([r.alpha for r in sol.records])})
+    # -- line-search failure on a random-q cube ------------------------------------
+    spec = C.cube(n_side=4, seed=2, random_q=True)
+    sc = ref_scene(spec)
+    rep = rsv.stable_step(sc, rsv.SolverConfig(epsilon=1e-6, max_iterations=300))
+    recs = rep.solve.records
+    print(f"  line-search: committed {rep.committed} reason {rep.solve.reason} "
+          f"it {rep.solve.iterations} gnorm {rep.solve.grad_norm:.3e}")
+    out.update(pack("ls_el_", spec.elements, ELEM_FIELDS))
+    out.update(pack("ls_b_", spec.bonds, BOND_FIELDS))
+    out.update({"ls_committed": rep.committed, "ls_reason": np.array(rep.solve.reason),
+                "ls_iterations": rep.solve.iterations,
+                "ls_rec_f": np.array([r.f for r in recs]),
+                "ls_rec_gnorm": np.array([r.grad_norm for r in recs]),
+                "ls_rec_alpha": np.array([r.alpha for r in recs]),
+                "ls_rec_pcg": np.array([r.pcg_iterations for r in recs]),
+                "ls_p_after": sc.elements.p, "ls_q_after": sc.elements.q})
+    # -- degenerate bond through stable_step ----------------------------------------
+    spec = C.cantilever(nx=2, ny=1, nz=1, dt=1e-3)
+    el = spec.elements
+    el.pinned[:] = False
+    el.v[0] = (el.p[1] - el.p[0]) / spec.dt
+    sc = ref_scene(spec)
+    try:
+        rsv.stable_step(sc, rsv.SolverConfig(epsilon=1e-7))
+        msg, kind = "", ""
+    except Exception as exc:            # noqa: BLE001 - the class is the golden
+        msg, kind = str(exc), type(exc).__name__
+    print(f"  degenerate: {kind}: {msg}")
+    out.update(pack("deg_el_", el, ELEM_FIELDS))
+    out.update({"deg_kind": np.array(kind), "deg_msg": np.array(msg)})
+    save("failures.npz", **out)
 
 
 def gold_fracture():

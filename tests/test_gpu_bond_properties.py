@@ -402,7 +402,7 @@ class TestElements:
         n = v.shape[0]
         el = ElementSet(np.zeros((n, 3)), np.asarray(q, float), np.asarray(v, float),
                         np.asarray(qdot, float), np.full(n, mass), np.full(n, radius))
-        scene = Scene("k", el, _no_bonds(), host_sync=False)
+        scene = Scene("k", None, el, _no_bonds(), host_sync=False)
         return _kinetic(scene.device)
 
     def test_rest_state_zero(self, cuda_ok):

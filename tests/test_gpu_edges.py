@@ -17,7 +17,7 @@ def _run_both(el, b, steps, eps=1e-8, colliders=(), k_element=1e6, k_contact=1e6
     from paper_2308_10459_b200 import Scene, SolverConfig, stable_step
     st = O.OracleState(el.copy(), b.copy(), dt, 1e7, colliders=list(colliders),
                        k_contact=k_contact, k_element=k_element, plastic=plastic)
-    scene = Scene("edge", el.copy(), b.copy(), colliders=list(colliders), dt=dt, youngs=1e7,
+    scene = Scene("edge", None, el.copy(), b.copy(), colliders=list(colliders), dt=dt, youngs=1e7,
                   k_contact=k_contact, k_element=k_element, plastic=plastic)
     reps = []
     for _ in range(steps):

@@ -299,27 +299,48 @@ def test_trajectory_vs_golden(cuda_ok, name):
     if name == "stack":
         cols = C.stack().colliders
     plastic = PlasticParams(*d["plastic"]) if "plastic" in d else None
-    scene = Scene(name, el, b, colliders=cols, gravity=d["gravity"], dt=float(d["dt"]),
+    scene = Scene(name, None, el, b, colliders=cols, gravity=d["gravity"], dt=float(d["dt"]),
                   youngs=float(d["youngs"]), k_contact=float(d["k_contact"]),
                   k_element=float(d["k_element"]), plastic=plastic, driver=driver,
                   mu_s=float(d.get("mu_s", 0.0)), mu_r=float(d.get("mu_r", 0.0)))
     cfg = SolverConfig(epsilon=float(d["epsilon"]), max_iterations=300)
-    # rtol 1e-8 with atol >= eps / (min inertia / dt^2) to absorb
-    # Newton-termination differences; rotations use m_q = 1.6 m r^2 (a8)
-    m_dt2 = (el.mass / float(d["dt"]) ** 2).min()
-    mq_dt2 = (1.6 * el.mass * el.radius**2 / float(d["dt"]) ** 2).min()
-    atol_p = max(10 * float(d["epsilon"]) / m_dt2, 1e-12)
-    atol_q = max(10 * float(d["epsilon"]) / mq_dt2, 1e-9)
+    # positions rtol 1e-8 with atol >= eps / (min m / dt^2) to
+    # absorb Newton-termination differences.  Rotations:
+    # * cantilever / plate / cube: q stays exactly identity -- equal;
+    # * rope (twist driver, the rotating config): GPU and reference take the
+    #   same Newton path (same iteration and PCG counts every step), so q is
+    #   held to rtol 1e-8 + atol 1e-10 (q moves 5e-4 per step) and qdot to
+    #   rtol 1e-8 + atol 1e-10 / dt;
+    # * stack (friction, spinning blocks): the Newton path diverges at the
+    #   termination tolerance after a few steps (PCG 105 vs 91 at step 6), so
+    #   the honest bound is eps over the smallest rotational Hessian stiffness
+    #   (bend/twist k_diag + inertia), not the rotational inertia alone.
+    dt = float(d["dt"])
+    eps = float(d["epsilon"])
+    m_dt2 = (el.mass / dt**2).min()
+    atol_p = max(10 * eps / m_dt2, 1e-12)
+    if name == "rope":
+        atol_q, rtol_q = 1e-10, 1e-8
+    elif name == "stack":
+        k_rot = float(np.min(b.k_diag)) + float((1.6 * el.mass * el.radius**2 / dt**2).min())
+        atol_q, rtol_q = 10 * eps / k_rot, 1e-8
+    else:
+        atol_q, rtol_q = 0.0, 0.0
     events = []
+    n_newton = []
     for s in range(d["p"].shape[0]):
         if sched is not None:
             scene.colliders = sched(scene.time + scene.dt)
         rep = stable_step(scene, cfg)
         assert rep.committed == bool(d["committed"][s])
+        n_newton.append(rep.solve.iterations)
         events += [(s, bb) for (bb, _, _) in rep.broken]
         _assert_close(scene.elements.p, d["p"][s], 1e-8, atol_p, f"step {s} p")
-        _assert_close(scene.elements.q, d["q"][s], 1e-8, atol_q, f"step {s} q")
-        _assert_close(scene.elements.v, d["v"][s], 1e-6, atol_p / float(d["dt"]), f"step {s} v")
+        _assert_close(scene.elements.q, d["q"][s], rtol_q, atol_q, f"step {s} q")
+        _assert_close(scene.elements.v, d["v"][s], 1e-6, atol_p / dt, f"step {s} v")
+        _assert_close(scene.elements.qdot, d["qdot"][s], rtol_q, atol_q / dt, f"step {s} qdot")
+    if name in ("cantilever", "rope", "plate", "cube"):
+        assert n_newton == [int(k) for k in d["newton"]]
     assert [tuple(e) for e in events] == [(int(a), int(bb)) for a, bb, _, _ in d["events"]]
     assert np.array_equal(scene.bonds.status, d["final_b_status"])
 
@@ -527,7 +548,7 @@ def test_friction_sweep_vs_golden(cuda_ok):
     d = load("friction.npz")
     el, cols = friction_inputs(d)
     b = C.build_bonds(el.p, el.radius, np.zeros((0, 2), dtype=np.int64), 1e7, 4e6)
-    scene = Scene("friction", el, b, colliders=cols, k_contact=float(d["k_c"]),
+    scene = Scene("friction", None, el, b, colliders=cols, k_contact=float(d["k_c"]),
                   k_element=float(d["k_ec"]), host_sync=False)
     dev = scene.device
     dev.set_physics(scene.gravity, scene.k_contact, scene.k_element, cols)
@@ -571,7 +592,7 @@ def test_friction_large_wave_path_vs_oracle(cuda_ok):
     ref = el.copy()
     O.apply_friction(ref, pairs, cols, 1e5, 1e5, 0.4, 0.1, 1e-4)
     b = C.build_bonds(pos, rad, np.zeros((0, 2), dtype=np.int64), 1e7, 4e6)
-    scene = Scene("cluster", el, b, colliders=cols, k_contact=1e5, k_element=1e5,
+    scene = Scene("cluster", None, el, b, colliders=cols, k_contact=1e5, k_element=1e5,
                   host_sync=False)
     dev = scene.device
     order = np.zeros(pairs.shape[0], dtype=np.int32)

@@ -20,21 +20,14 @@ pytestmark = pytest.mark.gpu
 def _predicted_system(spec, k_element=None):
     import torch
 
-    from paper_2308_10459_b200.newton import GPUProblem
     from paper_2308_10459_b200.scene import Scene
-    from paper_2308_10459_b200.step import contact_candidates
+    from paper_2308_10459_b200.step import prepare_step
     scene = Scene.from_spec(spec, host_sync=False)
     if k_element is not None:
         scene.k_element = k_element
-    dev = scene.device
-    dev.set_physics(scene.gravity, scene.k_contact, scene.k_element, scene.colliders)
-    dev.set_pairs(contact_candidates(scene))
-    dev.call("bdem_predict", dev.sysp, dev.p.data_ptr(), dev.q.data_ptr(), dev.v.data_ptr(),
-             dev.qdot.data_ptr(), dev.p_prev.data_ptr(), dev.q_prev.data_ptr(), spec.dt,
-             dev.p_hat.data_ptr(), dev.q_hat.data_ptr(), dev.mp_dt2.data_ptr(),
-             dev.mq_dt2.data_ptr(), dev.xp.data_ptr(), dev.xq.data_ptr(), dev.stream)
+    prep = prepare_step(scene)            # stable_step's prologue: predictor in xp, xq
     torch.cuda.synchronize()
-    return scene, dev, GPUProblem(dev)
+    return scene, scene.device, prep.problem
 
 
 def _operator_checks(dev, seed):
