@@ -7,28 +7,37 @@ onto a half-space, tilted 10 deg, plasticity/fracture on, dt=5e-6,
 eps=1e-3 (the fp64 gradient noise floor at 600K is ~3e-5 N).
 Synthetic, seeded inputs; no dataset.
 
-A bench "step" is one implicit time step (``stable_step``: broad phase,
-predictor, full manifold Newton solve with PCG and line search, velocity
-update, fracture update, energies).  ``value`` = Newton iterations (all
-ranks) / max-over-ranks device time.  ``e2e`` repeats the measurement through
-the same public call with host buffers (``Scene(host_sync=True)``: host->device
-upload of the element and bond state before, device->host download after,
-every step).  Per-kernel durations (fused bond assembly, every SpMV) are
-taken with CUDA events on the launching stream around every launch of a
-replay of exactly the timed steps (the timed region itself runs the
+A bench "step" is one committed time step of the trajectory, advanced the
+way the reference's runner does it (``runner.advance``, runner.py:47-71): a
+``stable_step`` (broad phase, predictor, manifold Newton solve with PCG and
+line search, velocity update, fracture update, energies) whose solve does
+not commit is replaced by two half steps (recursively, 2 levels) -- the
+plate's Newton iteration cycles at the penalty-contact onset around step 18,
+in the reference as well.  Every timed step therefore
+commits; a step that cannot be committed even at dt/4 aborts the bench.
+``value`` = all Newton iterations performed in the timed region (committed
+solves and the attempts that triggered a split; both are full Newton
+iterations) / max-over-ranks device time; the split-off work and the
+committed-only rate are reported beside it, with per-step Newton / PCG /
+line-search counts.  ``e2e`` repeats the same steps through the same public
+call with host buffers (``Scene(host_sync=True)``: host->device upload of the
+element and bond state before, device->host download after, every
+``stable_step``).  Per-kernel durations (fused bond + element assembly, every
+SpMV) are taken with CUDA events on the launching stream around every launch
+of a replay of exactly the timed steps (the timed region itself runs the
 production path uninstrumented).  ``rot_zero_shortcut`` replays the timed
-steps once more with ``bdem_pcg_set_rot_skip(1)``: on this config the rotation
-half of every Newton system is exactly zero, the PCG kernels skip it, and the
-final state must equal the timed run's bit for bit; it is reported beside the
-full 6-DOF headline, not as it (SURVEY §9 / DESIGN §9).
+steps with ``bdem_pcg_set_rot_skip(1)`` (exact; reported beside the full 6-DOF
+headline, not as it).
 
-``--impl reference`` times the reference's algorithm on the host cores: the
-CPU oracle (``oracle/cpu_oracle.py``, a restatement of the reference pinned to
-its golden vectors; the reference itself is Python and cannot travel) on a
-bounded sample of the same workload -- Newton iterations of the first step of
-a 100x60 crop of the plate -- scaled to 600K-equivalent Newton it/s by the
-bond-count ratio (the reference's per-iteration cost is linear in bonds,
-SURVEY §2/§6).
+``--impl reference`` times the UNMODIFIED reference (``bdem``, shipped to the
+GPU box as bytecode in ``oracle/_ref``; ``oracle/build_ref.py``) on the host
+cores at the same 600K config: K=2 Newton iterations of
+``minimize_second_order`` (solver.py:511-562) on the step-1 problem exactly
+as ``stable_step`` builds it (solver.py:894-908), started (a) from a mid-solve
+iterate -- the first Newton iterate of the GPU step-1 solve whose PCG count
+reaches that solve's average, computed on the GPU during setup, outside the
+timed region -- and (b) from the predictor, each with ``workers=cpu_count``
+and ``workers=1``.  The headline is (a) with ``workers=cpu_count``.
 """
 
 from __future__ import annotations
@@ -64,10 +73,15 @@ def parse():
     ap.add_argument("--no-rot-leg", action="store_true",
                     help="skip the rotation-free (bdem_pcg_set_rot_skip) leg")
     ap.add_argument("--c5-side", type=int, default=126)
-    ap.add_argument("--crop", type=int, nargs=2, default=(100, 60),
-                    help="plate crop for the CPU sample (nx ny)")
-    ap.add_argument("--ref-crop", type=int, nargs=2, default=(60, 36),
-                    help="plate crop of one reference-arm step (nx ny)")
+    ap.add_argument("--ref-plate", type=int, nargs=2, default=None,
+                    help="plate size of the reference measurement (default: --nx --ny)")
+    ap.add_argument("--ref-k", type=int, default=2,
+                    help="Newton iterations per reference measurement (BASELINE.md §3: 2)")
+    ap.add_argument("--ref-starts", type=lambda s: s.split(","),
+                    default=["mid-solve", "predictor"],
+                    help="reference start points, headline first")
+    ap.add_argument("--max-retries", type=int, default=2,
+                    help="dt-halving levels per timed step (runner.py:47-71)")
     return ap.parse_args()
 
 
@@ -82,65 +96,134 @@ def peaks():
 
 
 # ---------------------------------------------------------------------------
-# CPU reference arm (oracle on a bounded crop)
+# the reference on the host cores
 # ---------------------------------------------------------------------------
 
-def cpu_sample(nx, ny, eps, warmup_steps, timed_steps, threads):
-    """The reference algorithm (CPU oracle) on a bounded sample of the same
-    workload: full implicit steps (stable_step) of an nx x ny crop of the
-    plate with the bench's epsilon; `warmup_steps` untimed, then exactly
-    `timed_steps` timed steps (at least one).  Returns (Newton it/s on the
-    crop, crop bonds, iterations, PCG per iteration, seconds, steps)."""
-    from threadpoolctl import threadpool_limits
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
-    from oracle import cpu_oracle as O
+
+def gpu_mid_iterate(spec, eps):
+    """Setup for the mid-solve start (outside any timed region): the step-1
+    Newton solve on the GPU, its per-iteration PCG counts, and the iterate at
+    the start of the first Newton iteration whose PCG count reaches the
+    solve's average.  Returns (p, q, info) or None without
+    a GPU."""
+    import torch
+    if not torch.cuda.is_available():
+        return None
+    from paper_2308_10459_b200 import SolverConfig
+    from paper_2308_10459_b200.newton import GPUProblem, minimize_second_order
+    from paper_2308_10459_b200.scene import Scene
+    from paper_2308_10459_b200.step import prepare_step
+    scene = Scene.from_spec(spec, host_sync=False)
+    prep = prepare_step(scene)
+    seen = []
+
+    class Capture(GPUProblem):
+        def assemble(self, p, q):
+            seen.append((p.cpu().numpy(), q.cpu().numpy()))
+            return super().assemble(p, q)
+
+    sol = minimize_second_order(Capture(prep.problem.dev), scene.device.xp, scene.device.xq,
+                                SolverConfig(epsilon=eps, max_iterations=300))
+    pcg = [r.pcg_iterations for r in sol.records if r.pcg_iterations > 0]
+    avg = sum(pcg) / max(len(pcg), 1)
+    k = next((i for i, c in enumerate(pcg) if c >= avg), len(pcg) - 1)
+    p, q = seen[k]
+    info = {"gpu_step1_newton": len(pcg), "gpu_step1_pcg": pcg, "gpu_step1_pcg_avg": avg,
+            "start_iteration": k, "gpu_pcg_at_start": pcg[k]}
+    del scene, prep, seen
+    torch.cuda.empty_cache()
+    return p, q, info
+
+
+def reference_newton(nx, ny, eps, k_iters, starts, workers, mid=None):
+    """K Newton iterations of the UNMODIFIED reference minimize_second_order
+    (solver.py:511-562) on the step-1 problem of the nx x ny plate, built as
+    stable_step builds it (solver.py:894-908), for every (start, workers).
+    Returns (kind, runs, setup info)."""
+    from oracle import build_ref
+    from oracle import ref_adapter as RA
     from paper_2308_10459_b200 import configs as C
+    bdem = build_ref.load()
+    if bdem is None:
+        raise RuntimeError("reference bdem unavailable: run __graft_entry__.build() where "
+                           "/root/reference exists (it writes oracle/_ref)")
+    from bdem import solver as rsv
+    import logging
+    logging.getLogger("bdem").setLevel(logging.ERROR)
     spec = C.plate(nx=nx, ny=ny, epsilon=eps)
-    st = O.OracleState(spec.elements.copy(), spec.bonds.copy(), spec.dt, spec.youngs,
-                       colliders=spec.colliders, gravity=spec.gravity,
-                       k_contact=spec.k_contact, k_element=spec.k_element, plastic=spec.plastic)
-    cfg = O.Config(epsilon=eps, max_iterations=300)
-    with threadpool_limits(limits=threads):
-        for _ in range(warmup_steps):
-            O.step(st, cfg)
-        its = pcg = steps = 0
-        t0 = time.perf_counter()
-        while steps < max(timed_steps, 1):
-            out = O.step(st, cfg)
-            its += out.solve.iterations
-            pcg += out.solve.pcg_total
-            steps += 1
-        dt = time.perf_counter() - t0
-    its = max(its, 1)
-    return its / dt, spec.bonds.n, its, pcg / its, dt, steps
+    t0 = time.perf_counter()
+    sc = RA.ref_scene(bdem, spec)
+    prob, p0, q0, pairs = RA.step_problem(bdem, sc)
+    setup = {"scene_and_step_problem_s": time.perf_counter() - t0, "bonds": int(sc.bonds.n),
+             "spheres": int(sc.elements.n), "contact_pairs": int(pairs.shape[0])}
+    start_pts = {"predictor": (p0, q0)}
+    if mid is not None:
+        start_pts["mid-solve"] = (mid[0], mid[1])
+    runs = []
+    for name in starts:
+        if name not in start_pts:
+            continue
+        p, q = start_pts[name]
+        for w in workers:
+            cfg = rsv.SolverConfig(epsilon=eps, max_iterations=k_iters, workers=w)
+            t = time.perf_counter()
+            sol = rsv.minimize_second_order(prob, p, q, cfg)
+            sec = time.perf_counter() - t
+            its = [r for r in sol.records if r.pcg_iterations > 0 or r.alpha > 0]
+            n_it = max(len(its), 1)
+            runs.append({"start": name, "workers": w, "newton_iterations": len(its),
+                         "seconds": sec, "newton_per_s": n_it / sec,
+                         "pcg_per_iteration": [r.pcg_iterations for r in its],
+                         "grad_norm": [r.grad_norm for r in its], "reason": sol.reason})
+    return "reference", runs, setup
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from paper_2308_10459_b200 import configs as C
-    nb_full = 3_591_004 if (args.nx, args.ny) == (1000, 600) else \
-        C.plate(nx=args.nx, ny=args.ny).bonds.n
     cores = os.cpu_count() or 1
-    rate, nb_crop, its, pcg, sec, steps = cpu_sample(
-        args.ref_crop[0], args.ref_crop[1], args.epsilon, args.warmup, args.steps, cores)
-    value = rate * nb_crop / nb_full
-    sample = (f"oracle (numpy/scipy, {cores} threads): each step one implicit step of a "
-              f"{args.ref_crop[0]}x{args.ref_crop[1]} crop of the plate ({nb_crop} bonds); {steps} "
-              f"timed after {args.warmup} warm-up: {its} Newton iterations, {pcg:.1f} PCG/it, "
-              f"{sec:.1f}s; scaled by bonds {nb_crop}/{nb_full}")
+    nx, ny = args.ref_plate if args.ref_plate else (args.nx, args.ny)
+    workers = sorted({cores, 1}, reverse=True)
+    mid = gpu_mid_iterate(__import__("paper_2308_10459_b200.configs", fromlist=["plate"])
+                          .plate(nx=nx, ny=ny, epsilon=args.epsilon), args.epsilon) \
+        if "mid-solve" in args.ref_starts else None
+    kind, runs, setup = reference_newton(nx, ny, args.epsilon, args.ref_k, args.ref_starts,
+                                         workers, mid)
+    head = runs[0]
+    value = head["newton_per_s"]
+    timed_s = sum(r["seconds"] for r in runs)
+    sample = (f"reference bdem (oracle/_ref bytecode, numpy/scipy) on {cpu_model()}: "
+              f"{head['newton_iterations']} Newton iterations of minimize_second_order on the "
+              f"{nx}x{ny} plate's step-1 problem from the {head['start']} start, "
+              f"workers={head['workers']} ({head['seconds']:.1f}s, PCG "
+              f"{head['pcg_per_iteration']})")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
-        # the sample's wall time per step scaled by the bond ratio (the
-        # crop's steps take fewer Newton iterations than the plate's)
-        "ms_per_step": 1e3 * sec / max(steps, 1) * nb_full / nb_crop,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        # one 600K Newton iteration of the reference takes minutes on the host:
+        # the timed region is the headline measurement, spread over the
+        # requested step count so ms_per_step x steps is its real duration
+        "ms_per_step": 1e3 * head["seconds"] / max(args.steps, 1),
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_block(args), "pcg_per_newton": pcg,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": sample},
+        "config": config_block(args),
+        "pcg_per_newton": sum(head["pcg_per_iteration"]) / max(head["newton_iterations"], 1),
+        "measurements": runs, "setup": setup, "mid_start": (mid[2] if mid else None),
+        "all_measurements_s": timed_s, "cpu_model": cpu_model(),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": int(head["workers"]),
+                         "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -307,10 +390,12 @@ def spmv_bytes(dev):
 
 
 def assembly_bytes(dev):
-    """Algorithmic bytes of one fused bond-assembly launch: per bond 161 B in
-    (i, j, status, 18 geometry fp64, scale) + 288 B staged out (36 fp64); per
-    element the gathered p, q rows once (56 B)."""
-    return dev.nb * (161 + 288) + dev.n * 56
+    """SURVEY §8(d)'s algorithmic bytes of one assembly (bond + element
+    kernels) per Newton iteration: per bond 161 B in (i, j, status, l0, d0,
+    frame, kn, kt, k_diag, scale) + 288 B out (the two off-diagonal 18-value
+    blocks); per free element 136 B in (p, q, p_hat, q_hat, m, r, pinned),
+    144 B diagonal, 144 B block-Jacobi inverse, 48 B z, 56 B gp + gq."""
+    return dev.nb * (161 + 288) + dev.nf * (136 + 144 + 144 + 48 + 56)
 
 
 # Chip-wide L2-slice (LTS) throughput cap per SM clock, measured on the
@@ -352,6 +437,35 @@ def load_ncu_traffic():
         return {}
 
 
+def _timed_steps(scene, cfg, steps, max_retries, record=None):
+    """``steps`` committed steps through runner.advance; returns the
+    per-step records (every attempt's Newton / PCG / line-search counts)."""
+    from paper_2308_10459_b200.runner import advance
+    per_step = []
+    for _ in range(steps):
+        attempts = []
+        committed = advance(scene, cfg, max_retries=max_retries, attempts=attempts)
+        per_step.append({
+            "newton": [a.solve.iterations for a in attempts],
+            "pcg": [a.solve.pcg_total for a in attempts],
+            "ls": [sum(r.ls_trials for r in a.solve.records) for a in attempts],
+            "committed": [bool(a.committed) for a in attempts],
+            "substeps": len(committed), "broken": sum(len(c.broken) for c in committed),
+            "pairs": max(c.contact_pairs for c in committed)})
+    return per_step
+
+
+def _totals(per_step):
+    flat = lambda key: [x for s in per_step for x in s[key]]  # noqa: E731
+    newton, pcg, ls, ok = flat("newton"), flat("pcg"), flat("ls"), flat("committed")
+    return {"newton": sum(newton), "pcg": sum(pcg), "ls": sum(ls),
+            "newton_committed": sum(n for n, c in zip(newton, ok) if c),
+            "newton_split_off": sum(n for n, c in zip(newton, ok) if not c),
+            "attempts": len(newton), "failed_attempts": ok.count(False),
+            "broken": sum(s["broken"] for s in per_step),
+            "pairs": max((s["pairs"] for s in per_step), default=0)}
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -364,7 +478,7 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl")
 
-    from paper_2308_10459_b200 import SolverConfig, configs, stable_step
+    from paper_2308_10459_b200 import SolverConfig, configs
     from paper_2308_10459_b200 import _lib as L
     from paper_2308_10459_b200.scene import Scene
     from paper_2308_10459_b200.timing import KernelTimer
@@ -381,69 +495,53 @@ def run_ours(args):
             dist.barrier()
             torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        stable_step(scene, cfg)
-    snap = snapshot(scene)      # the e2e leg replays exactly the timed steps
+    _timed_steps(scene, cfg, args.warmup, args.max_retries)
+    snap = snapshot(scene)      # the replays below run exactly the timed steps
 
-    stats = {"newton": 0, "pcg": 0, "ls": 0, "committed": 0, "broken": 0, "pairs": 0}
     barrier()
     launches0 = lib.bdem_launch_count()
     with ClockSampler(local) as clocks:
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()
-        for _ in range(args.steps):
-            rep = stable_step(scene, cfg)
-            stats["newton"] += rep.solve.iterations
-            stats["pcg"] += rep.solve.pcg_total
-            stats["ls"] += sum(r.ls_trials for r in rep.solve.records)
-            stats["committed"] += int(rep.committed)
-            stats["broken"] += len(rep.broken)
-            stats["pairs"] = max(stats["pairs"], rep.contact_pairs)
+        per_step = _timed_steps(scene, cfg, args.steps, args.max_retries)
         t1.record()
         barrier()
     launches = lib.bdem_launch_count() - launches0
     ms = t0.elapsed_time(t1)
+    tot = _totals(per_step)
     final = snapshot(scene)     # the rotation-free leg must reproduce it bit for bit
 
     # kernel timing: the timed region runs the production path uninstrumented;
     # the same steps are replayed from the snapshot with CUDA events around
-    # every SpMV and bond-assembly launch (same kernels, same inputs)
+    # every SpMV and assembly launch (same kernels, same inputs)
     restore(scene, snap)
     scene.host_sync = True
     timer = KernelTimer()
     dev.timer = timer
-    replay_newton = 0
-    for _ in range(args.steps):
-        replay_newton += stable_step(scene, cfg).solve.iterations
+    replay = _totals(_timed_steps(scene, cfg, args.steps, args.max_retries))
     torch.cuda.synchronize()
     durations = timer.resolve()
     dev.timer = None
 
     # e2e: the same steps again, from the same state, through the same public
-    # call with host buffers every step (H2D of the state before, D2H after)
+    # call with host buffers every stable_step (H2D of the state before, D2H after)
     n_e2e = args.e2e_steps if args.e2e_steps is not None else args.steps
     restore(scene, snap)
     scene.host_sync = True
-    e2e_newton = 0
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(n_e2e):
-        rep = stable_step(scene, cfg)
-        e2e_newton += rep.solve.iterations
+    e2e = _totals(_timed_steps(scene, cfg, n_e2e, args.max_retries))
     e1.record()
     barrier()
     e2e_ms = e0.elapsed_time(e1)
     h2d = dev.n * (3 + 4 + 3 + 4 + 3 + 4) * 8 + dev.nb * (5 * 8 + 1)
     d2h = h2d
 
-    # rotation-free leg (SURVEY 8(f)'s exact shortcut, reported separately):
+    # rotation-free leg (SURVEY §0.5's exact shortcut, reported separately):
     # the same timed steps from the same snapshot with bdem_pcg_set_rot_skip(1)
-    # -- on this config the rotation half of every Newton system is exactly
-    # zero (identity orientations, centre-based contact), so the PCG kernels
-    # skip it; the headline `value` above runs the full 6-DOF path
     rot = None
     if not args.no_rot_leg:
         prev = lib.bdem_pcg_set_rot_skip(1)
@@ -451,15 +549,11 @@ def run_ours(args):
         scene.host_sync = False
         dev.upload_elements(scene.elements, scene.p_prev, scene.q_prev)
         dev.upload_bond_state(scene.bonds)
-        rot_newton = rot_pcg = 0
         barrier()
         r0 = torch.cuda.Event(enable_timing=True)
         r1 = torch.cuda.Event(enable_timing=True)
         r0.record()
-        for _ in range(args.steps):
-            rep = stable_step(scene, cfg)
-            rot_newton += rep.solve.iterations
-            rot_pcg += rep.solve.pcg_total
+        rt = _totals(_timed_steps(scene, cfg, args.steps, args.max_retries))
         r1.record()
         barrier()
         rot_ms = r0.elapsed_time(r1)
@@ -468,21 +562,23 @@ def run_ours(args):
         scene.sync_to_host()
         same = all(np.array_equal(getattr(scene.elements, k), getattr(final["el"], k))
                    for k in ("p", "q", "v", "qdot"))
-        rot = {"value": rot_newton / (rot_ms * 1e-3), "unit": UNIT,
-               "ms_per_step": rot_ms / args.steps, "newton_iterations": rot_newton,
-               "pcg_per_newton": rot_pcg / max(rot_newton, 1),
+        rot = {"value": rt["newton_committed"] / (rot_ms * 1e-3), "unit": UNIT,
+               "ms_per_step": rot_ms / args.steps, "newton_iterations": rt["newton"],
+               "newton_committed": rt["newton_committed"],
+               "pcg_per_newton": rt["pcg"] / max(rt["newton"], 1),
                "rotation_half_skipped": skipped, "bit_identical_final_state": bool(same),
                "note": "bdem_pcg_set_rot_skip(1): the rotation half of every Newton "
                        "system is exactly zero on this config, so the PCG kernels skip it "
                        "(exact; reported separately from the full 6-DOF headline)"}
 
-    (ms_max, e2e_ms_max), (newton_all, e2e_newton_all) = reduce_across_ranks(
-        [ms, e2e_ms], [stats["newton"], e2e_newton], world, "cuda")
+    # headline work = Newton iterations of COMMITTED solves; the time also
+    # covers the attempts that were split (their iterations are reported beside)
+    (ms_max, e2e_ms_max), (newton_all, e2e_newton_all, newton_any) = reduce_across_ranks(
+        [ms, e2e_ms], [tot["newton_committed"], e2e["newton_committed"], tot["newton"]],
+        world, "cuda")
     if rot is not None and world > 1:
-        # whole-job figure like the headline: all ranks' Newton iterations
-        # over the slowest rank's time
         (rot_ms_max,), (rot_newton_all, same_all) = reduce_across_ranks(
-            [rot["ms_per_step"] * args.steps], [rot["newton_iterations"],
+            [rot["ms_per_step"] * args.steps], [rot["newton_committed"],
                                                 float(rot["bit_identical_final_state"])],
             world, "cuda")
         rot["value"] = rot_newton_all / (rot_ms_max * 1e-3)
@@ -494,9 +590,12 @@ def run_ours(args):
 
     peak, peak_kind = peaks()
     spmv = durations.get("spmv", [])
-    asm = durations.get("bond_assemble", [])
+    basm = durations.get("bond_assemble", [])
+    easm = durations.get("element_assemble", [])
     spmv_ms = statistics.mean(spmv) if spmv else float("nan")
-    asm_ms = statistics.mean(asm) if asm else float("nan")
+    basm_ms = statistics.mean(basm) if basm else float("nan")
+    easm_ms = statistics.mean(easm) if easm else float("nan")
+    asm_ms = basm_ms + easm_ms
     sb = spmv_bytes(dev)
     ab = assembly_bytes(dev)
     achieved = sb / (spmv_ms * 1e-3) / 1e9
@@ -508,25 +607,38 @@ def run_ours(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, paper_2308_10459_b200/configs.py)",
         "config": config_block(args),
-        "newton_iterations": stats["newton"], "pcg_per_newton": stats["pcg"] / max(stats["newton"], 1),
-        "ls_trials_per_newton": stats["ls"] / max(stats["newton"], 1),
-        "committed_steps": stats["committed"], "broken_bonds": stats["broken"],
+        "value_counts": "Newton iterations of committed solves only; the timed region also "
+                        "contains the split attempts (all_attempts_newton_per_s counts them)",
+        "newton_iterations": tot["newton"],
+        "newton_committed": tot["newton_committed"],
+        "newton_in_split_attempts": tot["newton_split_off"],
+        "all_attempts_newton_per_s": newton_any / (ms_max * 1e-3),
+        "attempts": tot["attempts"], "split_attempts": tot["failed_attempts"],
+        "every_step_committed": True,
+        "pcg_per_newton": tot["pcg"] / max(tot["newton"], 1),
+        "ls_trials_per_newton": tot["ls"] / max(tot["newton"], 1),
+        "per_step": per_step, "broken_bonds": tot["broken"],
         "bonds_per_sec_assembled": dev.nb / (asm_ms * 1e-3),
-        "assembly": {"ms": asm_ms, "launches": len(asm), "bytes": ab,
+        "assembly": {"ms": asm_ms, "bond_kernel_ms": basm_ms, "element_kernel_ms": easm_ms,
+                     "launches": len(basm), "bytes": ab,
+                     "bytes_rule": "SURVEY 8(d): n_b (161 + 288) + n_f (136+144+144+48+56)",
                      "achieved_gbs": ab / (asm_ms * 1e-3) / 1e9,
                      "frac": ab / (asm_ms * 1e-3) / 1e9 / peak},
         "spmv": {"ms": spmv_ms, "launches": len(spmv), "bytes": sb, "achieved_gbs": achieved,
                  "timing": "CUDA events around every SpMV launch in a replay of the timed steps "
                            "(the timed region itself runs uninstrumented)",
-                 "replay_newton_iterations": replay_newton},
+                 "replay_newton_iterations": replay["newton"]},
         "roofline": {"kernel": "bdem::k_spmv (PCG SpMV)", "bound": "hbm", "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": peak_kind,
                      "traffic": traffic.get("k_spmv", {}).get("dram_bytes_per_launch"),
                      "l2": l2_roofline(traffic.get("k_spmv", {}), spmv_ms, clocks)},
         "e2e": {"value": e2e_newton_all / (e2e_ms_max * 1e-3) if n_e2e else None, "unit": UNIT,
-                "same_steps_as_value": True, "newton_iterations": e2e_newton,
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n_e2e},
+                "same_steps_as_value": n_e2e == args.steps,
+                "newton_committed": e2e["newton_committed"],
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n_e2e,
+                "note": "h2d/d2h bytes per stable_step call (a step split in halves makes "
+                        "several calls)"},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
     }
@@ -535,15 +647,21 @@ def run_ours(args):
     if not args.no_c5:
         line["c5_block"] = c5_leg(args.c5_side, peak)
     if not args.no_cpu_baseline and world == 1:
-        rate, nb_crop, its, pcg, sec, steps = cpu_sample(args.crop[0], args.crop[1],
-                                                         args.epsilon, 0, 1, 1)
+        cores = os.cpu_count() or 1
+        # a fresh copy of the inputs: the scene above mutated spec's arrays
+        mid = gpu_mid_iterate(configs.plate(nx=args.nx, ny=args.ny, epsilon=args.epsilon),
+                              args.epsilon)
+        kind, runs, setup = reference_newton(args.nx, args.ny, args.epsilon, 1, ["mid-solve"],
+                                             [cores], mid)
+        r = runs[0]
         line["cpu_baseline"] = {
-            "value": rate * nb_crop / dev.nb, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": (f"oracle (numpy/scipy, 1 thread): step 1 of a {args.crop[0]}x"
-                       f"{args.crop[1]} crop of the plate ({nb_crop} bonds), {its} Newton "
-                       f"iterations, {pcg:.1f} PCG/it, {sec:.1f}s; scaled by bonds "
-                       f"{nb_crop}/{dev.nb} (PCG counts grow with size, so this favours "
-                       f"the CPU)")}
+            "value": r["newton_per_s"], "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": (f"reference bdem (oracle/_ref bytecode) on {cpu_model()}: "
+                       f"{r['newton_iterations']} Newton iteration of minimize_second_order on "
+                       f"this 600K plate's step-1 problem from the GPU mid-solve iterate "
+                       f"(iteration {mid[2]['start_iteration']} of {mid[2]['gpu_step1_newton']}), "
+                       f"workers={cores}: {r['seconds']:.1f}s, PCG {r['pcg_per_iteration']}"),
+            "setup": setup}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -1,16 +1,20 @@
-"""The reference ``bdem`` package as a checker (tests only).
+"""The reference ``bdem`` package as a checker and CPU baseline.
+
+TEST / MEASUREMENT INFRASTRUCTURE ONLY: imported by ``tests/`` and by
+``bench.py``'s reference / cpu_baseline legs, never by the product path.
 
 ``oracle.build_ref.load()`` imports the unmodified reference: its bytecode
 build under ``oracle/_ref`` (travels to the GPU box) or, in the build
 container, the sources under ``/root/reference``.  The helpers turn the
 shared seeded generator's arrays (``paper_2308_10459_b200.configs``) into
-reference objects, like ``tests/golden/make_golden.py`` does.
+reference objects, like ``tests/golden/make_golden.py`` does, and build the
+step-1 ``ImplicitProblem`` exactly as ``stable_step`` does
+(``solver.py:894-908``).
 """
 
 from __future__ import annotations
 
 import numpy as np
-import pytest
 
 from oracle import build_ref
 
@@ -22,6 +26,7 @@ ELEM_FIELDS = ("p", "q", "v", "qdot", "mass", "radius", "pinned")
 
 
 def bdem_or_skip():
+    import pytest
     mod = build_ref.load()
     if mod is None:
         pytest.skip("reference bdem unavailable (run build() where /root/reference exists)")
@@ -69,3 +74,21 @@ def ref_scene(bdem, spec):
                     k_contact=spec.k_contact, k_element=spec.k_element, plastic=spec.plastic,
                     driver=ref_driver(bdem, spec), mu_s=spec.mu_s, mu_r=spec.mu_r,
                     surface_flags=np.zeros(el.n, dtype=bool))
+
+
+def step_problem(bdem, sc):
+    """The step-1 problem of ``stable_step`` (solver.py:894-908): driver rows
+    at t + dt, the step context, frozen contact candidates, the potential and
+    ``ImplicitProblem``; returns (problem, p0, q0, pairs)."""
+    from bdem import integrator as ri
+    from bdem import solver as rsv
+    el = sc.elements
+    if sc.driver is not None:
+        sc.driver(el, sc.time + sc.dt)
+    ctx = ri.StepContext(sc.dt, sc.p_prev.copy(), sc.q_prev.copy(), el.p.copy(), el.q.copy())
+    pairs = rsv.contact_candidates(sc)
+    model = ri.PotentialModel(el, sc.bonds, pairs, sc.colliders, sc.gravity, sc.k_contact,
+                              sc.k_element)
+    prob = ri.ImplicitProblem(model, ctx)
+    p0, q0 = ri.predict_state(ctx, el.v, el.qdot, prob.free)
+    return prob, p0, q0, pairs

@@ -118,7 +118,12 @@ class GPUProblem:
                 tm.end("bond_assemble")
         if d.n_pair:
             d.call("bdem_pair_assemble", s, p.data_ptr(), 0, st)
+        tm = self.timer
+        if tm is not None:
+            tm.begin("element_assemble")
         d.call("bdem_element_assemble", s, p.data_ptr(), q.data_ptr(), d.z.data_ptr(), st)
+        if tm is not None:
+            tm.end("element_assemble")
         d.call("bdem_reduce_finish", s, 0, 7, L.RED_BLOCKS, st)
         d.eval_pq = (p, q)
         sc = d.read_scalars()

@@ -19,7 +19,7 @@ import pytest
 
 from paper_2308_10459_b200 import configs as C
 from _fixtures import close
-from _reference import bdem_or_skip, ref_scene
+from oracle.ref_adapter import bdem_or_skip, ref_scene
 
 pytestmark = pytest.mark.gpu
 
