@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define BDEM_ABI_VERSION 3
+#define BDEM_ABI_VERSION 4
 
 enum {
   BDEM_OK = 0,
@@ -195,33 +195,6 @@ typedef struct {
   const int32_t *elem_row;       /* (n_elem) row of an element          */
   const int32_t *slice_slot;     /* (n_slices + 1) first free slot of a slice */
   const int32_t *row_slot;       /* (n_slices * 32) free slot of a row, -1 pinned/pad */
-  /* contribution-table SpMV (bdem_spmv_set_kernel(2)): tiles of
-   * bdem_spmv_sym_slices() slices; a bond whose rows share a tile is read once
-   * and hands row j its product through a per-tile shared-memory table */
-  const int32_t *sym_jloc;       /* (n_bond) table slot k*R + (row_j - tile_row0), -1 boundary */
-  const int32_t *sym_jbase;      /* (n_slices + 1) boundary-only j-role lists, SELL shape */
-  const int32_t *sym_jpos, *sym_jslot;
-  int64_t sym_kc;                /* table depth (max in-tile j-role bonds of a row) */
-  /* dataflow SpMV (bdem_spmv_set_kernel(3)): needs row(i) < row(j) for every
-   * bond.  wave_jring[jk] = ring slot of j-role entry jk's product written by
-   * the i-role pass, -1 none; wave_lag = max slice(j) - slice(i) (-1: variant
-   * unavailable); ring of wave_ring_slices slices x sell_kmax slots x 32 */
-  const int32_t *wave_jring;
-  int64_t wave_lag, wave_ring_slices;
-  double *wave_ring;             /* 6 planes x wave_ring_slices * sell_kmax * 32 */
-  double *wave_ypart;            /* 6 planes x vstride: rows' i-role sums */
-  int32_t *wave_flags;           /* 2 x n_slices epoch stamps (A done, B done) + ticket */
-  /* warp-shuffle SpMV (bdem_spmv_set_kernel(4)): a bond whose two rows share
-   * a slice hands row j its product -a+ x_i, C^T x_i through a warp shuffle
-   * at its i-role slot.  shfl_src[pos] = sending lane for the RECEIVING lane
-   * (pos & 31) at that slot, -1 none (at most one sender per receiver and
-   * slot; the rest stay in the lists); shfl_jbase/jpos/jslot: the j-role
-   * lists without the handed-over bonds, SELL shape */
-  const int8_t *shfl_src;
-  const int32_t *shfl_jbase, *shfl_jpos, *shfl_jslot;
-  const int32_t *tile_hdr;       /* per SpMV tile (bdem_spmv_tile_slices() slices):
-                                    BDEM_TILE_HDR ints = slice_base[t0..t0+TS],
-                                    jslice_base[t0..t0+TS], slice_slot[t0], slice_slot[t1] */
   /* contact pairs (sorted i<j); pairs with i == e are [pi_ptr[e], pi_ptr[e+1]),
    * pairs with j == e are pj_idx[pj_ptr[e] .. pj_ptr[e+1]) ascending */
   const int32_t *pair_i, *pair_j, *pi_ptr, *pj_ptr, *pj_idx;
@@ -355,15 +328,6 @@ int bdem_finish_step(const bdem_system_t *sys, const double *p, const double *q,
  * solver.py:198-258, applied as `mat @ v`, solver.py:475).  Also writes the
  * per-block partials of x.y, |y|^2, |x|^2 for PCG. */
 int bdem_spmv(const bdem_system_t *sys, const double *x, double *y, void *stream);
-/* SpMV kernel variant for every later SpMV launch: 0 = slot-parallel
- * (default), 1 = tiled (cp.async.bulk + mbarrier ring, warp-specialised
- * producer; pays off only with compact tiles, BDEM_ROW_ORDER=z), 2 =
- * contribution table (BDEM_ROW_ORDER=strip), 3 = dataflow ring, 4 =
- * slot-parallel with in-slice hand-over by warp shuffle (compact slices:
- * BDEM_ROW_ORDER=strip8 or z).  Returns the
- * previous variant; any other value only queries.  BDEM_SPMV_TILE=1 in the
- * environment selects the tiled one at load time. */
-int bdem_spmv_set_kernel(int kernel);
 /* PCG update path of bdem_pcg_iterate: 0 = k_pcg_update + k_pcg_pupdate
  * (default), 1 = one fused kernel over a co-resident grid (grid barrier
  * between the r/z and the x/p halves; bit-identical iterates; used only when
@@ -379,13 +343,6 @@ int bdem_pcg_set_fused(int on);
  * (up to the sign of zeros).  Default off; BDEM_ROT_SKIP=1 selects it at load
  * time.  Returns the previous setting; any other value only queries. */
 int bdem_pcg_set_rot_skip(int on);
-/* Slices per tile of the tiled SpMV and the int32 stride of sys->tile_hdr. */
-int bdem_spmv_tile_slices(void);
-int bdem_spmv_tile_hdr_ints(void);
-/* Slices per tile of the contribution-table SpMV and its table-depth cap. */
-int bdem_spmv_sym_slices(void);
-int bdem_spmv_sym_kcap(void);
-
 /* PCG (linalg.py:40-97) on device state sys->pcg; see pcg_kernels.cu. */
 int bdem_pcg_init(const bdem_system_t *sys, const double *b, double sign, double *x,
                   double *r, double *zv, double *pv, double tol, int max_iter, double boost,

@@ -28,7 +28,7 @@ SC = dict(F=0, GNORM2=1, CNORM2=2, MAXDEV=3, SLOPE=4, FT=5, NSING=6, EBOND=7, EC
 PCG = dict(RZ=0, PAP=1, ALPHA=2, BETA=3, RR=4, BNORM=5, REL=6, TOL=7, BOOST=8, APNORM2=9,
            PNORM2=10, K=11, MAXIT=12, STATE=13, ROTZERO=14, COUNT=16)
 PCG_RUNNING, PCG_CONVERGED, PCG_BREAKDOWN, PCG_MAXIT = 0, 1, 2, 3
-ABI_VERSION = 3
+ABI_VERSION = 4
 RED_BLOCKS = 1184
 MAX_COLLIDERS = 8
 N_COUNTERS = 16
@@ -50,11 +50,6 @@ class System(C.Structure):
         ("bond_i", _p), ("bond_j", _p), ("status", _p), ("geom", _p), ("bstate", _p),
         ("slice_base", _p), ("pos_oslot", _p), ("jslice_base", _p), ("jpos", _p), ("jslot", _p),
         ("row_elem", _p), ("elem_row", _p), ("slice_slot", _p), ("row_slot", _p),
-        ("sym_jloc", _p), ("sym_jbase", _p), ("sym_jpos", _p), ("sym_jslot", _p),
-        ("sym_kc", C.c_int64), ("wave_jring", _p), ("wave_lag", C.c_int64),
-        ("wave_ring_slices", C.c_int64), ("wave_ring", _p), ("wave_ypart", _p),
-        ("wave_flags", _p), ("shfl_src", _p), ("shfl_jbase", _p), ("shfl_jpos", _p),
-        ("shfl_jslot", _p), ("tile_hdr", _p),
         ("pair_i", _p), ("pair_j", _p), ("pi_ptr", _p), ("pj_ptr", _p), ("pj_idx", _p),
         ("stage", _p), ("scoef", _p), ("pstage", _p), ("diag", _p), ("minv", _p), ("red", _p),
         ("scalars", _p), ("pcg", _p), ("err", _p), ("counter", _p), ("clamp_list", _p),
@@ -102,13 +97,8 @@ SIGNATURES = {
     "bdem_components": (_int, [_i64, _i64, _p, _p, _p, _p, _p, C.POINTER(C.c_int64), _p]),
     "bdem_select_workspace": (_i64, [_i64]),
     "bdem_select_flagged": (_int, [_p, _i64, _p, _p, C.POINTER(C.c_int64), _p]),
-    "bdem_spmv_set_kernel": (_int, [_int]),
     "bdem_pcg_set_fused": (_int, [_int]),
     "bdem_pcg_set_rot_skip": (_int, [_int]),
-    "bdem_spmv_tile_slices": (_int, []),
-    "bdem_spmv_sym_slices": (_int, []),
-    "bdem_spmv_sym_kcap": (_int, []),
-    "bdem_spmv_tile_hdr_ints": (_int, []),
     "bdem_friction_workspace": (_i64, [_i64, _i64]),
     "bdem_friction": (_int, [_p, _p, _p, _p, _p, _dbl, _dbl, _dbl, _p, C.POINTER(C.c_int64), _p]),
     "bdem_friction_schedule": (_i64, [_p, _i64, _i64, _p, _p]),

@@ -415,110 +415,6 @@ __global__ void __launch_bounds__(kSpmvThreads, BDEM_SPMV_MINB) k_spmv(bdem_syst
   TL_EXIT(0, tl_it)
 }
 
-// ---------------------------------------------------------------------------
-// SpMV variant 4: slot-parallel as k_spmv, plus in-slice hand-over.  At an
-// i-role slot every lane also forms the transposed product of its bond for
-// row j, t = -a+ x_i (+) C^T x_i, from its OWN row's x; the lane of row j
-// takes it with a warp shuffle when the host marked it as the receiver
-// (shfl_src).  Such a bond's coefficients and x_i are therefore read once
-// instead of twice (no j-role re-read from L2, no x_i gather); the j-role
-// lists hold only the remaining bonds.  Same terms per row as k_spmv in a
-// different (fixed) order: deterministic, equal to round-off.
-// ---------------------------------------------------------------------------
-#ifndef BDEM_SHFL_MINB
-#define BDEM_SHFL_MINB 6
-#endif
-__global__ void __launch_bounds__(kSpmvThreads, BDEM_SHFL_MINB)
-    k_spmv_shfl(bdem_system_t S, const double *x, double *y, int mode) {
-  __shared__ double part[kSpmvWarps][6][32];
-  __shared__ double sh[kSpmvThreads / 32];
-  griddep_wait();
-  double *pcg = S.pcg;
-  if (mode == 1 && pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
-  const double boost = mode == 1 ? pcg[BDEM_PCG_BOOST] : 0.0;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t nf = S.vstride;
-  const int ns = (int)((S.n_elem + 31) >> 5);
-  double acc_xy = 0.0, acc_yy = 0.0, acc_xx = 0.0;
-#pragma unroll 1
-  for (int sl = blockIdx.x; sl < ns; sl += gridDim.x) {
-    const int a0 = __ldg(S.slice_base + sl), a1 = __ldg(S.slice_base + sl + 1);
-    const int c0 = __ldg(S.shfl_jbase + sl), c1 = __ldg(S.shfl_jbase + sl + 1);
-    const int ki = (a1 - a0) >> 5, kj = (c1 - c0) >> 5;
-    const int own = __ldg(S.row_slot + (int64_t)sl * 32 + lane);
-    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    // i-role slots with hand-over (warp-uniform trip count: shuffles); the
-    // next slot's indices are in flight while this slot's data arrive
-    int o_n = -1, src_n = -1;
-    if (w < ki) {
-      o_n = __ldg(S.pos_oslot + a0 + 32 * w + lane);
-      src_n = __ldg(S.shfl_src + a0 + 32 * w + lane);
-    }
-#pragma unroll 1
-    for (int k = w; k < ki; k += kSpmvWarps) {
-      const int64_t b = a0 + 32 * k + lane;
-      const int o = o_n, src = src_n;
-      if (k + kSpmvWarps < ki) {
-        o_n = __ldg(S.pos_oslot + b + 32 * kSpmvWarps);
-        src_n = __ldg(S.shfl_src + b + 32 * kSpmvWarps);
-      }
-      double t[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      if (o >= 0) {
-        double xo[6];
-        load6_ro(x, o, nf, xo);
-        const Coef cv = load_coef<true>(S.scoef + cf_idx(b, 0));
-        const double nx = cv.al * ((cv.n[0] * xo[0] + cv.n[1] * xo[1]) + cv.n[2] * xo[2]);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) acc[c] -= nx * cv.n[c] + cv.be * xo[c];
-#pragma unroll
-        for (int qq = 0; qq < 3; ++qq)
-          acc[3 + qq] += (cv.C[3 * qq] * xo[3] + cv.C[3 * qq + 1] * xo[4]) + cv.C[3 * qq + 2] * xo[5];
-        if (own >= 0) {
-          // row j's product from this row's x (the j-role formula of slot_apply)
-          double xi[6];
-          load6_ro(x, own, nf, xi);
-          const double ni = cv.al * ((cv.n[0] * xi[0] + cv.n[1] * xi[1]) + cv.n[2] * xi[2]);
-#pragma unroll
-          for (int c = 0; c < 3; ++c) t[c] = -(ni * cv.n[c] + cv.be * xi[c]);
-#pragma unroll
-          for (int qq = 0; qq < 3; ++qq)
-            t[3 + qq] = (cv.C[qq] * xi[3] + cv.C[3 + qq] * xi[4]) + cv.C[6 + qq] * xi[5];
-        }
-      }
-      const int from = src >= 0 ? src : lane;
-#pragma unroll
-      for (int c = 0; c < 6; ++c) {
-        const double v = __shfl_sync(0xffffffffu, t[c], from);
-        if (src >= 0) acc[c] += v;
-      }
-    }
-    // remaining j-role bonds (lists without the handed-over ones)
-    SlotRef cur{0, -1, true};
-    if (w < kj) {
-      cur.o = __ldg(S.shfl_jslot + c0 + 32 * w + lane);
-      cur.b = __ldg(S.shfl_jpos + c0 + 32 * w + lane);
-    }
-#pragma unroll 1
-    for (int k = w; k < kj; k += kSpmvWarps) {
-      SlotRef nxt{0, -1, true};
-      if (k + kSpmvWarps < kj) {
-        const int64_t jk = c0 + 32 * (k + kSpmvWarps) + lane;
-        nxt.o = __ldg(S.shfl_jslot + jk);
-        nxt.b = __ldg(S.shfl_jpos + jk);
-      }
-      slot_apply(S, x, cur, acc);
-      cur = nxt;
-    }
-#pragma unroll
-    for (int q = 0; q < 6; ++q) part[w][q][lane] = acc[q];
-    __syncthreads();
-    spmv_tail<kSpmvWarps>(S, x, y, sl, w, lane, part, boost, acc_xy, acc_yy, acc_xx, own);
-    __syncthreads();
-  }
-  if (mode == 0) return;
-  spmv_pcg_epilogue<kSpmvThreads>(S, boost, acc_xy, acc_yy, acc_xx, sh);
-}
-
 // x += alpha p; r -= alpha Ap; z = M^-1 r; r.r, r.z (linalg.py:79-89)
 #ifndef BDEM_UPD_MINB
 #define BDEM_UPD_MINB 4
@@ -942,861 +838,6 @@ __global__ void __launch_bounds__(kThreads) k_pair(bdem_system_t S, const double
   if (threadIdx.x == 0) *red_slot(S.red, BDEM_SC_EPAIR, blockIdx.x) = s;
 }
 
-// ---------------------------------------------------------------------------
-// Tiled SpMV (default).  The slot-parallel kernel above moves ~1.8 GB of L2
-// sectors per plate SpMV -- every bond's coefficients are read twice (i-role
-// stream, j-role gather) plus one neighbour-x gather per slot -- which sits on
-// the chip's L2-slice throughput cap.  Here SELL rows are in Z-order, so a
-// tile of TS slices (TS*32 rows) is a compact patch and most bonds join two
-// rows of the same tile.  Per tile, warp 0 streams the tile's i-role
-// coefficient planes, their neighbour slots and the tile's own x and
-// diagonal blocks into a STAGES-deep shared-memory ring with cp.async.bulk
-// (one transaction-counted mbarrier per stage).  The warps read i-role
-// coefficients from shared memory, and j-role coefficients / neighbour x
-// from shared memory whenever the partner row is inside the tile: only
-// tile-boundary bonds go through L2.  Per-row summation order is the same
-// fixed order as k_spmv (deterministic).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      " .reg .pred p;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
-                                         uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-constexpr int kTilePlanes = BDEM_CF_COUNT;
-
-// capacities of one stage (host and device agree through this struct)
-struct TileCaps {
-  int cap;   // i-role positions staged
-  int capj;  // j-role list entries staged
-  int xcap;  // slot window (TS*32 + 2 for the 16-byte alignment of the copies)
-  int rows;  // TS*32
-  bool diag; // stage the diagonal blocks too
-  __host__ __device__ int off_x() const { return kTilePlanes * cap; }
-  __host__ __device__ int off_diag() const { return off_x() + 6 * xcap; }
-  __host__ __device__ int off_int() const { return off_diag() + (diag ? 12 * xcap : 0); }
-  // int32 region: oslot[cap] | jslot[capj] | jpos[capj] | rslot[rows]
-  __host__ __device__ int stage_doubles() const {
-    return off_int() + (cap + 2 * capj + rows + 1) / 2;
-  }
-};
-
-// per-stage header, written by the producer before it arrives on the barrier
-template <int TS>
-struct TileHdr {
-  int64_t p0;        // first i-role position of the tile
-  int64_t jb[TS + 1];  // j-role list bounds of the tile's slices
-  int64_t ib[TS + 1];  // i-role position bounds of the tile's slices
-  int ncopy, njcopy, nrows;
-  int s0, s1, xa, xn;
-};
-
-#ifdef BDEM_TILE_PROF
-__device__ unsigned long long g_tile_prof[8];
-#define TPROF_DECL() long long _pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}
-#define TPROF_T0() long long _tp = clock64()
-#define TPROF_MARK(k)                  \
-  do {                                 \
-    const long long _n = clock64();    \
-    _pacc[k] += _n - _tp;              \
-    _tp = _n;                          \
-  } while (0)
-#define TPROF_FLUSH()                                                                    \
-  do {                                                                                   \
-    if (threadIdx.x == 0)                                                                \
-      for (int _k = 0; _k < 6; ++_k) atomicAdd(&g_tile_prof[_k], (unsigned long long)_pacc[_k]); \
-  } while (0)
-#else
-#define TPROF_DECL()
-#define TPROF_T0()
-#define TPROF_MARK(k)
-#define TPROF_FLUSH()
-#endif
-
-// Header words of a tile, one per lane of warp 0 (loaded early so their
-// latency hides under the previous tile's work): lanes 0..TS slice_base,
-// TS+1..2TS+1 jslice_base, 2TS+2 / 2TS+3 slice_slot of the first / end slice.
-// header record of a tile (host-built, BDEM_TILE_HDR ints, 16-byte multiple)
-template <int TS>
-struct TileHdrWords {
-  static constexpr int kInts = (2 * (TS + 1) + 2 + 3) & ~3;
-};
-template <int TS>
-__device__ __forceinline__ int64_t tile_hdr_word_g(const bdem_system_t &S, int tile, int lane) {
-  return lane < TileHdrWords<TS>::kInts
-             ? __ldg(S.tile_hdr + (int64_t)tile * TileHdrWords<TS>::kInts + lane)
-             : 0;
-}
-
-// warp 0 fills one stage: header + every bulk copy of the tile (copy q by
-// lane q % 32): 0..13 coefficient planes, 14..19 x planes, 20..31 diagonal
-// planes, 32 oslot, 33 jslot, 34 jpos, 35 row slots
-template <int TS>
-__device__ __forceinline__ void tile_issue(const bdem_system_t &S, const double *x, int tile,
-                                           int ns, const TileCaps &cp, double *buf,
-                                           TileHdr<TS> *hdr, uint64_t *bar, int lane,
-                                           int64_t word, int next_tile, int32_t *next_words) {
-  const int64_t vs = S.vstride;
-  const int t0 = tile * TS, t1 = min(ns, t0 + TS);
-  TileHdr<TS> h;
-#pragma unroll
-  for (int t = 0; t <= TS; ++t) {
-    h.ib[t] = __shfl_sync(0xffffffffu, word, t);
-    h.jb[t] = __shfl_sync(0xffffffffu, word, TS + 1 + t);
-  }
-  h.s0 = (int)__shfl_sync(0xffffffffu, word, 2 * TS + 2);
-  h.s1 = (int)__shfl_sync(0xffffffffu, word, 2 * TS + 3);
-  h.p0 = h.ib[0];
-  h.ncopy = (int)min(h.ib[TS] - h.p0, (int64_t)cp.cap);
-  h.njcopy = (int)min(h.jb[TS] - h.jb[0], (int64_t)cp.capj);
-  h.nrows = (t1 - t0) * 32;
-  h.xa = h.s0 & ~1;
-  h.xn = (h.s1 - h.xa + 1) & ~1;
-  const uint32_t cb = 8u * h.ncopy, xb = 8u * h.xn, jb = 4u * h.njcopy;
-  const uint32_t hb = next_tile >= 0 ? 4u * TileHdrWords<TS>::kInts : 0u;
-  const uint32_t total = kTilePlanes * cb + (cp.diag ? 18u : 6u) * xb + 4u * h.ncopy + 2u * jb +
-                         4u * h.nrows + hb;
-  if (lane == 0) {
-    *hdr = h;
-#ifndef BDEM_TILE_NOFENCE
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#endif
-    mbar_arrive_expect_tx(bar, total);
-  }
-  __syncwarp();
-  // lane 0: the tile's AoSoA-32 coefficient block (one contiguous range);
-  // 1..6 x planes, 7..18 diagonal planes, 19..22 slot / j-list / row indices
-  int *ib = reinterpret_cast<int *>(buf + cp.off_int());
-  const int q = lane;
-  if (q == 0) {
-    if (cb) bulk_g2s(buf, S.scoef + h.p0 * kTilePlanes, kTilePlanes * cb, bar);
-  } else if (q <= 6) {
-    if (xb) bulk_g2s(buf + cp.off_x() + (q - 1) * cp.xcap, x + (q - 1) * vs + h.xa, xb, bar);
-  } else if (q <= 18) {
-    if (cp.diag && xb)
-      bulk_g2s(buf + cp.off_diag() + (q - 7) * cp.xcap, S.diag + (q - 7) * vs + h.xa, xb, bar);
-  } else if (q == 19) {
-    if (cb) bulk_g2s(ib, S.pos_oslot + h.p0, 4u * h.ncopy, bar);
-  } else if (q == 20) {
-    if (jb) bulk_g2s(ib + cp.cap, S.jslot + h.jb[0], jb, bar);
-  } else if (q == 21) {
-    if (jb) bulk_g2s(ib + cp.cap + cp.capj, S.jpos + h.jb[0], jb, bar);
-  } else if (q == 22) {
-    bulk_g2s(ib + cp.cap + 2 * cp.capj, S.row_slot + (int64_t)t0 * 32, 4u * h.nrows, bar);
-  } else if (q == 23) {
-    // the header of the next tile this stage will be refilled with
-    if (hb) bulk_g2s(next_words, S.tile_hdr + (int64_t)next_tile * TileHdrWords<TS>::kInts, hb, bar);
-  }
-}
-
-
-
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// named barrier among the NW consumer warps (the producer warp never joins)
-__device__ __forceinline__ void consumers_sync(int nthreads) {
-  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
-}
-
-// Warp-specialised: warps 0..NW-1 consume tiles, warp NW produces them.  The
-// producer refills stage s as soon as every consumer warp has arrived on
-// empty[s], so copy issue never sits on the consumers' critical path.
-template <int TS, int NW, int STAGES, int MINB>
-__global__ void __launch_bounds__((NW + 1) * 32, MINB)
-    k_spmv_tile(bdem_system_t S, const double *__restrict__ x, double *__restrict__ y, int mode,
-                TileCaps cp) {
-  extern __shared__ __align__(128) double tsm[];
-  __shared__ double part[NW][6][32];
-  __shared__ double sh[NW + 1];
-  __shared__ TileHdr<TS> hdrs[STAGES];
-  __shared__ __align__(16) int32_t hnext[STAGES][TileHdrWords<TS>::kInts];
-  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
-  double *pcg = S.pcg;
-  if (mode == 1 && pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
-  const double boost = mode == 1 ? pcg[BDEM_PCG_BOOST] : 0.0;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t vs = S.vstride;
-  const int ns = (int)((S.n_elem + 31) >> 5);
-  const int ntiles = (ns + TS - 1) / TS;
-  const int sd = cp.stage_doubles();
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < STAGES; ++k) {
-      mbar_init(&full[k], 1);
-      mbar_init(&empty[k], NW);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  double acc_xy = 0.0, acc_yy = 0.0, acc_xx = 0.0;
-  if (w == NW) {
-    // ---- producer ----
-    int i = 0;
-#pragma unroll 1
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
-      const int stg = i % STAGES;
-      int64_t word;
-      if (i >= STAGES) {
-        mbar_wait(&empty[stg], (uint32_t)(((i / STAGES) - 1) & 1));
-        word = lane < TileHdrWords<TS>::kInts ? hnext[stg][lane] : 0;  // came with stage's copies
-      } else {
-        word = tile_hdr_word_g<TS>(S, tile, lane);
-      }
-      const int nxt = tile + STAGES * gridDim.x;
-      tile_issue<TS>(S, x, tile, ns, cp, tsm + stg * sd, &hdrs[stg], &full[stg], lane, word,
-                     nxt < ntiles ? nxt : -1, hnext[stg]);
-    }
-  } else {
-    // ---- consumers ----
-    TPROF_DECL();
-    const int t_mine = w % TS;   // slice of the tile this warp works on
-    constexpr int WPS = NW / TS;  // warps per slice
-    int it = 0;
-#pragma unroll 1
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      const int stg = it % STAGES;
-      double *buf = tsm + stg * sd;
-      const double *cf = buf;
-      const double *xs = buf + cp.off_x();
-      const int *osl = reinterpret_cast<const int *>(buf + cp.off_int());
-      const int *jsl = osl + cp.cap;
-      const int *jps = jsl + cp.capj;
-      const int *rsl = jps + cp.capj;
-      TPROF_T0();
-      mbar_wait(&full[stg], (uint32_t)((it / STAGES) & 1));
-      TPROF_MARK(0);
-      const TileHdr<TS> &h = hdrs[stg];
-      const int64_t p0 = h.p0, jb0 = h.jb[0];
-      const int ncopy = h.ncopy, njcopy = h.njcopy, s0 = h.s0, s1 = h.s1, xa = h.xa;
-      const int64_t i0 = h.ib[t_mine], j0 = h.jb[t_mine];
-      const int ki = (int)((h.ib[t_mine + 1] - i0) >> 5), kj = (int)((h.jb[t_mine + 1] - j0) >> 5);
-      double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  #pragma unroll 1
-      for (int k = w / TS; k < ki + kj; k += WPS) {
-        int64_t b;
-        int o;
-        bool tr;
-        if (k < ki) {
-          b = i0 + 32 * k + lane;
-          const int64_t lb = b - p0;
-          o = lb < ncopy ? osl[lb] : __ldg(S.pos_oslot + b);
-          tr = false;
-        } else {
-          const int64_t jk = j0 + 32 * (k - ki) + lane;
-          const int64_t lj = jk - jb0;
-          if (lj < njcopy) {
-            o = jsl[lj];
-            b = jps[lj];
-          } else {
-            o = __ldg(S.jslot + jk);
-            b = __ldg(S.jpos + jk);
-          }
-          tr = true;
-        }
-        if (o < 0) continue;
-        double xo[6], n[3], C[9], al, be;
-        if (o >= s0 && o < s1) {
-  #pragma unroll
-          for (int c = 0; c < 6; ++c) xo[c] = xs[c * cp.xcap + (o - xa)];
-        } else {
-          load6_ro(x, o, vs, xo);
-        }
-        const int64_t lb = b - p0;
-        const bool local = lb >= 0 && lb < ncopy;
-        const double *cb = local ? cf + cf_idx(lb, 0) : S.scoef + cf_idx(b, 0);
-        if (local) {
-  #pragma unroll
-          for (int t = 0; t < 3; ++t) n[t] = cb[32 * (BDEM_CF_N + t)];
-          al = cb[32 * BDEM_CF_ALPHA];
-          be = cb[32 * BDEM_CF_BETA];
-  #pragma unroll
-          for (int t = 0; t < 9; ++t) C[t] = cb[32 * (BDEM_CF_C + t)];
-        } else {
-  #pragma unroll
-          for (int t = 0; t < 3; ++t) n[t] = __ldg(cb + 32 * (BDEM_CF_N + t));
-          al = __ldg(cb + 32 * BDEM_CF_ALPHA);
-          be = __ldg(cb + 32 * BDEM_CF_BETA);
-  #pragma unroll
-          for (int t = 0; t < 9; ++t) C[t] = __ldg(cb + 32 * (BDEM_CF_C + t));
-        }
-        const double nx = al * ((n[0] * xo[0] + n[1] * xo[1]) + n[2] * xo[2]);
-  #pragma unroll
-        for (int c = 0; c < 3; ++c) acc[c] -= nx * n[c] + be * xo[c];
-        if (!tr) {
-  #pragma unroll
-          for (int q = 0; q < 3; ++q)
-            acc[3 + q] += (C[3 * q] * xo[3] + C[3 * q + 1] * xo[4]) + C[3 * q + 2] * xo[5];
-        } else {
-  #pragma unroll
-          for (int q = 0; q < 3; ++q)
-            acc[3 + q] += (C[q] * xo[3] + C[3 + q] * xo[4]) + C[6 + q] * xo[5];
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 6; ++q) part[w][q][lane] = acc[q];
-      TPROF_MARK(1);
-      consumers_sync(NW * 32);
-      TPROF_MARK(2);
-      // tail: (slice, component) items; y = D x + partials (fixed warp order) - pairs
-  #pragma unroll 1
-      for (int item = w; item < TS * 6; item += NW) {
-        const int t = item / 6, c = item - 6 * t;
-        if (32 * t >= h.nrows) continue;
-        const int sslot = rsl[32 * t + lane];
-        if (sslot < 0) continue;
-        const int base = c < 3 ? 0 : 3, rr = c - base;
-        const int ls = sslot - xa;
-        double dg0, dg1, dg2;
-        if (cp.diag) {
-          const double *dg = buf + cp.off_diag() + (c < 3 ? 0 : 6 * cp.xcap);
-          dg0 = dg[sidx<3>(rr, 0) * cp.xcap + ls];
-          dg1 = dg[sidx<3>(rr, 1) * cp.xcap + ls];
-          dg2 = dg[sidx<3>(rr, 2) * cp.xcap + ls];
-        } else {
-          const double *dg = S.diag + (c < 3 ? 0 : 6 * vs);
-          dg0 = __ldg(dg + sidx<3>(rr, 0) * vs + sslot);
-          dg1 = __ldg(dg + sidx<3>(rr, 1) * vs + sslot);
-          dg2 = __ldg(dg + sidx<3>(rr, 2) * vs + sslot);
-        }
-        double yc = (dg0 * xs[(base + 0) * cp.xcap + ls] + dg1 * xs[(base + 1) * cp.xcap + ls]) +
-                    dg2 * xs[(base + 2) * cp.xcap + ls];
-  #pragma unroll
-        for (int ww = t; ww < NW; ww += TS) yc += part[ww][c][lane];
-        if (c < 3 && S.n_pair > 0) {
-          const int64_t e = __ldg(S.row_elem + (int64_t)(tile * TS + t) * 32 + lane);
-          const int64_t pc = S.pair_cap;
-          const double *ps = S.pstage;
-          for (int k = S.pi_ptr[e]; k < S.pi_ptr[e + 1]; ++k) {
-            const int o = S.slot[S.pair_j[k]];
-            if (o < 0) continue;
-            yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[0 * vs + o] +
-                   ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[1 * vs + o]) +
-                  ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[2 * vs + o];
-          }
-          for (int kk = S.pj_ptr[e]; kk < S.pj_ptr[e + 1]; ++kk) {
-            const int64_t k = S.pj_idx[kk];
-            const int o = S.slot[S.pair_i[k]];
-            if (o < 0) continue;
-            yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[0 * vs + o] +
-                   ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[1 * vs + o]) +
-                  ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[2 * vs + o];
-          }
-        }
-        const double xc = xs[c * cp.xcap + ls];
-        if (boost != 0.0) yc = yc + boost * xc;
-        y[c * vs + sslot] = yc;
-        acc_xy += xc * yc;
-        acc_yy += yc * yc;
-        acc_xx += xc * xc;
-      }
-      TPROF_MARK(3);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stg]);  // this warp is done with the stage
-      consumers_sync(NW * 32);                  // part[] is rewritten next tile
-      TPROF_MARK(4);
-    }
-    TPROF_FLUSH();
-  }
-  __syncthreads();
-  if (mode == 0) return;
-  spmv_pcg_epilogue<(NW + 1) * 32>(S, boost, acc_xy, acc_yy, acc_xx, sh);
-}
-
-#ifndef BDEM_TILE_TS
-#define BDEM_TILE_TS 1
-#endif
-#ifndef BDEM_TILE_NW
-#define BDEM_TILE_NW 8
-#endif
-#ifndef BDEM_TILE_STAGES
-#define BDEM_TILE_STAGES 3
-#endif
-#ifndef BDEM_TILE_MINB
-#define BDEM_TILE_MINB 2
-#endif
-#ifndef BDEM_TILE_DIAG
-#define BDEM_TILE_DIAG 1
-#endif
-#ifndef BDEM_TILE_KCAP
-#define BDEM_TILE_KCAP 8
-#endif
-constexpr int kTileTS = BDEM_TILE_TS, kTileNW = BDEM_TILE_NW, kTileStages = BDEM_TILE_STAGES;
-
-// tiled launch when enabled and the staging fits; returns false otherwise
-// SpMV variant: 0 slot-parallel k_spmv (default), 1 tiled k_spmv_tile
-static int g_spmv_kernel = -1;
-static int spmv_kernel() {
-  if (g_spmv_kernel < 0) {
-    const char *env = getenv("BDEM_SPMV_TILE");
-    g_spmv_kernel = env ? atoi(env) : 0;
-    if (g_spmv_kernel < 0 || g_spmv_kernel > 4) g_spmv_kernel = 0;
-  }
-  return g_spmv_kernel;
-}
-
-static bool launch_spmv_tile(const bdem_system_t &S, const double *x, double *y, int mode,
-                             cudaStream_t st) {
-  static int sms = 0;
-  if (spmv_kernel() != 1 || S.n_elem == 0 || !S.tile_hdr) return false;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  auto clampk = [](int64_t k) { return (int)(k < 1 ? 1 : (k > BDEM_TILE_KCAP ? BDEM_TILE_KCAP : k)); };
-  TileCaps cp;
-  cp.rows = kTileTS * 32;
-  cp.cap = cp.rows * clampk(S.sell_kmax);
-  cp.capj = cp.rows * clampk(S.sell_kjmax);
-  cp.xcap = cp.rows + 2;
-  cp.diag = BDEM_TILE_DIAG != 0;
-  const size_t bytes = sizeof(double) * (size_t)cp.stage_doubles() * kTileStages;
-  auto kern = k_spmv_tile<kTileTS, kTileNW, kTileStages, BDEM_TILE_MINB>;
-  static size_t configured = 0;
-  static int per_sm = 1;
-  if (bytes > configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
-        cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
-    configured = bytes;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (kTileNW + 1) * 32, bytes);
-    if (per_sm < 1) per_sm = 1;
-  }
-  const int ns = (int)((S.n_elem + 31) >> 5);
-  const int ntiles = (ns + kTileTS - 1) / kTileTS;
-  int g = sms * per_sm;
-  if (g > ntiles) g = ntiles;
-  if (g > kRedBlocks) g = kRedBlocks;
-  kern<<<g, (kTileNW + 1) * 32, bytes, st>>>(S, x, y, mode, cp);
-  return true;
-}
-
-// ---------------------------------------------------------------------------
-// Contribution-table SpMV (variant 2).  Rows in strip-major order; a CTA owns
-// a tile of TS slices (R = 32 TS rows).  Each i-role slot reads its bond once
-// from the coefficient stream and forms both products: row i's goes to the
-// thread's accumulator, and when row j is in the same tile, row j's product
-// (-a+ x_i, C^T x_i) is stored in the tile's shared-memory table at the
-// bond's precomputed slot (unique per bond: no atomics).  Only boundary bonds
-// (rows in different tiles) remain in the j-role lists and are gathered from
-// L2.  Row sums: D x + slot partials (fixed warp order) + table entries (rank
-// order) + boundary j-role partials -- deterministic.
-// ---------------------------------------------------------------------------
-#ifndef BDEM_SYM_TS
-#define BDEM_SYM_TS 4
-#endif
-#ifndef BDEM_SYM_NW
-#define BDEM_SYM_NW 8
-#endif
-#ifndef BDEM_SYM_MINB
-#define BDEM_SYM_MINB 2
-#endif
-#ifndef BDEM_SYM_KCAP
-#define BDEM_SYM_KCAP 8
-#endif
-constexpr int kSymTS = BDEM_SYM_TS, kSymNW = BDEM_SYM_NW;
-
-template <int TS, int NW, int MINB>
-__global__ void __launch_bounds__(NW * 32, MINB)
-    k_spmv_sym(bdem_system_t S, const double *__restrict__ x, double *__restrict__ y, int mode,
-               int kc) {
-  constexpr int R = TS * 32;
-  extern __shared__ __align__(16) double tab[];  // [kc][6][R]
-  __shared__ double part[NW][6][32];
-  __shared__ double sh[NW];
-  double *pcg = S.pcg;
-  if (mode == 1 && pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
-  const double boost = mode == 1 ? pcg[BDEM_PCG_BOOST] : 0.0;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t vs = S.vstride;
-  const int ns = (int)((S.n_elem + 31) >> 5);
-  const int ntiles = (ns + TS - 1) / TS;
-  const int t_mine = w % TS;
-  constexpr int WPS = NW / TS;
-  const int ntab = kc * 6 * R;
-  double acc_xy = 0.0, acc_yy = 0.0, acc_xx = 0.0;
-#pragma unroll 1
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    for (int k = threadIdx.x; k < ntab; k += NW * 32) tab[k] = 0.0;
-    const int sl = tile * TS + t_mine;
-    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    if (sl < ns) {
-      const int64_t row = (int64_t)sl * 32 + lane;
-      const int myslot = __ldg(S.row_slot + row);
-      double xi[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      if (myslot >= 0) load6_ro(x, myslot, vs, xi);
-      const int64_t i0 = __ldg(S.slice_base + sl), j0 = __ldg(S.sym_jbase + sl);
-      const int ki = (int)((__ldg(S.slice_base + sl + 1) - i0) >> 5);
-      const int kj = (int)((__ldg(S.sym_jbase + sl + 1) - j0) >> 5);
-      __syncthreads();  // table zeroed before any warp writes into it
-#pragma unroll 1
-      for (int k = w / TS; k < ki + kj; k += WPS) {
-        int64_t b;
-        int o, jl = -1;
-        bool tr;
-        if (k < ki) {
-          b = i0 + 32 * k + lane;
-          o = __ldg(S.pos_oslot + b);
-          jl = myslot >= 0 ? __ldg(S.sym_jloc + b) : -1;
-          tr = false;
-        } else {
-          const int64_t jk = j0 + 32 * (k - ki) + lane;
-          o = __ldg(S.sym_jslot + jk);
-          b = __ldg(S.sym_jpos + jk);
-          tr = true;
-        }
-        if (o < 0 || myslot < 0) continue;
-        double xo[6];
-        load6_ro(x, o, vs, xo);
-        const Coef cv = load_coef<true>(S.scoef + cf_idx(b, 0));
-        const double nx = cv.al * ((cv.n[0] * xo[0] + cv.n[1] * xo[1]) + cv.n[2] * xo[2]);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) acc[c] -= nx * cv.n[c] + cv.be * xo[c];
-        if (!tr) {
-#pragma unroll
-          for (int q = 0; q < 3; ++q)
-            acc[3 + q] += (cv.C[3 * q] * xo[3] + cv.C[3 * q + 1] * xo[4]) + cv.C[3 * q + 2] * xo[5];
-          if (jl >= 0) {  // row j in this tile: its product from the same read
-            const int rk = jl / R, rl = jl - rk * R;
-            double *tb = tab + (size_t)rk * 6 * R + rl;
-            const double ni = cv.al * ((cv.n[0] * xi[0] + cv.n[1] * xi[1]) + cv.n[2] * xi[2]);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) tb[c * R] = -(ni * cv.n[c] + cv.be * xi[c]);
-#pragma unroll
-            for (int q = 0; q < 3; ++q)
-              tb[(3 + q) * R] = (cv.C[q] * xi[3] + cv.C[3 + q] * xi[4]) + cv.C[6 + q] * xi[5];
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < 3; ++q)
-            acc[3 + q] += (cv.C[q] * xo[3] + cv.C[3 + q] * xo[4]) + cv.C[6 + q] * xo[5];
-        }
-      }
-    } else {
-      __syncthreads();
-    }
-#pragma unroll
-    for (int q = 0; q < 6; ++q) part[w][q][lane] = acc[q];
-    __syncthreads();
-#pragma unroll 1
-    for (int item = w; item < TS * 6; item += NW) {
-      const int t = item / 6, c = item - 6 * t;
-      const int slc = tile * TS + t;
-      if (slc >= ns) continue;
-      const int64_t row = (int64_t)slc * 32 + lane;
-      const int sslot = __ldg(S.row_slot + row);
-      if (sslot < 0) continue;
-      const int base = c < 3 ? 0 : 3, rr = c - base;
-      const double *dg = S.diag + (c < 3 ? 0 : 6 * vs);
-      double xs3[3];
-#pragma unroll
-      for (int u = 0; u < 3; ++u) xs3[u] = __ldg(x + (base + u) * vs + sslot);
-      double yc = (__ldg(dg + sidx<3>(rr, 0) * vs + sslot) * xs3[0] +
-                   __ldg(dg + sidx<3>(rr, 1) * vs + sslot) * xs3[1]) +
-                  __ldg(dg + sidx<3>(rr, 2) * vs + sslot) * xs3[2];
-#pragma unroll
-      for (int ww = t; ww < NW; ww += TS) yc += part[ww][c][lane];
-      const int rl = t * 32 + lane;
-      for (int rk = 0; rk < kc; ++rk) yc += tab[((size_t)rk * 6 + c) * R + rl];
-      if (c < 3 && S.n_pair > 0) {
-        const int64_t e = __ldg(S.row_elem + row);
-        const int64_t pc = S.pair_cap;
-        const double *ps = S.pstage;
-        for (int k = S.pi_ptr[e]; k < S.pi_ptr[e + 1]; ++k) {
-          const int o = S.slot[S.pair_j[k]];
-          if (o < 0) continue;
-          yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[0 * vs + o] +
-                 ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[1 * vs + o]) +
-                ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[2 * vs + o];
-        }
-        for (int kk = S.pj_ptr[e]; kk < S.pj_ptr[e + 1]; ++kk) {
-          const int64_t k = S.pj_idx[kk];
-          const int o = S.slot[S.pair_i[k]];
-          if (o < 0) continue;
-          yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[0 * vs + o] +
-                 ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[1 * vs + o]) +
-                ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[2 * vs + o];
-        }
-      }
-      const double xc = xs3[rr];
-      if (boost != 0.0) yc = yc + boost * xc;
-      y[c * vs + sslot] = yc;
-      acc_xy += xc * yc;
-      acc_yy += yc * yc;
-      acc_xx += xc * xc;
-    }
-    __syncthreads();
-  }
-  if (mode == 0) return;
-  spmv_pcg_epilogue<NW * 32>(S, boost, acc_xy, acc_yy, acc_xx, sh);
-}
-
-static bool launch_spmv_sym(const bdem_system_t &S, const double *x, double *y, int mode,
-                            cudaStream_t st) {
-  static int sms = 0, per_sm = 0;
-  static size_t configured = 0;
-  if (S.n_elem == 0 || !S.sym_jloc || S.sym_kc > BDEM_SYM_KCAP) return false;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  const int kc = (int)(S.sym_kc > 0 ? S.sym_kc : 1);
-  const size_t bytes = sizeof(double) * (size_t)kc * 6 * kSymTS * 32;
-  auto kern = k_spmv_sym<kSymTS, kSymNW, BDEM_SYM_MINB>;
-  if (bytes > configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
-        cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
-    configured = bytes;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSymNW * 32, bytes);
-    if (per_sm < 1) per_sm = 1;
-  }
-  const int ns = (int)((S.n_elem + 31) >> 5);
-  const int ntiles = (ns + kSymTS - 1) / kSymTS;
-  int g = sms * per_sm;
-  if (g > ntiles) g = ntiles;
-  if (g > kRedBlocks) g = kRedBlocks;
-  kern<<<g, kSymNW * 32, bytes, st>>>(S, x, y, mode, kc);
-  return true;
-}
-
-// ---------------------------------------------------------------------------
-// Dataflow SpMV (variant 3).  Rows in the caller order with row(i) < row(j)
-// for every bond.  Work items, taken in ticket order by persistent CTAs:
-//   A(s): slice s's i-role slots -- each bond read ONCE from the coefficient
-//         stream; row i's product is summed (-> wave_ypart), row j's product
-//         (-a+ x_i, C^T x_i) goes to a ring slot in L2 (wave_ring);
-//   B(s): slice s's j-role entries read those 48-byte products from the ring
-//         (no coefficient re-read, no x_i gather), then the row tail.
-// B(s) needs A(s-lag .. s): tickets run A lag+1 slices ahead and B spins on
-// epoch-stamped done flags (its producers hold earlier tickets, so they are
-// running or done: no deadlock).  The ring holds wave_ring_slices slices
-// (far beyond the in-flight window, and A checks the B flags of the slot's
-// previous owners), so products are consumed from L2 and never written back.
-// Row sum: D x + i-role sum + j-role sum + pairs, fixed order.
-// ---------------------------------------------------------------------------
-#ifndef BDEM_WAVE_NW
-#define BDEM_WAVE_NW 4
-#endif
-#ifndef BDEM_WAVE_MINB
-#define BDEM_WAVE_MINB 8
-#endif
-constexpr int kWaveNW = BDEM_WAVE_NW;
-
-__device__ __forceinline__ int ld_acquire(const int32_t *p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(int32_t *p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// warp-wide spin until flags[lo..hi] all equal epoch (acquire loads)
-__device__ __forceinline__ void wait_flags(const int32_t *flags, int lo, int hi, int epoch,
-                                           int lane) {
-  for (int base = lo; base <= hi; base += 32) {
-    const int k = base + lane;
-    if (k <= hi)
-      while (ld_acquire(flags + k) != epoch) __nanosleep(32);
-  }
-  __syncwarp();
-}
-
-template <int NW>
-__global__ void __launch_bounds__(NW * 32, BDEM_WAVE_MINB)
-    k_spmv_wave(bdem_system_t S, const double *__restrict__ x, double *__restrict__ y, int mode,
-                int epoch, int lead_rounds) {
-  __shared__ double part[NW][6][32];
-  __shared__ double sh[NW];
-  double *pcg = S.pcg;
-  if (mode == 1 && pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
-  const double boost = mode == 1 ? pcg[BDEM_PCG_BOOST] : 0.0;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t vs = S.vstride;
-  const int ns = (int)((S.n_elem + 31) >> 5);
-  const int L = (int)S.wave_lag, RING = (int)S.wave_ring_slices;
-  const int kmax = (int)(S.sell_kmax > 0 ? S.sell_kmax : 1);
-  const int64_t rs = (int64_t)RING * kmax * 32;  // ring plane stride
-  int32_t *flagA = S.wave_flags, *flagB = flagA + ns;
-  double *ring = S.wave_ring, *ypart = S.wave_ypart;
-  const int G = gridDim.x;
-  double acc_xy = 0.0, acc_yy = 0.0, acc_xx = 0.0;
-  // round m: A(blockIdx + (m + lead) G) then B(blockIdx + (m - 0) G); the first
-  // `lead` rounds only produce.  A waits on nothing but the ring's previous
-  // owners; B waits on A(s - L .. s), produced lead rounds earlier.
-  const int rounds = (ns + G - 1) / G + lead_rounds;
-#pragma unroll 1
-  for (int m = 0; m < rounds; ++m) {
-    const int sa = blockIdx.x + m * G;             // A slice of this round
-    const int sb = blockIdx.x + (m - lead_rounds) * G;  // B slice of this round
-    if (sa < ns) {
-      const int64_t row = (int64_t)sa * 32 + lane;
-      const int myslot = __ldg(S.row_slot + row);
-      if (sa >= RING && w == 0) wait_flags(flagB, sa - RING, min(sa - RING + L, ns - 1), epoch, lane);
-      __syncthreads();
-      double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      double xi[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      if (myslot >= 0) load6_ro(x, myslot, vs, xi);
-      const int64_t i0 = __ldg(S.slice_base + sa);
-      const int ki = (int)((__ldg(S.slice_base + sa + 1) - i0) >> 5);
-      double *rb = ring + ((int64_t)(sa % RING) * kmax) * 32 + lane;
-#pragma unroll 1
-      for (int k = w; k < ki; k += NW) {
-        const int64_t b = i0 + 32 * k + lane;
-        const int o = __ldg(S.pos_oslot + b);
-        if (o < 0 || myslot < 0) continue;
-        double xo[6];
-        load6_ro(x, o, vs, xo);
-        const Coef cv = load_coef<true>(S.scoef + cf_idx(b, 0));
-        const double nx = cv.al * ((cv.n[0] * xo[0] + cv.n[1] * xo[1]) + cv.n[2] * xo[2]);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) acc[c] -= nx * cv.n[c] + cv.be * xo[c];
-#pragma unroll
-        for (int q = 0; q < 3; ++q)
-          acc[3 + q] += (cv.C[3 * q] * xo[3] + cv.C[3 * q + 1] * xo[4]) + cv.C[3 * q + 2] * xo[5];
-        // row j's product: -(a+ x_i) and C^T x_i (what k_spmv's j-role slot computes)
-        const double ni = cv.al * ((cv.n[0] * xi[0] + cv.n[1] * xi[1]) + cv.n[2] * xi[2]);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) __stcg(rb + c * rs + (int64_t)k * 32, -(ni * cv.n[c] + cv.be * xi[c]));
-#pragma unroll
-        for (int q = 0; q < 3; ++q)
-          __stcg(rb + (3 + q) * rs + (int64_t)k * 32,
-                 (cv.C[q] * xi[3] + cv.C[3 + q] * xi[4]) + cv.C[6 + q] * xi[5]);
-      }
-#pragma unroll
-      for (int q = 0; q < 6; ++q) part[w][q][lane] = acc[q];
-      __syncthreads();
-      for (int c = w; c < 6; c += NW) {
-        if (myslot < 0) continue;
-        double v = 0.0;
-#pragma unroll
-        for (int ww = 0; ww < NW; ++ww) v += part[ww][c][lane];
-        __stcg(ypart + c * vs + myslot, v);
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) st_release(flagA + sa, epoch);
-    }
-    if (sb >= 0 && sb < ns) {
-      const int64_t row = (int64_t)sb * 32 + lane;
-      const int myslot = __ldg(S.row_slot + row);
-      const int64_t j0 = __ldg(S.jslice_base + sb);
-      const int kj = (int)((__ldg(S.jslice_base + sb + 1) - j0) >> 5);
-      if (w == 0) wait_flags(flagA, max(sb - L, 0), sb, epoch, lane);
-      __syncthreads();
-      double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll 1
-      for (int k = w; k < kj; k += NW) {
-        const int r = __ldg(S.wave_jring + j0 + 32 * k + lane);
-        if (r < 0 || myslot < 0) continue;
-#pragma unroll
-        for (int c = 0; c < 6; ++c) acc[c] += __ldcg(ring + c * rs + r);
-      }
-#pragma unroll
-      for (int q = 0; q < 6; ++q) part[w][q][lane] = acc[q];
-      __syncthreads();
-      for (int c = w; c < 6; c += NW) {
-        if (myslot < 0) continue;
-        const int base = c < 3 ? 0 : 3, rr = c - base;
-        const double *dg = S.diag + (c < 3 ? 0 : 6 * vs);
-        double xs3[3];
-#pragma unroll
-        for (int u = 0; u < 3; ++u) xs3[u] = __ldg(x + (base + u) * vs + myslot);
-        double yc = (__ldg(dg + sidx<3>(rr, 0) * vs + myslot) * xs3[0] +
-                     __ldg(dg + sidx<3>(rr, 1) * vs + myslot) * xs3[1]) +
-                    __ldg(dg + sidx<3>(rr, 2) * vs + myslot) * xs3[2];
-        yc += __ldcg(ypart + c * vs + myslot);
-#pragma unroll
-        for (int ww = 0; ww < NW; ++ww) yc += part[ww][c][lane];
-        if (c < 3 && S.n_pair > 0) {
-          const int64_t e = __ldg(S.row_elem + row);
-          const int64_t pc = S.pair_cap;
-          const double *ps = S.pstage;
-          for (int k = S.pi_ptr[e]; k < S.pi_ptr[e + 1]; ++k) {
-            const int o = S.slot[S.pair_j[k]];
-            if (o < 0) continue;
-            yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[0 * vs + o] +
-                   ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[1 * vs + o]) +
-                  ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[2 * vs + o];
-          }
-          for (int kk = S.pj_ptr[e]; kk < S.pj_ptr[e + 1]; ++kk) {
-            const int64_t k = S.pj_idx[kk];
-            const int o = S.slot[S.pair_i[k]];
-            if (o < 0) continue;
-            yc -= (ps[(BDEM_PS_A + sidx<3>(c, 0)) * pc + k] * x[0 * vs + o] +
-                   ps[(BDEM_PS_A + sidx<3>(c, 1)) * pc + k] * x[1 * vs + o]) +
-                  ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[2 * vs + o];
-          }
-        }
-        const double xc = xs3[rr];
-        if (boost != 0.0) yc = yc + boost * xc;
-        y[c * vs + myslot] = yc;
-        acc_xy += xc * yc;
-        acc_yy += yc * yc;
-        acc_xx += xc * xc;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) st_release(flagB + sb, epoch);
-    }
-  }
-  if (mode == 0) return;
-  spmv_pcg_epilogue<NW * 32>(S, boost, acc_xy, acc_yy, acc_xx, sh);
-}
-
-static bool launch_spmv_wave(const bdem_system_t &S, const double *x, double *y, int mode,
-                             cudaStream_t st) {
-  static int sms = 0, per_sm = 0, epoch = 0;
-  if (S.n_elem == 0 || S.wave_lag < 0 || !S.wave_flags || !S.wave_ring) return false;
-  auto kern = k_spmv_wave<kWaveNW>;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWaveNW * 32, 0);
-    if (per_sm < 1) per_sm = 1;
-  }
-  const int ns = (int)((S.n_elem + 31) >> 5);
-  int g = sms * per_sm;
-  if (g > kRedBlocks) g = kRedBlocks;
-  // A runs lead rounds (lead * g slices) ahead of B: at least the lag, and the
-  // ring must outlast lead + lag + one round of slices
-  int lead_rounds = (int)((S.wave_lag + g) / g);
-  if ((int64_t)(lead_rounds + 2) * g + S.wave_lag > S.wave_ring_slices) return false;
-  if (++epoch <= 0) epoch = 1;
-  kern<<<g, kWaveNW * 32, 0, st>>>(S, x, y, mode, epoch, lead_rounds);
-  return true;
-}
-
 // launch with programmatic stream serialisation (see griddep_wait)
 template <typename... KArgs, typename... Args>
 static void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t st,
@@ -1902,18 +943,10 @@ static void launch_update_fused(unsigned int grid, cudaStream_t st, bool pdl,
   cudaLaunchKernelEx(&cfg, k_pcg_update_fused, S, x, r, ap, p);
 }
 
-// one SpMV launch (plain or PCG mode) with the configured kernel
+// one SpMV launch (plain or PCG mode)
 static void launch_spmv(const bdem_system_t &S, const double *x, double *y, int mode,
                         cudaStream_t st) {
-  if (spmv_kernel() == 3 && launch_spmv_wave(S, x, y, mode, st)) return;
-  if (spmv_kernel() == 4 && S.shfl_src && S.shfl_jbase) {
-    k_spmv_shfl<<<spmv_grid(), kSpmvThreads, 0, st>>>(S, x, y, mode);
-    return;
-  }
-  if (spmv_kernel() == 2 && launch_spmv_sym(S, x, y, mode, st)) return;
-  if (launch_spmv_tile(S, x, y, mode, st)) return;
-  const unsigned int g = spmv_grid();
-  k_spmv<<<g, kSpmvThreads, 0, st>>>(S, x, y, mode);
+  k_spmv<<<spmv_grid(), kSpmvThreads, 0, st>>>(S, x, y, mode);
 }
 
 }  // namespace bdem
@@ -1922,12 +955,6 @@ using namespace bdem;
 
 extern "C" {
 
-int bdem_spmv_tile_slices(void) { return kTileTS; }
-int bdem_spmv_set_kernel(int kernel) {
-  const int prev = spmv_kernel();
-  if (kernel >= 0 && kernel <= 4) g_spmv_kernel = kernel;
-  return prev;
-}
 #if BDEM_TIMELINE
 // diagnostic builds: reset / read the PCG kernel timeline (3 x 1024 x 3 u64)
 int bdem_timeline_reset(void) {
@@ -1954,18 +981,7 @@ int bdem_pcg_set_fused(int on) {
   if (on == 0 || on == 1) g_fused_on = on;
   return prev;
 }
-int bdem_spmv_sym_slices(void) { return kSymTS; }
-int bdem_spmv_sym_kcap(void) { return BDEM_SYM_KCAP; }
-int bdem_spmv_tile_hdr_ints(void) { return TileHdrWords<kTileTS>::kInts; }
 
-#ifdef BDEM_TILE_PROF
-int bdem_tile_prof(unsigned long long *out) {
-  cudaMemcpyFromSymbol(out, g_tile_prof, sizeof(unsigned long long) * 8);
-  unsigned long long z[8] = {0};
-  cudaMemcpyToSymbol(g_tile_prof, z, sizeof(z));
-  return 0;
-}
-#endif
 
 int bdem_spmv(const bdem_system_t *sys, const double *x, double *y, void *stream) {
   if (!sys) return BDEM_ERR_ARG;
@@ -1994,10 +1010,9 @@ int bdem_pcg_iterate(const bdem_system_t *sys, double *x, double *r, double *zv,
                      double *ap, int n_iter, void *stream) {
   if (!sys || n_iter < 0) return BDEM_ERR_ARG;
   cudaStream_t st = as_stream(stream);
-  // PDL chain for the slot-parallel SpMV kernels (0, 4)
-  const bool shfl = spmv_kernel() == 4 && sys->shfl_src && sys->shfl_jbase;
-  auto spmv_k = shfl ? k_spmv_shfl : k_spmv;
-  const bool pdl = pdl_enabled() && (spmv_kernel() == 0 || shfl);
+  // programmatic dependent launch chain SpMV -> update -> p update
+  auto spmv_k = k_spmv;
+  const bool pdl = pdl_enabled();
   const unsigned int fg = upd_fused_grid(*sys);
   if (fg > 0) {
     for (int it = 0; it < n_iter; ++it) {

@@ -39,66 +39,12 @@ def _ptr(t) -> int:
     return 0 if t is None else t.data_ptr()
 
 
-def _spread3(v):
-    """Spread the low 21 bits of v so bit k lands at bit 3k (Morton interleave)."""
-    v = v.astype(np.uint64) & np.uint64(0x1FFFFF)
-    for shift, mask in ((32, 0x1F00000000FFFF), (16, 0x1F0000FF0000FF), (8, 0x100F00F00F00F00F),
-                        (4, 0x10C30C30C30C30C3), (2, 0x1249249249249249)):
-        v = (v | (v << np.uint64(shift))) & np.uint64(mask)
-    return v
-
-
-def z_order(p: np.ndarray, cell: float) -> np.ndarray:
-    """Elements sorted along a Z-order curve of cells of size ``cell``, ties by id.
-
-    Consecutive runs of 32..128 elements then form compact patches, so the
-    bonds of a SELL tile mostly join two rows of the same tile."""
-    p = np.asarray(p, dtype=float)
-    if p.shape[0] == 0:
-        return np.zeros(0, dtype=np.int64)
-    g = np.floor((p - p.min(axis=0)) / max(cell, 1e-300))
-    g = np.clip(g, 0, 2**21 - 1).astype(np.uint64)
-    key = _spread3(g[:, 0]) | (_spread3(g[:, 1]) << np.uint64(1)) | (_spread3(g[:, 2]) << np.uint64(2))
-    return np.argsort(key, kind="stable")
-
-
-def strip_order(p: np.ndarray, a: float, width: int = 32) -> np.ndarray:
-    """Strip-major order: strips ``width`` spacings wide along the longest
-    axis, then layers, rows, and position inside the row.  Sheet-like scenes
-    are first rotated into their principal axes (a tilted plate keeps its
-    lattice rows).  A slice is then 32 consecutive elements of one lattice
-    row and its row neighbours sit in the adjacent slices, at fixed offsets."""
-    p = np.asarray(p, dtype=float)
-    c = p - p.mean(axis=0)
-    ext = c.max(axis=0) - c.min(axis=0)
-    if ext.min() < 0.1 * ext.max():          # sheet: use in-plane principal axes
-        _, _, vt = np.linalg.svd(c[:: max(1, c.shape[0] // 20000)], full_matrices=False)
-        c = c @ vt.T
-        ext = c.max(axis=0) - c.min(axis=0)
-    ax = np.argsort(-ext, kind="stable")
-    u = [c[:, k] - c[:, k].min() for k in ax]
-    strip = np.floor(u[0] / (width * a) + 1e-9).astype(np.int64)
-    row = np.round(u[1] / (0.5 * a)).astype(np.int64)
-    layer = np.round(u[2] / (0.5 * a)).astype(np.int64)
-    return np.lexsort((u[0], row, layer, strip))
-
-
-def row_order(el, mode: str | None = None) -> np.ndarray:
-    """SELL row order: the caller's element order (default: on lattices its
-    neighbour offsets are constant, so the SpMV's j-role and x gathers are
-    shift-coalesced) or a Z-order of the initial positions (``BDEM_ROW_ORDER=z``:
-    compact tiles for the tiled SpMV variant)."""
-    import os
-    mode = mode or os.environ.get("BDEM_ROW_ORDER", "id")
-    n = int(el.p.shape[0])
-    if mode == "id" or n == 0:
-        return np.arange(n, dtype=np.int64)
-    cell = 2.0 * float(np.median(np.asarray(el.radius)))
-    if mode == "strip":
-        return strip_order(el.p, cell)
-    if mode.startswith("strip") and mode[5:].isdigit():    # e.g. strip8: 8-wide strips
-        return strip_order(el.p, cell, width=int(mode[5:]))
-    return z_order(el.p, cell)
+def row_order(el) -> np.ndarray:
+    """SELL row order: the caller's element order.  On lattices the neighbour
+    offsets are then constant, so the SpMV's j-role and x gathers are
+    shift-coalesced (Z-order and strip-major orders were measured for the
+    tiled SpMV variants and lost, profiles/r01/README.md)."""
+    return np.arange(int(el.p.shape[0]), dtype=np.int64)
 
 
 class SellLayout:
@@ -146,127 +92,6 @@ class SellLayout:
         self.row_slot[:n] = slot[rows]
         self.slice_slot = np.zeros(ns + 1, dtype=np.int64)
         np.cumsum(free_row.reshape(ns, 32).sum(axis=1), out=self.slice_slot[1:])
-
-    def sym_tables(self, bi, bj, slot, ts: int, kcap: int):
-        """Tables of the contribution-table SpMV for tiles of ``ts`` slices.
-
-        A bond whose two rows lie in one tile gets the table slot
-        ``rank * R + (row_j - tile_row0)`` (R = 32 ts; rank = its order among
-        row j's in-tile bonds, ascending bond id); the others -- and in-tile
-        bonds beyond ``kcap`` -- stay in boundary-only j-role lists of the
-        usual SELL shape."""
-        n = self.elem_row.shape[0]
-        ns = self.n_slices
-        R = 32 * max(ts, 1)
-        ri, rj = self.elem_row[bi], self.elem_row[bj]
-        same = (ri // R) == (rj // R)
-        order = np.lexsort((np.arange(bi.shape[0]), rj))          # by row j, then bond id
-        rank = np.empty(bi.shape[0], dtype=np.int64)
-        same_sorted = same[order]
-        cs = np.cumsum(same_sorted) - same_sorted                  # in-tile bonds before, globally
-        rj_sorted = rj[order]
-        first = np.ones(order.shape[0], dtype=bool)
-        first[1:] = rj_sorted[1:] != rj_sorted[:-1]
-        base = np.maximum.accumulate(np.where(first, cs, 0))
-        rank[order] = cs - base
-        inside = same & (rank < kcap)
-        jloc = np.full(self.n_pos, -1, dtype=np.int32)
-        jloc[self.pos_of_bond[inside]] = (rank[inside] * R + (rj[inside] % R)).astype(np.int32)
-        kc = int(rank[inside].max()) + 1 if inside.any() else 1
-        bnd = np.nonzero(~inside)[0]
-        jb_base, rank_b, _ = self._slices(rj[bnd], n, ns)
-        nj = int(jb_base[-1])
-        jidx = jb_base[rj[bnd] // 32] + 32 * rank_b + (rj[bnd] % 32)
-        jpos = np.full(max(nj, 1), -1, dtype=np.int32)
-        jslot = np.full(max(nj, 1), -1, dtype=np.int32)
-        jpos[jidx] = self.pos_of_bond[bnd]
-        jslot[jidx] = slot[bi[bnd]]
-        return jloc, jb_base.astype(np.int32), jpos, jslot, kc, float(inside.mean()) if inside.size else 0.0
-
-    def shfl_tables(self, bi, bj, slot):
-        """Tables of the warp-shuffle SpMV (bdem_spmv_set_kernel(4)).
-
-        A bond whose rows i, j (both free) lie in the same slice is handed to
-        row j at its i-role slot k through a warp shuffle from lane(i) to
-        lane(j); a receiving lane takes at most one bond per slot (the lowest
-        sending lane), the others stay in j-role lists of the usual SELL shape.
-        Returns (src int8 per position: sending lane for the receiving lane
-        pos & 31, -1 none), the reduced j-role lists (base, pos, slot) and the
-        handed-over fraction of the bonds."""
-        nb = bi.shape[0]
-        n = self.elem_row.shape[0]
-        ns = self.n_slices
-        src = np.full(max(self.n_pos, 1), -1, dtype=np.int8)
-        if nb == 0:
-            base, _, _ = self._slices(np.zeros(0, dtype=np.int64), n, ns)
-            return src, base.astype(np.int32), np.full(1, -1, np.int32), \
-                np.full(1, -1, np.int32), 0.0
-        ri, rj = self.elem_row[bi], self.elem_row[bj]
-        pos = self.pos_of_bond
-        k = (pos - self.slice_base[ri // 32]) // 32
-        cand = ((ri // 32) == (rj // 32)) & (slot[bi] >= 0) & (slot[bj] >= 0)
-        # receiving slot key (slice, k, lane_j); keep the lowest sending lane
-        key = (ri // 32) * (self.kmax + 1) * 32 + k * 32 + (rj % 32)
-        c = np.nonzero(cand)[0]
-        order = c[np.lexsort((ri[c] % 32, key[c]))]
-        first = np.ones(order.shape[0], dtype=bool)
-        first[1:] = key[order][1:] != key[order][:-1]
-        handed = np.zeros(nb, dtype=bool)
-        handed[order[first]] = True
-        h = np.nonzero(handed)[0]
-        recv_pos = self.slice_base[ri[h] // 32] + 32 * k[h] + (rj[h] % 32)
-        src[recv_pos] = (ri[h] % 32).astype(np.int8)
-        rest = np.nonzero(~handed)[0]
-        jb_base, rank_b, _ = self._slices(rj[rest], n, ns)
-        nj = int(jb_base[-1])
-        jidx = jb_base[rj[rest] // 32] + 32 * rank_b + (rj[rest] % 32)
-        jpos = np.full(max(nj, 1), -1, dtype=np.int32)
-        jslot = np.full(max(nj, 1), -1, dtype=np.int32)
-        jpos[jidx] = pos[rest]
-        jslot[jidx] = slot[bi[rest]]
-        return src, jb_base.astype(np.int32), jpos, jslot, float(handed.mean())
-
-    def wave_tables(self, bi, bj, slot, ring_slices: int):
-        """Tables of the dataflow SpMV: per j-role list entry the ring slot its
-        bond's i-role pass writes row j's product to (-1 when either end is
-        pinned or the entry is padding), and the lag = max slice(j) - slice(i).
-        Returns lag -1 when some bond has row(i) > row(j)."""
-        ri, rj = self.elem_row[bi], self.elem_row[bj]
-        kmax = max(self.kmax, 1)
-        jring = np.full(max(self.n_jpos, 1), -1, dtype=np.int32)
-        if bi.shape[0] == 0:
-            return jring, 0
-        if np.any(ri >= rj):
-            return jring, -1
-        si, sj = ri // 32, rj // 32
-        pos = self.pos_of_bond
-        k = (pos - self.slice_base[si]) // 32
-        ring = ((si % ring_slices) * kmax + k) * 32 + (ri % 32)
-        live = (slot[bi] >= 0) & (slot[bj] >= 0)
-        inv = np.full(self.n_pos, -1, dtype=np.int64)
-        inv[pos[live]] = ring[live]
-        valid = self.jpos >= 0
-        jring[:self.n_jpos][valid] = inv[self.jpos[valid]]
-        lag = int((sj - si)[live].max()) if live.any() else 0
-        return jring, lag
-
-    def tile_headers(self, ts: int, stride: int) -> np.ndarray:
-        """Per-tile header records of the tiled SpMV (see bdem_system_t.tile_hdr)."""
-        ns = self.n_slices
-        if ts <= 0:
-            return np.zeros(max(stride, 1), dtype=np.int32)
-        nt = (ns + ts - 1) // ts
-        t0 = np.arange(nt) * ts
-        t1 = np.minimum(t0 + ts, ns)
-        out = np.zeros((nt, stride), dtype=np.int64)
-        for k in range(ts + 1):
-            sl = np.minimum(t0 + k, t1)
-            out[:, k] = self.slice_base[sl]
-            out[:, ts + 1 + k] = self.jslice_base[sl]
-        out[:, 2 * ts + 2] = self.slice_slot[t0]
-        out[:, 2 * ts + 3] = self.slice_slot[t1]
-        assert out.max() < 2**31
-        return out.astype(np.int32).reshape(-1)
 
     @staticmethod
     def _slices(key, n, ns):
@@ -329,7 +154,7 @@ class DeviceSystem:
         self.nb = nb = int(b.i.shape[0])
         pinned = np.asarray(el.pinned, dtype=bool)
         self.free_np = ~pinned
-        # SELL rows in Z-order; free slots numbered in row order (contiguous per slice)
+        # SELL rows; free slots numbered in row order (contiguous per slice)
         rows = row_order(el)
         slot = np.full(n, -1, dtype=np.int32)
         free_rows = rows[self.free_np[rows]]
@@ -378,24 +203,6 @@ class DeviceSystem:
         self.elem_row = _t(np.append(sell.elem_row, -1).astype(np.int32), I32, dev)
         self.slice_slot = _t(sell.slice_slot.astype(np.int32), I32, dev)
         self.row_slot = _t(sell.row_slot, I32, dev)
-        self.tile_hdr = _t(sell.tile_headers(int(self.lib.bdem_spmv_tile_slices()),
-                                             int(self.lib.bdem_spmv_tile_hdr_ints())), I32, dev)
-        jloc, jbase, jpos_b, jslot_b, kc, self.sym_inside = sell.sym_tables(
-            bi64, bj64, slot, int(self.lib.bdem_spmv_sym_slices()),
-            int(self.lib.bdem_spmv_sym_kcap()))
-        self.sym_jloc = _t(np.append(jloc, -1), I32, dev)
-        self.sym_jbase, self.sym_jpos = _t(jbase, I32, dev), _t(jpos_b, I32, dev)
-        self.sym_jslot, self.sym_kc = _t(jslot_b, I32, dev), kc
-        src, sjb, sjp, sjs, self.shfl_handed = sell.shfl_tables(bi64, bj64, slot)
-        self.shfl_src = _t(src, torch.int8, dev)
-        self.shfl_jbase, self.shfl_jpos = _t(sjb, I32, dev), _t(np.append(sjp, -1), I32, dev)
-        self.shfl_jslot = _t(np.append(sjs, -1), I32, dev)
-        ring = 4096
-        jring, lag = sell.wave_tables(bi64, bj64, slot, ring)
-        self.wave_jring, self.wave_lag, self.wave_ring_slices = _t(jring, I32, dev), lag, ring
-        self.wave_ring = torch.zeros(6 * ring * max(sell.kmax, 1) * 32, dtype=F64, device=dev)
-        self.wave_ypart = torch.zeros(6 * max(32, (nf + 31) // 32 * 32), dtype=F64, device=dev)
-        self.wave_flags = torch.zeros(2 * sell.n_slices + 4, dtype=I32, device=dev)
         self.pos_of_bond_d = torch.as_tensor(sell.pos_of_bond).to(dev)
         # staging / reduced system
         self.stage = torch.zeros((L.ST["COUNT"], npos), dtype=F64, device=dev)
@@ -444,14 +251,6 @@ class DeviceSystem:
                                           _ptr(self.jslot))
         s.row_elem, s.elem_row = _ptr(self.row_elem), _ptr(self.elem_row)
         s.slice_slot, s.row_slot = _ptr(self.slice_slot), _ptr(self.row_slot)
-        s.tile_hdr = _ptr(self.tile_hdr)
-        s.sym_jloc, s.sym_jbase = _ptr(self.sym_jloc), _ptr(self.sym_jbase)
-        s.sym_jpos, s.sym_jslot, s.sym_kc = _ptr(self.sym_jpos), _ptr(self.sym_jslot), self.sym_kc
-        s.wave_jring, s.wave_lag = _ptr(self.wave_jring), self.wave_lag
-        s.wave_ring_slices, s.wave_ring = self.wave_ring_slices, _ptr(self.wave_ring)
-        s.wave_ypart, s.wave_flags = _ptr(self.wave_ypart), _ptr(self.wave_flags)
-        s.shfl_src, s.shfl_jbase = _ptr(self.shfl_src), _ptr(self.shfl_jbase)
-        s.shfl_jpos, s.shfl_jslot = _ptr(self.shfl_jpos), _ptr(self.shfl_jslot)
         s.stage, s.diag, s.minv = _ptr(self.stage), _ptr(self.diag), _ptr(self.minv)
         s.scoef = _ptr(self.scoef)
         s.red, s.scalars, s.pcg = _ptr(self.red), _ptr(self.scalars), _ptr(self.pcg_state)

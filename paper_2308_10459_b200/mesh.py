@@ -99,70 +99,6 @@ class TetMesh:
         return float(np.sum(self.volumes))
 
 
-def parse_tet_mesh(text: str) -> TetMesh:
-    """``tetmesh <nv> <nt>`` header, ``v x y z`` and ``t i0 i1 i2 i3`` lines
-    (0-based), ``#`` comments and blank lines skipped (geometry.py:100-156)."""
-    content = [(k, ln.strip()) for k, ln in enumerate(text.splitlines())
-               if ln.strip() and not ln.strip().startswith("#")]
-    pos = 0
-
-    def take():
-        nonlocal pos
-        if pos >= len(content):
-            raise MeshError("unexpected end of mesh input")
-        pos += 1
-        return content[pos - 1]
-
-    def fail(lineno, msg):
-        raise MeshError(f"line {lineno + 1}: {msg}")
-
-    lineno, header = take()
-    parts = header.split()
-    if len(parts) != 3 or parts[0] != "tetmesh":
-        fail(lineno, "expected header 'tetmesh <n_vertices> <n_tets>'")
-    try:
-        nv, nt = int(parts[1]), int(parts[2])
-    except ValueError:
-        fail(lineno, "vertex/tet counts must be integers")
-    if nv < 4 or nt < 1:
-        fail(lineno, "mesh needs at least 4 vertices and 1 tet")
-    vertices = np.zeros((nv, 3))
-    for k in range(nv):
-        lineno, line = take()
-        parts = line.split()
-        if len(parts) != 4 or parts[0] != "v":
-            fail(lineno, "expected 'v x y z'")
-        try:
-            vertices[k] = [float(x) for x in parts[1:]]
-        except ValueError:
-            fail(lineno, "vertex coordinates must be numbers")
-    tets = np.zeros((nt, 4), dtype=np.int64)
-    for k in range(nt):
-        lineno, line = take()
-        parts = line.split()
-        if len(parts) != 5 or parts[0] != "t":
-            fail(lineno, "expected 't i0 i1 i2 i3'")
-        try:
-            ids = [int(x) for x in parts[1:]]
-        except ValueError:
-            fail(lineno, "tet indices must be integers")
-        if len(set(ids)) != 4 or min(ids) < 0 or max(ids) >= nv:
-            fail(lineno, f"invalid tet vertex indices {ids}")
-        tets[k] = ids
-    return TetMesh(vertices, tets)
-
-
-def load_tet_mesh(path) -> TetMesh:
-    return parse_tet_mesh(Path(path).read_text())
-
-
-def write_tet_mesh(path, vertices: np.ndarray, tets: np.ndarray):
-    lines = [f"tetmesh {len(vertices)} {len(tets)}"]
-    lines += [f"v {x!r} {y!r} {z!r}" for x, y, z in np.asarray(vertices, dtype=float).tolist()]
-    lines += [f"t {a} {b} {c} {d}" for a, b, c, d in np.asarray(tets, dtype=np.int64).tolist()]
-    Path(path).write_text("\n".join(lines) + "\n")
-
-
 def grid_tet_mesh(nx: int, ny: int, nz: int, h: float, origin=(0.0, 0.0, 0.0)) -> TetMesh:
     """Cube grid, six Kuhn tets per cube, cubes in (i, j, k) order and paths in
     KUHN_PATHS order; a negatively oriented tet swaps its last two corners

@@ -609,87 +609,20 @@ def test_friction_large_wave_path_vs_oracle(cuda_ok):
 
 
 # ---------------------------------------------------------------------------
-# tiled SpMV variant (cp.async.bulk + mbarrier ring, warp-specialised)
+# PCG execution paths (fused update, rotation-free) against the default path
 # ---------------------------------------------------------------------------
-
-def _spmv_both(dev, seed, variant=1):
-    import torch
-    g = torch.Generator(device="cuda").manual_seed(seed)
-    x = torch.randn(6 * dev.vstride, generator=g, dtype=torch.float64, device="cuda")
-    ys = []
-    for kern in (0, variant):
-        prev = dev.lib.bdem_spmv_set_kernel(kern)
-        y = torch.full_like(x, float("nan"))
-        dev.call("bdem_spmv", dev.sysp, x.data_ptr(), y.data_ptr(), dev.stream)
-        torch.cuda.synchronize()
-        dev.lib.bdem_spmv_set_kernel(prev)
-        ys.append(y.view(6, dev.vstride)[:, :dev.nf].cpu().numpy())
-    return ys
-
 
 def _assembled(spec, k_element=None):
     from paper_2308_10459_b200.newton import GPUProblem
     from paper_2308_10459_b200.scene import Scene
-    from paper_2308_10459_b200.step import contact_candidates
+    from paper_2308_10459_b200.step import prepare_step
     scene = Scene.from_spec(spec, host_sync=False)
     if k_element is not None:
         scene.k_element = k_element
+    prepare_step(scene)
     dev = scene.device
-    dev.set_physics(scene.gravity, scene.k_contact, scene.k_element, scene.colliders)
-    dev.set_pairs(contact_candidates(scene))
-    dev.call("bdem_predict", dev.sysp, dev.p.data_ptr(), dev.q.data_ptr(), dev.v.data_ptr(),
-             dev.qdot.data_ptr(), dev.p_prev.data_ptr(), dev.q_prev.data_ptr(), spec.dt,
-             dev.p_hat.data_ptr(), dev.q_hat.data_ptr(), dev.mp_dt2.data_ptr(),
-             dev.mq_dt2.data_ptr(), dev.xp.data_ptr(), dev.xq.data_ptr(), dev.stream)
     GPUProblem(dev).assemble(dev.xp, dev.xq)
     return dev
-
-
-@pytest.mark.parametrize("variant", [1, 2, 3, 4])
-@pytest.mark.parametrize("case", ["plate_z", "cube_random_q", "dense_overflow"])
-def test_tiled_spmv_matches_default(cuda_ok, monkeypatch, case, variant):
-    """Same terms per row as k_spmv; with 8 warps per slice (k_spmv: 4) the
-    slot partials associate differently, so the two agree to round-off."""
-    from paper_2308_10459_b200 import configs as C
-    if case == "plate_z":
-        monkeypatch.setenv("BDEM_ROW_ORDER", {1: "z", 2: "strip", 3: "id", 4: "strip"}[variant])
-        spec = C.plate(nx=100, ny=60, epsilon=1e-6)
-    elif case == "cube_random_q":
-        spec = C.cube(n_side=9, seed=4, random_q=True)
-    else:
-        rng = np.random.default_rng(8)
-        n = 3000
-        pos = rng.uniform(0.0, 0.03, size=(n, 3))
-        rad = np.full(n, 0.002)
-        pairs = C._pairs_within(pos, 0.0042)
-        el = C._elements(pos, C._random_unit_quats(rng, n), rad, 2500.0,
-                         pinned=rng.random(n) < 0.05)
-        b = C.build_bonds(pos, rad, pairs, 1e7, 4e6)
-        spec = C.SceneSpec("dense", el, b, 1e-4, 1e7, 4e6, 2500.0)
-    dev = _assembled(spec)
-    if case == "dense_overflow":
-        assert dev.sell.kmax > 8 and dev.sell.kjmax > 8   # beyond the staged slots
-    if variant == 2:
-        assert 0.0 < dev.sym_inside <= 1.0
-    if variant == 3:
-        assert 0 <= dev.wave_lag and 4 * (dev.wave_lag + 1) <= dev.wave_ring_slices
-    if variant == 4 and case == "plate_z":
-        assert dev.shfl_handed > 0.5            # most bonds handed over in-slice
-    y0, y1 = _spmv_both(dev, 11, variant)
-    assert np.all(np.isfinite(y0))
-    np.testing.assert_allclose(y1, y0, rtol=1e-12, atol=1e-13 * np.abs(y0).max())
-
-
-@pytest.mark.parametrize("variant", [1, 2, 3, 4])
-def test_tiled_spmv_newton_solve_vs_golden(cuda_ok, variant):
-    """The reference Newton solve (newton_solve.npz) through the SpMV variants."""
-    import paper_2308_10459_b200._lib as L
-    lib = L.load()
-    prev = lib.bdem_spmv_set_kernel(variant)
-    try:
-        test_newton_solve_vs_golden(cuda_ok)
-    finally:
-        lib.bdem_spmv_set_kernel(prev)
 
 
 def test_fused_pcg_update_bit_identical(cuda_ok):
@@ -706,14 +639,18 @@ def test_fused_pcg_update_bit_identical(cuda_ok):
         try:
             dev.call("bdem_pcg_init", dev.sysp, dev.z.data_ptr(), -1.0, *ptrs, 1e-7, 3000, 0.0,
                      dev.stream)
+            n0 = dev.lib.bdem_launch_count()
             for _ in range(50):
                 dev.call("bdem_pcg_iterate", dev.sysp, *ptrs, dev.ap.data_ptr(), 64, dev.stream)
+            per_it = (dev.lib.bdem_launch_count() - n0) / (50 * 64)
             torch.cuda.synchronize()
         finally:
             dev.lib.bdem_pcg_set_fused(prev)
         st = dev.pcg_state.cpu().numpy().copy()
-        out.append((st, dev.y.cpu().numpy().copy(), dev.pv.cpu().numpy().copy()))
-    (s0, y0, p0), (s1, y1, p1) = out
+        out.append((st, dev.y.cpu().numpy().copy(), dev.pv.cpu().numpy().copy(), per_it))
+    (s0, y0, p0, k0), (s1, y1, p1, k1) = out
+    # the fused path really ran: SpMV + one update kernel per iteration, not 3
+    assert (k0, k1) == (3.0, 2.0)
     assert s0[13] in (1, 3) and s0[11] > 50   # stopped (converged / max-it) after many iterations
     assert np.array_equal(s0, s1)
     assert np.array_equal(y0, y1) and np.array_equal(p0, p1)
@@ -773,16 +710,25 @@ def test_rot_skip_with_fracture_and_fused_update(cuda_ok):
             spec = C.cube(n_side=6, random_q=False, seed=3, youngs=3e8, k_contact=1e9, speed=2.0,
                           dt=1e-4)
             scene = Scene.from_spec(spec)
-            recs, events = [], []
+            recs, events, flags = [], [], []
+            n0 = lib.bdem_launch_count()
             for _ in range(6):
                 scene.colliders = spec.collider_schedule(scene.time + scene.dt)
                 rep = stable_step(scene, SolverConfig(epsilon=1e-6, max_iterations=300))
                 recs.append((rep.committed, rep.solve.iterations, rep.solve.pcg_total))
                 events.append([b for (b, _, _) in rep.broken])
+                flags.append(float(scene.device.pcg_state[L.PCG["ROTZERO"]].item()))
+            launches = lib.bdem_launch_count() - n0
         finally:
             lib.bdem_pcg_set_rot_skip(prev_s)
             lib.bdem_pcg_set_fused(prev_f)
-        out.append((recs, events, scene.elements.p.copy(), scene.elements.q.copy()))
-    (r0, e0, p0, q0), (r1, e1, p1, q1) = out
+        out.append((recs, events, scene.elements.p.copy(), scene.elements.q.copy(), flags,
+                    launches))
+    (r0, e0, p0, q0, f0, n0), (r1, e1, p1, q1, f1, n1) = out
     assert r0 == r1 and e0 == e1
     assert np.array_equal(p0, p1) and np.array_equal(q0, q1)
+    # the run exercised what it is named for: bonds broke, the rotation half
+    # was skipped, and the fused update replaced two kernels per PCG iteration
+    assert sum(len(e) for e in e0) > 0
+    assert all(f == 0.0 for f in f0) and all(f == 1.0 for f in f1)
+    assert n1 < n0

@@ -44,27 +44,6 @@ def test_drop_scene_elements_and_bonds(gold):
                           M.boundary_masks(spec.mesh) != 0)
 
 
-def test_tetmesh_text_round_trip(tmp_path):
-    m = M.grid_tet_mesh(2, 1, 1, 0.5)
-    path = tmp_path / "m.tet"
-    M.write_tet_mesh(path, m.vertices, m.tets)
-    r = M.load_tet_mesh(path)
-    assert np.array_equal(r.vertices, m.vertices) and np.array_equal(r.tets, m.tets)
-    text = "# comment\n\n" + path.read_text()
-    assert np.array_equal(M.parse_tet_mesh(text).interior, m.interior)
-
-
-@pytest.mark.parametrize("text,msg", [
-    ("mesh 4 1\n", "expected header"),
-    ("tetmesh 4 1\nv 0 0 0\nv 1 0 0\nv 0 1 0\nv 0 0 1\nt 0 1 2 9\n", "invalid tet vertex"),
-    ("tetmesh 4 1\nv 0 0 0\nv 1 0 0\nv 0 1 0\n", "unexpected end"),
-    ("tetmesh 4 1\nv 0 0 0\nv 1 0 0\nv 0 1 0\nv 0 0 1\nt 0 2 1 3\n", "inverted or flat"),
-])
-def test_tetmesh_errors(text, msg):
-    with pytest.raises(M.MeshError, match=msg):
-        M.parse_tet_mesh(text)
-
-
 def test_non_manifold_face():
     v = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [0, 0, -1], [1, 1, 1.0]])
     tets = np.array([[0, 1, 2, 3], [0, 2, 1, 4], [0, 1, 2, 5]])
