@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define BDEM_ABI_VERSION 4
+#define BDEM_ABI_VERSION 5
 
 enum {
   BDEM_OK = 0,
@@ -41,7 +41,8 @@ enum {
   BDEM_ERR_ANTIPODAL = 2,       /* bonds.py:223-227 DegenerateShearError  */
   BDEM_ERR_NONFINITE = 3,
   BDEM_ERR_ARG = 4,
-  BDEM_ERR_CUDA = 5
+  BDEM_ERR_CUDA = 5,
+  BDEM_ERR_CAPACITY = 6         /* output larger than the given capacity */
 };
 
 /* device error words (int32) in sys->err */
@@ -373,6 +374,33 @@ int64_t bdem_broadphase_workspace(int64_t n);
 int bdem_broadphase(const double *p, const double *radii, int64_t n, double cell,
                     const int64_t *labels, void *work, int32_t *pairs, int64_t cap,
                     int64_t *n_out, void *stream);
+
+/* The step's frozen self-contact candidates, straight into the system
+ * (contact_candidates, solver.py:856-878): radii inflated by dt |v| +
+ * dt^2 |g| (dt2g = dt^2 |g| from the host) written to `radii` (n doubles),
+ * cell = 2 max(inflated) + 1e-12 formed on the device, the broad phase
+ * restricted to labels[i] != labels[j], pairs written to sys->pair_i/pair_j
+ * (ascending) and their element adjacency (pi_ptr, pj_ptr, pj_idx).  Sets
+ * sys->n_pair and *n_out (host); returns BDEM_ERR_CAPACITY with the needed
+ * count in *n_out when it exceeds sys->pair_cap.  Synchronises `stream`
+ * twice (grid bounds, pair count).  bp_work: bdem_broadphase_workspace(n);
+ * adj_work: bdem_pair_adjacency_workspace(n, pair_cap) bytes. */
+int bdem_contact_pairs(bdem_system_t *sys, const double *p, const double *v, double dt,
+                       double dt2g, const int64_t *labels, void *bp_work, void *adj_work,
+                       double *radii, int64_t *n_out, void *stream);
+int64_t bdem_pair_adjacency_workspace(int64_t n, int64_t cap);
+/* Install caller-given pairs ((m,2) int32 device array, sorted i<j) and
+ * their element adjacency; sets sys->n_pair. */
+int bdem_set_pairs(bdem_system_t *sys, const int32_t *pairs, int64_t m, void *work,
+                   void *stream);
+
+/* Element rows <-> a packed buffer (m x 14 doubles: p, q, v, qdot) for the
+ * listed ids: to_buf=1 gathers (pinned-state backup, solver.py:894-896),
+ * to_buf=0 scatters (restore, :910-916; driver rows at t + dt, :898-900). */
+int bdem_rows_copy(const int32_t *ids, int64_t m, double *p, double *q, double *v,
+                   double *qdot, double *buf, int to_buf, void *stream);
+/* Zero the device error words (first-index slots to INT32_MAX). */
+int bdem_reset_errors(const bdem_system_t *sys, void *stream);
 
 /* Connected components over non-broken bonds with labels numbered in order of
  * each component's smallest element (label_components, geometry.py:295-310).

@@ -12,7 +12,7 @@ import os
 from ._build import lib_path
 
 BDEM_OK = 0
-ERR_DEGENERATE_BOND, ERR_ANTIPODAL, ERR_NONFINITE, ERR_ARG, ERR_CUDA = 1, 2, 3, 4, 5
+ERR_DEGENERATE_BOND, ERR_ANTIPODAL, ERR_NONFINITE, ERR_ARG, ERR_CUDA, ERR_CAPACITY = 1, 2, 3, 4, 5, 6
 ERRSLOT_DEG_COUNT, ERRSLOT_DEG_FIRST, ERRSLOT_ANTI_COUNT, ERRSLOT_ANTI_FIRST = 0, 1, 2, 3
 ERRSLOT_COUNT = 8
 
@@ -28,7 +28,7 @@ SC = dict(F=0, GNORM2=1, CNORM2=2, MAXDEV=3, SLOPE=4, FT=5, NSING=6, EBOND=7, EC
 PCG = dict(RZ=0, PAP=1, ALPHA=2, BETA=3, RR=4, BNORM=5, REL=6, TOL=7, BOOST=8, APNORM2=9,
            PNORM2=10, K=11, MAXIT=12, STATE=13, ROTZERO=14, COUNT=16)
 PCG_RUNNING, PCG_CONVERGED, PCG_BREAKDOWN, PCG_MAXIT = 0, 1, 2, 3
-ABI_VERSION = 4
+ABI_VERSION = 5
 RED_BLOCKS = 1184
 MAX_COLLIDERS = 8
 N_COUNTERS = 16
@@ -93,6 +93,12 @@ SIGNATURES = {
     "bdem_precond_apply": (_int, [_sys, _p, _p, _p]),
     "bdem_broadphase_workspace": (_i64, [_i64]),
     "bdem_broadphase": (_int, [_p, _p, _i64, _dbl, _p, _p, _p, _i64, C.POINTER(C.c_int64), _p]),
+    "bdem_contact_pairs": (_int, [_p, _p, _p, _dbl, _dbl, _p, _p, _p, _p,
+                                  C.POINTER(C.c_int64), _p]),
+    "bdem_pair_adjacency_workspace": (_i64, [_i64, _i64]),
+    "bdem_set_pairs": (_int, [_p, _p, _i64, _p, _p]),
+    "bdem_rows_copy": (_int, [_p, _i64, _p, _p, _p, _p, _p, _int, _p]),
+    "bdem_reset_errors": (_int, [_p, _p]),
     "bdem_components_workspace": (_i64, [_i64]),
     "bdem_components": (_int, [_i64, _i64, _p, _p, _p, _p, _p, C.POINTER(C.c_int64), _p]),
     "bdem_select_workspace": (_i64, [_i64]),

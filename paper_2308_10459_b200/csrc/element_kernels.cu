@@ -426,6 +426,35 @@ __global__ void __launch_bounds__(kThreads) k_dot(bdem_system_t S, const double 
   }
 }
 
+// element rows <-> a packed buffer of 14 doubles per listed element (p 3,
+// q 4, v 3, qdot 4): the pinned-state backup / restore of stable_step
+// (solver.py:894-896, 910-916) and the driver rows at t + dt (:898-900)
+__global__ void k_rows_copy(const int32_t *ids, int64_t m, double *p, double *q, double *v,
+                            double *qdot, double *buf, int to_buf) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int64_t e = ids[k];
+  double *r = buf + 14 * k;
+  if (to_buf) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) { r[c] = p[3 * e + c]; r[7 + c] = v[3 * e + c]; }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) { r[3 + c] = q[4 * e + c]; r[10 + c] = qdot[4 * e + c]; }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) { p[3 * e + c] = r[c]; v[3 * e + c] = r[7 + c]; }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) { q[4 * e + c] = r[3 + c]; qdot[4 * e + c] = r[10 + c]; }
+  }
+}
+
+__global__ void k_reset_errors(int32_t *err) {
+  const int t = threadIdx.x;
+  if (t < BDEM_ERRSLOT_COUNT)
+    err[t] = (t == BDEM_ERRSLOT_DEGENERATE_FIRST || t == BDEM_ERRSLOT_ANTIPODAL_FIRST)
+                 ? 0x7fffffff : 0;
+}
+
 }  // namespace bdem
 
 using namespace bdem;
@@ -509,6 +538,20 @@ int bdem_finish_step(const bdem_system_t *sys, const double *p, const double *q,
   if (sys->n_free == 0) return BDEM_OK;
   k_finish_step<<<grid_for(sys->n_free), kThreads, 0, as_stream(stream)>>>(*sys, p, q, p_c, q_c,
                                                                            dt, v, qdot);
+  return launch_status();
+}
+
+int bdem_rows_copy(const int32_t *ids, int64_t m, double *p, double *q, double *v,
+                   double *qdot, double *buf, int to_buf, void *stream) {
+  if (m < 0) return BDEM_ERR_ARG;
+  if (m == 0) return BDEM_OK;
+  k_rows_copy<<<grid_for(m), kThreads, 0, as_stream(stream)>>>(ids, m, p, q, v, qdot, buf, to_buf);
+  return launch_status();
+}
+
+int bdem_reset_errors(const bdem_system_t *sys, void *stream) {
+  if (!sys) return BDEM_ERR_ARG;
+  k_reset_errors<<<1, 32, 0, as_stream(stream)>>>(sys->err);
   return launch_status();
 }
 

@@ -17,12 +17,51 @@ namespace bdem {
 struct GridHdr {
   long long lo[3];
   long long hi[3];
+  unsigned long long rmax_bits;  // max inflated radius (non-negative double's bits)
+  double cell;
 };
 
-__global__ void k_cells(const double *p, int64_t n, double cell, long long *cxyz,
+// contact_candidates (solver.py:866-870): inflated radii r + dt |v| +
+// dt^2 |g| with numpy's order of operations (|v| = sqrt((x x + y y) + z z);
+// travel = dt |v|; travel += dt2g; r + travel), and their maximum (the bits
+// of non-negative doubles order like the values)
+__global__ void k_inflate(const double *v, const double *radius, int64_t n, double dt,
+                          double dt2g, double *out, GridHdr *hdr) {
+  __shared__ unsigned long long sh[kThreads / 32];
+  unsigned long long m = 0ull;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double x = v[3 * e], y = v[3 * e + 1], z = v[3 * e + 2];
+    double travel = dt * sqrt((x * x + y * y) + z * z);
+    travel += dt2g;
+    const double r = radius[e] + travel;
+    out[e] = r;
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(r);
+    m = bits > m ? bits : m;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long u = __shfl_xor_sync(0xffffffffu, m, o);
+    m = u > m ? u : m;
+  }
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < kThreads / 32; ++k) m = sh[k] > m ? sh[k] : m;
+    atomicMax(&hdr->rmax_bits, m);
+  }
+}
+
+// cell = 2 max(inflated) + 1e-12 (solver.py:871), on the device
+__global__ void k_cell_from_rmax(GridHdr *hdr) {
+  hdr->cell = 2.0 * __longlong_as_double((long long)hdr->rmax_bits) + 1e-12;
+}
+
+__global__ void k_cells(const double *p, int64_t n, const GridHdr *cellh, long long *cxyz,
                         GridHdr *hdr) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n) return;
+  const double cell = cellh->cell;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     const long long v = (long long)floor(p[3 * e + c] / cell);
@@ -58,11 +97,13 @@ __device__ __forceinline__ int64_t lower_bound(const unsigned long long *k, int6
   return lo;
 }
 
-// pass 0: count pairs per element a (a < b); pass 1: write and sort them
+// pass 0: count pairs per element a (a < b); pass 1: write and sort them,
+// interleaved (pairs) or as two planes (pi, pj) when pairs == NULL
 __global__ void k_pairs(const double *p, const double *rad, int64_t n, const long long *cxyz,
                         GridHdr hdr, long long ny, long long nz, const unsigned long long *skeys,
                         const int32_t *sids, const int64_t *labels, int32_t *count,
-                        const int64_t *offs, int32_t *pairs, int pass) {
+                        const int64_t *offs, int32_t *pairs, int pass, int32_t *pi = nullptr,
+                        int32_t *pj = nullptr) {
   const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (a >= n) return;
   const long long cx = cxyz[3 * a], cy = cxyz[3 * a + 1], cz = cxyz[3 * a + 2];
@@ -83,7 +124,7 @@ __global__ void k_pairs(const double *p, const double *rad, int64_t n, const lon
                      d2 = p[3 * (int64_t)b + 2] - pa2;
         const double dist = sqrt((d0 * d0 + d1 * d1) + d2 * d2);
         if (!(dist < ra + rad[b])) continue;
-        if (pass) {
+        if (pass && pairs) {
           // insertion into the sorted segment [base, base+cnt)
           int64_t w = base + cnt;
           while (w > base && pairs[2 * (w - 1) + 1] > b) {
@@ -93,6 +134,14 @@ __global__ void k_pairs(const double *p, const double *rad, int64_t n, const lon
           }
           pairs[2 * w] = (int32_t)a;
           pairs[2 * w + 1] = b;
+        } else if (pass) {
+          int64_t w = base + cnt;
+          while (w > base && pj[w - 1] > b) {
+            pj[w] = pj[w - 1];
+            --w;
+          }
+          pj[w] = b;
+          pi[base + cnt] = (int32_t)a;
         }
         ++cnt;
       }
@@ -137,6 +186,27 @@ __global__ void k_cc_label(const int32_t *parent, const int32_t *rank, int64_t n
   if (e < n) labels[e] = rank[parent[e]];
 }
 
+// ---------------------------------------------------------------------------
+// element adjacency of the frozen contact pairs (sorted i<j): pairs with
+// i == e are [pi_ptr[e], pi_ptr[e+1]); pairs with j == e are
+// pj_idx[pj_ptr[e] .. pj_ptr[e+1]) in ascending pair order
+// ---------------------------------------------------------------------------
+__global__ void k_pair_counts(const int32_t *pi, const int32_t *pj, int64_t m, int32_t *ci,
+                              int32_t *cj, int32_t *iota) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  atomicAdd(&ci[pi[k]], 1);
+  atomicAdd(&cj[pj[k]], 1);
+  iota[k] = (int32_t)k;
+}
+
+__global__ void k_split_pairs(const int32_t *pairs, int64_t m, int32_t *pi, int32_t *pj) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  pi[k] = pairs[2 * k];
+  pj[k] = pairs[2 * k + 1];
+}
+
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace bdem
@@ -175,17 +245,14 @@ int64_t bdem_broadphase_workspace(int64_t n) {
   return (int64_t)b;
 }
 
-int bdem_broadphase(const double *p, const double *radii, int64_t n, double cell,
-                    const int64_t *labels, void *work, int32_t *pairs, int64_t cap,
-                    int64_t *n_out, void *stream) {
-  if (n < 0 || !(cell > 0.0) || !n_out) return BDEM_ERR_ARG;
-  cudaStream_t st = as_stream(stream);
-  if (n < 2) {
-    *n_out = 0;
-    return BDEM_OK;
-  }
-  char *w = static_cast<char *>(work);
-  GridHdr *hdr = reinterpret_cast<GridHdr *>(w); w += align256(sizeof(GridHdr));
+// the broad phase proper; the cell size is hdr->cell on the device (set by
+// the caller: a host value copied in, or k_cell_from_rmax).  Writes
+// interleaved pairs, or two planes (pi, pj) when pairs == NULL and pi != NULL;
+// with no output buffer only counts.
+static int broadphase_impl(const double *p, const double *radii, int64_t n,
+                           const int64_t *labels, char *w, GridHdr *hdr, int32_t *pairs,
+                           int32_t *pi, int32_t *pj, int64_t cap, int64_t *n_out,
+                           cudaStream_t st, int64_t launched) {
   long long *cxyz = reinterpret_cast<long long *>(w); w += align256(sizeof(long long) * 3 * n);
   unsigned long long *keys = reinterpret_cast<unsigned long long *>(w); w += align256(sizeof(unsigned long long) * n);
   unsigned long long *skeys = reinterpret_cast<unsigned long long *>(w); w += align256(sizeof(unsigned long long) * n);
@@ -196,10 +263,7 @@ int bdem_broadphase(const double *p, const double *radii, int64_t n, double cell
   void *cub_tmp = w;
   size_t cub_bytes = bp_cub_bytes(n);
 
-  GridHdr h0;
-  for (int c = 0; c < 3; ++c) { h0.lo[c] = LLONG_MAX; h0.hi[c] = LLONG_MIN; }
-  cudaMemcpyAsync(hdr, &h0, sizeof(GridHdr), cudaMemcpyHostToDevice, st);
-  k_cells<<<grid_for(n), kThreads, 0, st>>>(p, n, cell, cxyz, hdr);
+  k_cells<<<grid_for(n), kThreads, 0, st>>>(p, n, hdr, cxyz, hdr);
   GridHdr h;
   cudaMemcpyAsync(&h, hdr, sizeof(GridHdr), cudaMemcpyDeviceToHost, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) return BDEM_ERR_CUDA;
@@ -218,11 +282,108 @@ int bdem_broadphase(const double *p, const double *radii, int64_t n, double cell
   cudaMemcpyAsync(&total, offs + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) return BDEM_ERR_CUDA;
   *n_out = total;
-  if (pairs == nullptr || total == 0) return launch_status(5);
-  if (total > cap) return BDEM_ERR_ARG;
+  if ((pairs == nullptr && pi == nullptr) || total == 0) return launch_status(launched + 5);
+  if (total > cap) return BDEM_ERR_CAPACITY;
   k_pairs<<<grid_for(n), kThreads, 0, st>>>(p, radii, n, cxyz, h, ny, nz, skeys, sids, labels, cnt,
-                                            offs, pairs, 1);
-  return launch_status(1);
+                                            offs, pairs, 1, pi, pj);
+  return launch_status(launched + 6);
+}
+
+int bdem_broadphase(const double *p, const double *radii, int64_t n, double cell,
+                    const int64_t *labels, void *work, int32_t *pairs, int64_t cap,
+                    int64_t *n_out, void *stream) {
+  if (n < 0 || !(cell > 0.0) || !n_out) return BDEM_ERR_ARG;
+  cudaStream_t st = as_stream(stream);
+  if (n < 2) {
+    *n_out = 0;
+    return BDEM_OK;
+  }
+  char *w = static_cast<char *>(work);
+  GridHdr *hdr = reinterpret_cast<GridHdr *>(w); w += align256(sizeof(GridHdr));
+  GridHdr h0;
+  for (int c = 0; c < 3; ++c) { h0.lo[c] = LLONG_MAX; h0.hi[c] = LLONG_MIN; }
+  h0.rmax_bits = 0ull;
+  h0.cell = cell;
+  cudaMemcpyAsync(hdr, &h0, sizeof(GridHdr), cudaMemcpyHostToDevice, st);
+  return broadphase_impl(p, radii, n, labels, w, hdr, pairs, nullptr, nullptr, cap, n_out, st, 0);
+}
+
+int64_t bdem_pair_adjacency_workspace(int64_t n, int64_t cap) {
+  if (n < 1) n = 1;
+  if (cap < 1) cap = 1;
+  size_t scan_b = 0, sort_b = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_b, (int32_t *)nullptr, (int32_t *)nullptr,
+                                (int)n + 1);
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_b, (int32_t *)nullptr, (int32_t *)nullptr,
+                                  (int32_t *)nullptr, (int32_t *)nullptr, (int)cap);
+  return (int64_t)(2 * align256(sizeof(int32_t) * (n + 1)) + 2 * align256(sizeof(int32_t) * cap) +
+                   align256(scan_b > sort_b ? scan_b : sort_b));
+}
+
+// element adjacency of sys->pair_i/pair_j (n_pair pairs, sorted i<j)
+static int pair_adjacency(const bdem_system_t *sys, void *work, cudaStream_t st) {
+  const int64_t n = sys->n_elem, m = sys->n_pair;
+  if (m == 0) return BDEM_OK;
+  char *w = static_cast<char *>(work);
+  int32_t *ci = reinterpret_cast<int32_t *>(w); w += align256(sizeof(int32_t) * (n + 1));
+  int32_t *cj = reinterpret_cast<int32_t *>(w); w += align256(sizeof(int32_t) * (n + 1));
+  int32_t *iota = reinterpret_cast<int32_t *>(w); w += align256(sizeof(int32_t) * sys->pair_cap);
+  int32_t *kout = reinterpret_cast<int32_t *>(w); w += align256(sizeof(int32_t) * sys->pair_cap);
+  void *cub_tmp = w;
+  size_t scan_b = 0, sort_b = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_b, ci, (int32_t *)nullptr, (int)n + 1);
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_b, (int32_t *)nullptr, (int32_t *)nullptr,
+                                  (int32_t *)nullptr, (int32_t *)nullptr, (int)sys->pair_cap);
+  size_t tmp_b = scan_b > sort_b ? scan_b : sort_b;
+  cudaMemsetAsync(ci, 0, sizeof(int32_t) * (n + 1), st);
+  cudaMemsetAsync(cj, 0, sizeof(int32_t) * (n + 1), st);
+  k_pair_counts<<<grid_for(m), kThreads, 0, st>>>(sys->pair_i, sys->pair_j, m, ci, cj, iota);
+  cub::DeviceScan::ExclusiveSum(cub_tmp, tmp_b, ci, const_cast<int32_t *>(sys->pi_ptr), (int)n + 1, st);
+  cub::DeviceScan::ExclusiveSum(cub_tmp, tmp_b, cj, const_cast<int32_t *>(sys->pj_ptr), (int)n + 1, st);
+  // stable radix sort by j: pair indices ascending within each j
+  int end_bit = 1;
+  while (end_bit < 31 && (n >> end_bit) != 0) ++end_bit;
+  cub::DeviceRadixSort::SortPairs(cub_tmp, tmp_b, sys->pair_j, kout, iota,
+                                  const_cast<int32_t *>(sys->pj_idx), (int)m, 0, end_bit, st);
+  return launch_status(4);
+}
+
+int bdem_set_pairs(bdem_system_t *sys, const int32_t *pairs, int64_t m, void *work,
+                   void *stream) {
+  if (!sys || m < 0 || m > sys->pair_cap) return BDEM_ERR_ARG;
+  cudaStream_t st = as_stream(stream);
+  sys->n_pair = m;
+  if (m == 0) return BDEM_OK;
+  k_split_pairs<<<grid_for(m), kThreads, 0, st>>>(pairs, m, const_cast<int32_t *>(sys->pair_i),
+                                                   const_cast<int32_t *>(sys->pair_j));
+  const int rc = launch_status();
+  return rc != BDEM_OK ? rc : pair_adjacency(sys, work, st);
+}
+
+int bdem_contact_pairs(bdem_system_t *sys, const double *p, const double *v, double dt,
+                       double dt2g, const int64_t *labels, void *bp_work, void *adj_work,
+                       double *radii, int64_t *n_out, void *stream) {
+  if (!sys || !n_out) return BDEM_ERR_ARG;
+  cudaStream_t st = as_stream(stream);
+  const int64_t n = sys->n_elem;
+  sys->n_pair = 0;
+  *n_out = 0;
+  if (n < 2) return BDEM_OK;
+  char *w = static_cast<char *>(bp_work);
+  GridHdr *hdr = reinterpret_cast<GridHdr *>(w); w += align256(sizeof(GridHdr));
+  GridHdr h0;
+  for (int c = 0; c < 3; ++c) { h0.lo[c] = LLONG_MAX; h0.hi[c] = LLONG_MIN; }
+  h0.rmax_bits = 0ull;
+  h0.cell = 0.0;
+  cudaMemcpyAsync(hdr, &h0, sizeof(GridHdr), cudaMemcpyHostToDevice, st);
+  k_inflate<<<kRedBlocks, kThreads, 0, st>>>(v, sys->radius, n, dt, dt2g, radii, hdr);
+  k_cell_from_rmax<<<1, 1, 0, st>>>(hdr);
+  const int rc = broadphase_impl(p, radii, n, labels, w, hdr, nullptr,
+                                 const_cast<int32_t *>(sys->pair_i),
+                                 const_cast<int32_t *>(sys->pair_j), sys->pair_cap, n_out, st, 2);
+  if (rc != BDEM_OK) return rc;
+  sys->n_pair = *n_out;
+  return pair_adjacency(sys, adj_work, st);
 }
 
 static size_t cc_cub_bytes(int64_t n) {

@@ -226,6 +226,11 @@ class DeviceSystem:
         self.h_pcg = torch.zeros(L.PCG["COUNT"], dtype=F64).pin_memory()
         self.h_err = torch.zeros(L.ERRSLOT_COUNT, dtype=I32).pin_memory()
         self._bp_work = None
+        self._bp_need = int(self.lib.bdem_broadphase_workspace(max(n, 1)))
+        # pinned rows: ids and the packed backup of stable_step (p, q, v, qdot)
+        self.pinned_ids = torch.as_tensor(np.nonzero(pinned)[0].astype(np.int32)).to(dev)
+        self.pin_buf = torch.zeros((max(int(self.pinned_ids.numel()), 1), 14), dtype=F64,
+                                   device=dev)
         self._cc_work = None
         self._sel_work = None
         self.launches = 0
@@ -436,6 +441,8 @@ class DeviceSystem:
         self._pair_j = torch.zeros(self.pair_cap, dtype=I32, device=dev)
         s.pair_i, s.pair_j = _ptr(self._pair_i), _ptr(self._pair_j)
         s.pi_ptr, s.pj_ptr, s.pj_idx = _ptr(self.pi_ptr), _ptr(self.pj_ptr), _ptr(self.pj_idx)
+        self._adj_work = torch.empty(int(self.lib.bdem_pair_adjacency_workspace(self.n, cap)),
+                                     dtype=torch.uint8, device=dev)
 
     def set_pairs(self, pairs: torch.Tensor):
         """Install the frozen self-contact candidates of this step ((m,2) int32,
@@ -443,27 +450,55 @@ class DeviceSystem:
         m = int(pairs.shape[0])
         if m > self.pair_cap:
             self._alloc_pairs(max(m, 2 * self.pair_cap))
+        pairs = pairs.to(device=self.device, dtype=I32).contiguous() if m else pairs
+        L.check(self.lib.bdem_set_pairs(self.sysp, pairs.data_ptr() if m else None, m,
+                                        self._adj_work.data_ptr(), self.stream),
+                "bdem_set_pairs")
+        self.launches += 1
         self.n_pair = m
-        self.sys.n_pair = m
-        if m == 0:
-            return
-        pi = pairs[:, 0].contiguous()
-        pj = pairs[:, 1].contiguous()
-        self._pair_i[:m].copy_(pi)
-        self._pair_j[:m].copy_(pj)
-        n = self.n
-        ci = torch.bincount(pi.long(), minlength=n)
-        cj = torch.bincount(pj.long(), minlength=n)
-        self.pi_ptr.zero_()
-        self.pj_ptr.zero_()
-        self.pi_ptr[1:] = torch.cumsum(ci, 0).to(I32)
-        self.pj_ptr[1:] = torch.cumsum(cj, 0).to(I32)
-        order = torch.sort(pj.long(), stable=True).indices
-        self.pj_idx[:m].copy_(order.to(I32))
+
+    def contact_pairs(self, dt: float, dt2g: float, labels) -> int:
+        """The step's frozen self-contact candidates straight into the pair
+        arrays (bdem_contact_pairs: inflated radii, device-side cell size,
+        labelled broad phase, CUB adjacency); returns their count."""
+        if self._bp_work is None or self._bp_work.numel() < self._bp_need:
+            self._bp_work = torch.empty(self._bp_need, dtype=torch.uint8, device=self.device)
+        if getattr(self, "_radii_buf", None) is None:
+            self._radii_buf = torch.empty(max(self.n, 1), dtype=F64, device=self.device)
+        cnt = C.c_int64(0)
+        lab = 0 if labels is None else labels.data_ptr()
+        for _ in range(2):
+            rc = self.lib.bdem_contact_pairs(self.sysp, self.p.data_ptr(), self.v.data_ptr(),
+                                             float(dt), float(dt2g), lab, self._bp_work.data_ptr(),
+                                             self._adj_work.data_ptr(), self._radii_buf.data_ptr(),
+                                             C.byref(cnt), self.stream)
+            if rc != L.ERR_CAPACITY:
+                break
+            self._alloc_pairs(max(int(cnt.value), 2 * self.pair_cap))
+        L.check(rc, "bdem_contact_pairs")
+        self.launches += 1
+        self.n_pair = int(cnt.value)
+        return self.n_pair
+
+    def pair_array(self) -> torch.Tensor:
+        """The installed pairs as an (m, 2) int32 tensor (a view for callers
+        of the reference's (m, 2) API; not used on the step path)."""
+        m = self.n_pair
+        return torch.stack([self._pair_i[:m], self._pair_j[:m]], dim=1)
 
     # ----------------------------------------------------------------- errors
     def reset_errors(self):
-        self.err.copy_(torch.tensor([0, 2**31 - 1, 0, 2**31 - 1, 0, 0, 0, 0], dtype=I32))
+        L.check(self.lib.bdem_reset_errors(self.sysp, self.stream), "bdem_reset_errors")
+
+    # ------------------------------------------------------- element rows
+    def rows_copy(self, ids: torch.Tensor, buf: torch.Tensor, to_buf: bool):
+        """Pinned/driven element rows <-> packed (m, 14) buffer (bdem_rows_copy)."""
+        m = int(ids.numel())
+        if m:
+            L.check(self.lib.bdem_rows_copy(ids.data_ptr(), m, self.p.data_ptr(), self.q.data_ptr(),
+                                            self.v.data_ptr(), self.qdot.data_ptr(), buf.data_ptr(),
+                                            int(to_buf), self.stream), "bdem_rows_copy")
+            self.launches += 1
 
     def bond_id(self, pos: int) -> int:
         """Caller bond index of a SELL position."""

@@ -117,20 +117,27 @@ def label_components(n_elements, bonds, scene=None) -> FragmentLabeling:
     return FragmentLabeling(labels.cpu().numpy())
 
 
+def _candidates_into_system(scene) -> int:
+    """contact_candidates (solver.py:856-878) straight into the device pair
+    arrays: inflated radii, cell size, labelled broad phase and the element
+    adjacency all in the library (bdem_contact_pairs).  Returns the count."""
+    dev = scene.device
+    if scene.k_element <= 0.0 or dev.n < 2:
+        dev.set_pairs(torch.zeros((0, 2), dtype=torch.int32, device=dev.device))
+        return 0
+    if getattr(dev, "labels", None) is None:
+        label_components(dev.n, scene.bonds, scene)
+    dt2g = scene.dt**2 * float(np.linalg.norm(scene.gravity))
+    return dev.contact_pairs(scene.dt, dt2g, dev.labels)
+
+
 def contact_candidates(scene):
     """Frozen self-contact candidates of one step (solver.py:856-878): broad
     phase on radii inflated by dt|v| + dt^2|g|, restricted to element pairs
-    in different fragments.  Returns an (m,2) int32 CUDA tensor."""
-    dev = scene.device
-    if scene.k_element <= 0.0 or dev.n < 2:
-        return torch.zeros((0, 2), dtype=torch.int32, device=dev.device)
-    travel = scene.dt * torch.linalg.vector_norm(dev.v, dim=1)
-    travel = travel + scene.dt**2 * float(np.linalg.norm(scene.gravity))
-    inflated = dev.radius + travel
-    cell = 2.0 * float(inflated.max()) + 1e-12
-    if getattr(dev, "labels", None) is None:
-        label_components(dev.n, scene.bonds, scene)
-    return _device_broadphase(dev, dev.p, inflated, cell, dev.labels)
+    in different fragments.  Installs them in the scene's device system and
+    returns them as an (m,2) int32 CUDA tensor."""
+    _candidates_into_system(scene)
+    return scene.device.pair_array()
 
 
 # ---------------------------------------------------------------------------
@@ -194,16 +201,27 @@ def update_bond_states(bonds, p, q, youngs, plastic=None, scene=None):
 # ---------------------------------------------------------------------------
 
 def _apply_driver(scene, dev, t):
+    """Driver rows at t + dt (solver.py:898-900, scenes.py:146-176): the few
+    driven rows are formed on the host, copied once and scattered by
+    bdem_rows_copy."""
     drv = scene.driver
     if drv is None:
         return
     if hasattr(drv, "rows") and hasattr(drv, "ids"):
         p, v, q, qd = drv.rows(t)
-        ids = torch.as_tensor(drv.ids, device=dev.device)
-        dev.p[ids] = torch.as_tensor(p, dtype=torch.float64, device=dev.device)
-        dev.v[ids] = torch.as_tensor(v, dtype=torch.float64, device=dev.device)
-        dev.q[ids] = torch.as_tensor(q, dtype=torch.float64, device=dev.device)
-        dev.qdot[ids] = torch.as_tensor(qd, dtype=torch.float64, device=dev.device)
+        m = len(drv.ids)
+        cache = getattr(dev, "_drv_cache", None)
+        if cache is None or cache[0] is not drv:
+            ids = torch.as_tensor(np.asarray(drv.ids, dtype=np.int32)).to(dev.device)
+            host = torch.zeros((m, 14), dtype=torch.float64).pin_memory()
+            cache = dev._drv_cache = (drv, ids, host, torch.zeros((m, 14), dtype=torch.float64,
+                                                                  device=dev.device))
+        _, ids, host, buf = cache
+        torch.cuda.current_stream(dev.device).synchronize()   # host buffer reuse
+        h = host.numpy()
+        h[:, 0:3], h[:, 3:7], h[:, 7:10], h[:, 10:14] = p, q, v, qd
+        buf.copy_(host, non_blocking=True)
+        dev.rows_copy(ids, buf, to_buf=False)
         return
     # arbitrary reference-style callable: run it on a host view of the state
     el = scene.elements
@@ -223,9 +241,7 @@ class PreparedStep:
     minimizer and the epilogue need."""
 
     problem: GPUProblem
-    pairs: object
-    pin: object
-    backup: tuple
+    n_pairs: int
     t_next: float
 
 
@@ -244,21 +260,19 @@ def prepare_step(scene) -> PreparedStep:
     dev.set_physics(scene.gravity, scene.k_contact, scene.k_element, scene.colliders)
     st = dev.stream
 
-    pin = torch.as_tensor(np.nonzero(~dev.free_np)[0], device=dev.device)
-    backup = (dev.p[pin].clone(), dev.q[pin].clone(), dev.v[pin].clone(), dev.qdot[pin].clone())
+    dev.rows_copy(dev.pinned_ids, dev.pin_buf, to_buf=True)     # pinned backup
     t_next = scene.time + scene.dt
     _apply_driver(scene, dev, t_next)
 
     dev.p_cur.copy_(dev.p)
     dev.q_cur.copy_(dev.q)
-    pairs = contact_candidates(scene)
-    dev.set_pairs(pairs)
+    n_pairs = _candidates_into_system(scene)
     dev.reset_errors()
     dev.call("bdem_predict", dev.sysp, dev.p.data_ptr(), dev.q.data_ptr(), dev.v.data_ptr(),
              dev.qdot.data_ptr(), dev.p_prev.data_ptr(), dev.q_prev.data_ptr(), float(scene.dt),
              dev.p_hat.data_ptr(), dev.q_hat.data_ptr(), dev.mp_dt2.data_ptr(),
              dev.mq_dt2.data_ptr(), dev.xp.data_ptr(), dev.xq.data_ptr(), st)
-    return PreparedStep(GPUProblem(dev), pairs, pin, backup, t_next)
+    return PreparedStep(GPUProblem(dev), n_pairs, t_next)
 
 
 def stable_step(scene, cfg: SolverConfig, method: str = "second-order") -> StepReport:
@@ -266,14 +280,12 @@ def stable_step(scene, cfg: SolverConfig, method: str = "second-order") -> StepR
     if method not in MINIMIZERS:
         raise ValueError(f"the GPU path implements {sorted(MINIMIZERS)}, got {method!r}")
     prep = prepare_step(scene)
-    dev, problem, pairs = scene.device, prep.problem, prep.pairs
-    pin, backup, t_next = prep.pin, prep.backup, prep.t_next
+    dev, problem, n_pairs, t_next = scene.device, prep.problem, prep.n_pairs, prep.t_next
     st = dev.stream
     result = MINIMIZERS[method](problem, dev.xp, dev.xq, cfg)
-    n_pairs = int(pairs.shape[0])
 
     if not result.converged:
-        dev.p[pin], dev.q[pin], dev.v[pin], dev.qdot[pin] = backup
+        dev.rows_copy(dev.pinned_ids, dev.pin_buf, to_buf=False)   # restore pinned rows
         energies = {"kinetic": _kinetic(dev)}
         if scene.host_sync:
             dev.download_state(scene)

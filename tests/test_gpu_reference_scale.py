@@ -42,7 +42,7 @@ def test_plate600k_first_two_newton_iterations(cuda_ok):
     dev = scene.device
     assert dev.n == int(g["n"]) and dev.nb == int(g["n_bonds"])
     prep = prepare_step(scene)             # stable_step's prologue (solver.py:894-906)
-    assert prep.pairs.shape[0] == int(g["n_pairs"])
+    assert prep.n_pairs == int(g["n_pairs"])
     rows = g["rows"]
     rows_t = torch.as_tensor(rows).cuda()
     np.testing.assert_array_equal(dev.xp[rows_t].cpu().numpy(), g["p0"])
