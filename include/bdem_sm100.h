@@ -394,6 +394,12 @@ int64_t bdem_pair_adjacency_workspace(int64_t n, int64_t cap);
 int bdem_set_pairs(bdem_system_t *sys, const int32_t *pairs, int64_t m, void *work,
                    void *stream);
 
+/* (sigma, tau) of the m flagged bond positions pos[] into out (m x 2): the
+ * event records (bond, sigma, tau) of update_bond_states (bonds.py:564-570),
+ * pre-update stresses as cached by bdem_bond_update. */
+int bdem_event_records(const bdem_system_t *sys, const int32_t *pos, int64_t m, double *out,
+                       void *stream);
+
 /* Element rows <-> a packed buffer (m x 14 doubles: p, q, v, qdot) for the
  * listed ids: to_buf=1 gathers (pinned-state backup, solver.py:894-896),
  * to_buf=0 scatters (restore, :910-916; driver rows at t + dt, :898-900). */

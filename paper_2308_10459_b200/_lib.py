@@ -97,6 +97,7 @@ SIGNATURES = {
                                   C.POINTER(C.c_int64), _p]),
     "bdem_pair_adjacency_workspace": (_i64, [_i64, _i64]),
     "bdem_set_pairs": (_int, [_p, _p, _i64, _p, _p]),
+    "bdem_event_records": (_int, [_p, _p, _i64, _p, _p]),
     "bdem_rows_copy": (_int, [_p, _i64, _p, _p, _p, _p, _p, _int, _p]),
     "bdem_reset_errors": (_int, [_p, _p]),
     "bdem_components_workspace": (_i64, [_i64]),

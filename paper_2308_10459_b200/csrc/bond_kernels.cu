@@ -401,6 +401,16 @@ __global__ void __launch_bounds__(kThreads) k_bond_update(bdem_system_t S, const
   flags[b] = broke ? 1 : 0;
 }
 
+// (sigma, tau) of the flagged positions, for the ordered event list
+// [(bond, sigma, tau)] of update_bond_states (bonds.py:564-570)
+__global__ void k_event_records(bdem_system_t S, const int32_t *pos, int64_t m, double *out) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int64_t b = pos[k];
+  out[2 * k] = S.bstate[BDEM_BS_SIGMA * S.n_bond + b];
+  out[2 * k + 1] = S.bstate[BDEM_BS_TAU * S.n_bond + b];
+}
+
 }  // namespace bdem
 
 using namespace bdem;
@@ -434,6 +444,14 @@ int bdem_bond_energy(const bdem_system_t *sys, const double *p, const double *q,
                      void *stream) {
   if (!sys || col < 0 || col >= BDEM_SC_COUNT) return BDEM_ERR_ARG;
   k_bond_energy<<<kRedBlocks, kThreads, 0, as_stream(stream)>>>(*sys, p, q, col);
+  return launch_status();
+}
+
+int bdem_event_records(const bdem_system_t *sys, const int32_t *pos, int64_t m, double *out,
+                       void *stream) {
+  if (!sys || m < 0) return BDEM_ERR_ARG;
+  if (m == 0) return BDEM_OK;
+  k_event_records<<<grid_for(m), kThreads, 0, as_stream(stream)>>>(*sys, pos, m, out);
   return launch_status();
 }
 

@@ -150,8 +150,9 @@ def _device_bond_update(dev, youngs, plastic):
         return []
     st = dev.stream
     if getattr(dev, "_flags", None) is None:
-        dev._flags = torch.zeros(dev.npos, dtype=torch.uint8, device=dev.device)
-        dev._ev_idx = torch.zeros(dev.npos, dtype=torch.int32, device=dev.device)
+        dev._flags = torch.empty(dev.npos, dtype=torch.uint8, device=dev.device)
+        dev._ev_idx = torch.empty(dev.npos, dtype=torch.int32, device=dev.device)
+        dev._ev_rec = torch.empty((dev.npos, 2), dtype=torch.float64, device=dev.device)
         dev._sel_work = torch.empty(int(dev.lib.bdem_select_workspace(dev.npos)),
                                     dtype=torch.uint8, device=dev.device)
     pl = None
@@ -169,12 +170,12 @@ def _device_bond_update(dev, youngs, plastic):
     m = int(cnt.value)
     if m == 0:
         return []
-    pos = dev._ev_idx[:m].long()
-    sig = dev.bstate[L.BS["SIGMA"]][pos].cpu().numpy()
-    tau = dev.bstate[L.BS["TAU"]][pos].cpu().numpy()
-    ids = dev.sell.bond_of_pos[pos.cpu().numpy()]
+    dev.call("bdem_event_records", dev.sysp, dev._ev_idx.data_ptr(), m, dev._ev_rec.data_ptr(), st)
+    pos = dev._ev_idx[:m].cpu().numpy()
+    rec = dev._ev_rec[:m].cpu().numpy()
+    ids = dev.sell.bond_of_pos[pos]
     order = np.argsort(ids, kind="stable")       # ascending bond id (bonds.py:564-569)
-    return [(int(ids[k]), float(sig[k]), float(tau[k])) for k in order]
+    return [(int(ids[k]), float(rec[k, 0]), float(rec[k, 1])) for k in order]
 
 
 def update_bond_states(bonds, p, q, youngs, plastic=None, scene=None):
@@ -214,7 +215,7 @@ def _apply_driver(scene, dev, t):
         if cache is None or cache[0] is not drv:
             ids = torch.as_tensor(np.asarray(drv.ids, dtype=np.int32)).to(dev.device)
             host = torch.zeros((m, 14), dtype=torch.float64).pin_memory()
-            cache = dev._drv_cache = (drv, ids, host, torch.zeros((m, 14), dtype=torch.float64,
+            cache = dev._drv_cache = (drv, ids, host, torch.empty((m, 14), dtype=torch.float64,
                                                                   device=dev.device))
         _, ids, host, buf = cache
         torch.cuda.current_stream(dev.device).synchronize()   # host buffer reuse
