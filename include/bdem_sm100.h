@@ -93,11 +93,12 @@ enum {
 };
 
 /* Off-diagonal coupling coefficients of a bond, read by the SpMV: stored
- * AoSoA-32 in sys->scoef -- coefficient k of position pos at
- * scoef[(pos & ~31) * BDEM_CF_COUNT + 32 k + (pos & 31)], so the 14 planes of
- * one 32-position slot are one contiguous 3.5 KB block (a warp's slot reads
- * stay 256-byte coalesced and touch one page) and the positions of
- * consecutive slices are one contiguous range (one bulk copy per SpMV tile). */
+ * AoSoA-32 in sys->scoef -- the 14 coefficients of the 32 positions of a
+ * slot form one contiguous 3.5 KB record at (pos & ~31) * BDEM_CF_COUNT;
+ * inside it coefficient k of lane l = pos & 31 sits at 64 (k >> 1) + 2 l +
+ * (k & 1), i.e. coefficient pairs interleaved per lane: a lane reads its 14
+ * values as 7 aligned 16-byte loads and a warp's load of one pair is a
+ * contiguous 512-byte segment. */
 enum {
   BDEM_CF_N = 0,     /* unit bond direction n [3]                     */
   BDEM_CF_ALPHA = 3, /* clamped stretch block a+ = alpha n n^T + beta I */

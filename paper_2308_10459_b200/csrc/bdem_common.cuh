@@ -11,29 +11,67 @@ constexpr int kRedBlocks = BDEM_RED_BLOCKS;
 constexpr int kClampCounter = 5;  // sys->counter slot: queued indefinite blocks
 constexpr int kThreads = 256;
 
-// index of coefficient k of position pos in sys->scoef (AoSoA-32, see BDEM_CF_*)
+// SpMV coefficient layout in sys->scoef (see BDEM_CF_* in the header): the
+// 14 coefficients of a 32-position block are one contiguous 3.5 KB record;
+// inside it, coefficient k of lane l sits at 64 (k >> 1) + 2 l + (k & 1)
+// (pairs of coefficients interleaved per lane), so a lane reads its 14
+// values as 7 aligned 16-byte loads and a warp's load of one pair is a
+// contiguous 512-byte segment.  BDEM_CF_PAIRED=0 selects the plain
+// plane-per-coefficient record (32 k + l).
+#ifndef BDEM_CF_PAIRED
+#define BDEM_CF_PAIRED 1
+#endif
+// offset of coefficient k from the lane's base cf_idx(pos, 0)
+__host__ __device__ __forceinline__ constexpr int cf_rel(int k) {
+#if BDEM_CF_PAIRED
+  return 64 * (k >> 1) + (k & 1);
+#else
+  return 32 * k;
+#endif
+}
 __host__ __device__ __forceinline__ int64_t cf_idx(int64_t pos, int k) {
-  return (pos & ~int64_t(31)) * BDEM_CF_COUNT + 32 * k + (pos & 31);
+#if BDEM_CF_PAIRED
+  return (pos & ~int64_t(31)) * BDEM_CF_COUNT + 2 * (pos & 31) + cf_rel(k);
+#else
+  return (pos & ~int64_t(31)) * BDEM_CF_COUNT + (pos & 31) + cf_rel(k);
+#endif
 }
 
-// the 14 coupling coefficients of one position (plane stride 32 doubles)
+// the 14 coupling coefficients of one position
 struct Coef {
   double n[3], al, be, C[9];
 };
 template <bool kGlobal>
 __device__ __forceinline__ Coef load_coef(const double *base) {
   Coef c;
+#if BDEM_CF_PAIRED
+  double v[BDEM_CF_COUNT];
+  const double2 *b2 = reinterpret_cast<const double2 *>(base);
 #pragma unroll
-  for (int t = 0; t < 3; ++t) c.n[t] = kGlobal ? __ldg(base + 32 * (BDEM_CF_N + t)) : base[32 * (BDEM_CF_N + t)];
-  c.al = kGlobal ? __ldg(base + 32 * BDEM_CF_ALPHA) : base[32 * BDEM_CF_ALPHA];
-  c.be = kGlobal ? __ldg(base + 32 * BDEM_CF_BETA) : base[32 * BDEM_CF_BETA];
+  for (int j = 0; j < BDEM_CF_COUNT / 2; ++j) {
+    const double2 t = kGlobal ? __ldg(b2 + 32 * j) : b2[32 * j];
+    v[2 * j] = t.x;
+    v[2 * j + 1] = t.y;
+  }
 #pragma unroll
-  for (int t = 0; t < 9; ++t) c.C[t] = kGlobal ? __ldg(base + 32 * (BDEM_CF_C + t)) : base[32 * (BDEM_CF_C + t)];
+  for (int t = 0; t < 3; ++t) c.n[t] = v[BDEM_CF_N + t];
+  c.al = v[BDEM_CF_ALPHA];
+  c.be = v[BDEM_CF_BETA];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) c.C[t] = v[BDEM_CF_C + t];
+#else
+#pragma unroll
+  for (int t = 0; t < 3; ++t) c.n[t] = kGlobal ? __ldg(base + cf_rel(BDEM_CF_N + t)) : base[cf_rel(BDEM_CF_N + t)];
+  c.al = kGlobal ? __ldg(base + cf_rel(BDEM_CF_ALPHA)) : base[cf_rel(BDEM_CF_ALPHA)];
+  c.be = kGlobal ? __ldg(base + cf_rel(BDEM_CF_BETA)) : base[cf_rel(BDEM_CF_BETA)];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) c.C[t] = kGlobal ? __ldg(base + cf_rel(BDEM_CF_C + t)) : base[cf_rel(BDEM_CF_C + t)];
+#endif
   return c;
 }
 __device__ __forceinline__ void store_coef(double *base, const double v[BDEM_CF_COUNT]) {
 #pragma unroll
-  for (int k = 0; k < BDEM_CF_COUNT; ++k) base[32 * k] = v[k];
+  for (int k = 0; k < BDEM_CF_COUNT; ++k) base[cf_rel(k)] = v[k];
 }
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }

@@ -170,9 +170,9 @@ __global__ void __launch_bounds__(BDEM_ASM_THREADS, BDEM_ASM_MINB) k_bond_assemb
     e_s = st.E;
     st_out[BDEM_ST_KC * nb + b] = st.kc;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) cf[32 * (BDEM_CF_N + c)] = st.n[c];
-    cf[32 * BDEM_CF_ALPHA] = alpha;
-    cf[32 * BDEM_CF_BETA] = beta;
+    for (int c = 0; c < 3; ++c) cf[cf_rel(BDEM_CF_N + c)] = st.n[c];
+    cf[cf_rel(BDEM_CF_ALPHA)] = alpha;
+    cf[cf_rel(BDEM_CF_BETA)] = beta;
   }
 
   double S6[21];
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(BDEM_ASM_THREADS, BDEM_ASM_MINB) k_bond_assemb
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) cf[32 * (BDEM_CF_C + 3 * r + c)] = S6[sidx<6>(r, c + 3)];
+    for (int c = 0; c < 3; ++c) cf[cf_rel(BDEM_CF_C + 3 * r + c)] = S6[sidx<6>(r, c + 3)];
   const int pr[6] = {0, 0, 0, 1, 1, 2}, pc[6] = {0, 1, 2, 1, 2, 2};
 #pragma unroll
   for (int t = 0; t < 6; ++t) {

@@ -35,8 +35,8 @@ __device__ __forceinline__ double stage_stretch(const double *st, const double *
                                                 int64_t b, double n[3], double a[6]) {
   const double *cb = cf + cf_idx(b, 0);
 #pragma unroll
-  for (int c = 0; c < 3; ++c) n[c] = cb[32 * (BDEM_CF_N + c)];
-  const double al = cb[32 * BDEM_CF_ALPHA], be = cb[32 * BDEM_CF_BETA];
+  for (int c = 0; c < 3; ++c) n[c] = cb[cf_rel(BDEM_CF_N + c)];
+  const double al = cb[cf_rel(BDEM_CF_ALPHA)], be = cb[cf_rel(BDEM_CF_BETA)];
   const int pr[6] = {0, 0, 0, 1, 1, 2}, pc[6] = {0, 1, 2, 1, 2, 2};
 #pragma unroll
   for (int t = 0; t < 6; ++t) a[t] = al * (n[pr[t]] * n[pc[t]]) + (pr[t] == pc[t] ? be : 0.0);

@@ -265,9 +265,18 @@ __device__ __forceinline__ void slot_apply(const bdem_system_t &S, const double 
     double xo[3], n[3];
 #pragma unroll
     for (int t = 0; t < 3; ++t) xo[t] = __ldg(x + t * S.vstride + r.o);
+#if BDEM_CF_PAIRED
+    // n0 n1 | n2 alpha | beta (C0): three 16-byte loads
+    const double2 *b2 = reinterpret_cast<const double2 *>(base);
+    const double2 c01 = __ldg(b2), c23 = __ldg(b2 + 32), c45 = __ldg(b2 + 64);
+    n[0] = c01.x; n[1] = c01.y; n[2] = c23.x;
+    const double al = c23.y, be = c45.x;
+    static_assert(BDEM_CF_N == 0 && BDEM_CF_ALPHA == 3 && BDEM_CF_BETA == 4, "pair layout");
+#else
 #pragma unroll
-    for (int t = 0; t < 3; ++t) n[t] = __ldg(base + 32 * (BDEM_CF_N + t));
-    const double al = __ldg(base + 32 * BDEM_CF_ALPHA), be = __ldg(base + 32 * BDEM_CF_BETA);
+    for (int t = 0; t < 3; ++t) n[t] = __ldg(base + cf_rel(BDEM_CF_N + t));
+    const double al = __ldg(base + cf_rel(BDEM_CF_ALPHA)), be = __ldg(base + cf_rel(BDEM_CF_BETA));
+#endif
     const double nx = al * ((n[0] * xo[0] + n[1] * xo[1]) + n[2] * xo[2]);
 #pragma unroll
     for (int c = 0; c < 3; ++c) acc[c] -= nx * n[c] + be * xo[c];

@@ -607,8 +607,10 @@ class DeviceSystem:
     def coef_planes(self) -> torch.Tensor:
         """The AoSoA-32 SpMV coefficients as (BDEM_CF_COUNT, n_pos) planes."""
         npos32 = self.scoef.numel() // L.CF["COUNT"]
-        v = self.scoef.view(npos32 // 32, L.CF["COUNT"], 32).permute(1, 0, 2)
-        return v.reshape(L.CF["COUNT"], npos32)[:, :self.npos]
+        k = L.CF["COUNT"]
+        # record per 32 positions: coefficient pair j, lane l, member m at 64 j + 2 l + m
+        v = self.scoef.view(npos32 // 32, k // 2, 32, 2).permute(1, 3, 0, 2)
+        return v.reshape(k, npos32)[:, :self.npos]
 
     def friction(self, mu_s: float, mu_r: float, dt: float) -> int:
         """apply_friction (contact.py:303-350) on the device state in place;
