@@ -370,6 +370,10 @@ __global__ void k_predict(bdem_system_t S, const double *p, const double *q, con
     for (int c = 0; c < 3; ++c) p0[3 * e + c] = pe[c] + dt * ve[c];
 #pragma unroll
     for (int c = 0; c < 4; ++c) st[c] = dt * we[c];
+#ifdef BDEM_MUTATE_RETRACT  // mutation check of the parity tests only (never shipped)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) st[c] *= 1.0 + BDEM_MUTATE_RETRACT;
+#endif
     retract_normalize(qe, st, out);  // geodesic then quat_normalize(q0)
   } else {
 #pragma unroll

@@ -295,7 +295,7 @@ def _run_traj(name, spec, steps, eps, driver=None, schedule=None, max_iter=300):
     sc = ref_scene(spec, driver=driver)
     cfg = rsv.SolverConfig(epsilon=eps, max_iterations=max_iter)
     rec = {k: [] for k in ("p", "q", "v", "qdot", "newton", "pcg", "committed", "reason",
-                           "pairs", "gnorm")}
+                           "pairs", "gnorm", "rec0_f", "rec0_gnorm")}
     events = []
     out = pack("init_el_", spec.elements, ELEM_FIELDS)
     out.update(pack("init_b_", spec.bonds, BOND_FIELDS))
@@ -313,6 +313,10 @@ def _run_traj(name, spec, steps, eps, driver=None, schedule=None, max_iter=300):
         rec["reason"].append(rep.solve.reason)
         rec["pairs"].append(rep.contact_pairs)
         rec["gnorm"].append(rep.solve.grad_norm)
+        # the first Newton record is evaluated at the predictor (p0, q0):
+        # it makes the predictor's retraction observable
+        rec["rec0_f"].append(rep.solve.records[0].f)
+        rec["rec0_gnorm"].append(rep.solve.records[0].grad_norm)
         events += [(s, b, sg, tu) for (b, sg, tu) in rep.broken]
     out.update({k: np.array(v) for k, v in rec.items()})
     out["events"] = np.array(events, dtype=float).reshape(-1, 4)
