@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define BDEM_ABI_VERSION 5
+#define BDEM_ABI_VERSION 6
 
 enum {
   BDEM_OK = 0,
@@ -81,15 +81,39 @@ enum {
   BDEM_BS_COUNT = 5
 };
 
-/* per-bond staging written by bdem_bond_assemble (each n_bond doubles) */
+/* per-bond staging written by bdem_bond_assemble (each n_bond doubles): the
+ * j-role pieces the element pass gathers for the bond's j end, and the
+ * clamped (i,i) rotation quadrant of the positions whose row could not fold
+ * it into its i-role partial sum (see BDEM_IP_* / ikpre) */
 enum {
-  BDEM_ST_E = 0,     /* bond energy                                   */
-  BDEM_ST_KC = 1,    /* k c: dE/dp_j = kc n, dE/dp_i = -kc n          */
-  BDEM_ST_GQI = 2,   /* d E / d q_i [4]                               */
-  BDEM_ST_GQJ = 6,   /* d E / d q_j [4]                               */
-  BDEM_ST_A = 10,    /* clamped (i,i) rotation quadrant (sym 6)        */
-  BDEM_ST_D = 16,    /* clamped (j,j) rotation quadrant (sym 6)        */
-  BDEM_ST_COUNT = 22
+  BDEM_ST_KC = 0,    /* k c: dE/dp_j = kc n, dE/dp_i = -kc n          */
+  BDEM_ST_GQJ = 1,   /* d E / d q_j [4]                               */
+  BDEM_ST_D = 5,     /* clamped (j,j) rotation quadrant (sym 6)        */
+  BDEM_ST_A = 11,    /* clamped (i,i) rotation quadrant (sym 6), only
+                        for slots >= ikpre[row] of its row            */
+  BDEM_ST_COUNT = 17
+};
+
+/* i-role partial sums of one SELL row, written by bdem_bond_assemble (each
+ * plane n_rows = 32 * n_slices doubles, indexed by row): the row thread of
+ * the bond pass walks its i-role slots in ascending bond id and adds each
+ * bond's pieces in np.add.at order (integrator.py:100-103); the element pass
+ * continues these sums with the j-role pieces.  The rotation quadrant of a
+ * slot is folded into BDEM_IP_R only while every earlier slot of the row had
+ * a PSD-certified block: ikpre[row] is the first slot whose (possibly
+ * eigen-clamped) quadrant is staged in BDEM_ST_A instead (-1: none). */
+enum {
+  BDEM_IP_GP = 0,    /* sum of -kc n (position gradient) [3]          */
+  BDEM_IP_GQ = 3,    /* sum of dE/dq_i [4]                            */
+  BDEM_IP_P = 7,     /* sum of clamped stretch blocks a+ (sym 6)      */
+  BDEM_IP_R = 13,    /* sum of (i,i) rotation quadrants (sym 6)       */
+  BDEM_IP_E = 19,    /* sum of bond energies                          */
+  BDEM_IP_COUNT = 20
+};
+
+/* sys->asm_flags */
+enum {
+  BDEM_ASM_STAGE_ALL_A = 1 /* stage every (i,i) quadrant (ikpre = 0): tests */
 };
 
 /* Off-diagonal coupling coefficients of a bond, read by the SpMV: stored
@@ -212,11 +236,13 @@ typedef struct {
   int32_t *err;                  /* BDEM_ERRSLOT_COUNT                 */
   unsigned int *counter;         /* last-block counters (zeroed)       */
   int32_t *clamp_list;           /* (n_bond) queue of indefinite rotation blocks */
+  double *ipart;                 /* BDEM_IP_COUNT planes x n_rows: i-role partial sums */
+  int32_t *ikpre;                /* (n_rows) first slot with a staged (i,i) quadrant, -1 */
   /* physics */
   double gravity[3];
   double k_contact, k_element;
   int32_t n_colliders;
-  int32_t pad_;
+  int32_t asm_flags;             /* BDEM_ASM_* */
   bdem_collider_t colliders[BDEM_MAX_COLLIDERS];
 } bdem_system_t;
 
@@ -238,8 +264,10 @@ int bdem_bond_eval_ambient(const bdem_system_t *sys, const double *p, const doub
                            double *gpj, double *gqi, double *gqj, double *hpp, double *hqq,
                            int want_hess, void *stream);
 
-/* Fused production bond kernel at (p, q): energy, gradient contributions and
- * the SPD-clamped reduced Hessian blocks, written to sys->stage.
+/* Fused production bond pass at (p, q): energy, gradient contributions and
+ * the SPD-clamped reduced Hessian blocks.  One thread per SELL row walks the
+ * row's i-role bonds: coupling coefficients to sys->scoef, the j-role pieces
+ * to sys->stage, the i-role pieces summed in order into sys->ipart.
  * Replaces energy_terms(want_hess=True) + spd_project of the position and the
  * G_l-reduced rotation blocks inside build_clamped_pieces (solver.py:141-162). */
 int bdem_bond_assemble(const bdem_system_t *sys, const double *p, const double *q,

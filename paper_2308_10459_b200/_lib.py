@@ -20,7 +20,9 @@ ERRSLOT_COUNT = 8
 BG = dict(L0=0, D0=1, FRAME=4, KN=13, KT=14, KDIAG=15, RADIUS=18, SECTION=19, SECOND=20,
           POLAR=21, TENSILE=22, SHEAR=23, COUNT=24)
 BS = dict(SCALE=0, DAMAGE=1, PLASTIC=2, SIGMA=3, TAU=4, COUNT=5)
-ST = dict(E=0, KC=1, GQI=2, GQJ=6, A=10, D=16, COUNT=22)
+ST = dict(KC=0, GQJ=1, D=5, A=11, COUNT=17)
+IP = dict(GP=0, GQ=3, P=7, R=13, E=19, COUNT=20)
+ASM_STAGE_ALL_A = 1
 CF = dict(N=0, ALPHA=3, BETA=4, C=5, COUNT=14)
 PS = dict(E=0, GI=1, A=4, COUNT=10)
 SC = dict(F=0, GNORM2=1, CNORM2=2, MAXDEV=3, SLOPE=4, FT=5, NSING=6, EBOND=7, ECOL=8, EGRAV=9,
@@ -28,7 +30,7 @@ SC = dict(F=0, GNORM2=1, CNORM2=2, MAXDEV=3, SLOPE=4, FT=5, NSING=6, EBOND=7, EC
 PCG = dict(RZ=0, PAP=1, ALPHA=2, BETA=3, RR=4, BNORM=5, REL=6, TOL=7, BOOST=8, APNORM2=9,
            PNORM2=10, K=11, MAXIT=12, STATE=13, ROTZERO=14, COUNT=16)
 PCG_RUNNING, PCG_CONVERGED, PCG_BREAKDOWN, PCG_MAXIT = 0, 1, 2, 3
-ABI_VERSION = 5
+ABI_VERSION = 6
 RED_BLOCKS = 1184
 MAX_COLLIDERS = 8
 N_COUNTERS = 16
@@ -53,8 +55,9 @@ class System(C.Structure):
         ("pair_i", _p), ("pair_j", _p), ("pi_ptr", _p), ("pj_ptr", _p), ("pj_idx", _p),
         ("stage", _p), ("scoef", _p), ("pstage", _p), ("diag", _p), ("minv", _p), ("red", _p),
         ("scalars", _p), ("pcg", _p), ("err", _p), ("counter", _p), ("clamp_list", _p),
+        ("ipart", _p), ("ikpre", _p),
         ("gravity", C.c_double * 3), ("k_contact", C.c_double), ("k_element", C.c_double),
-        ("n_colliders", C.c_int32), ("pad_", C.c_int32),
+        ("n_colliders", C.c_int32), ("asm_flags", C.c_int32),
         ("colliders", Collider * MAX_COLLIDERS),
     ]
 

@@ -123,101 +123,217 @@ __global__ void __launch_bounds__(128) k_bond_ambient(bdem_system_t S, const dou
 }
 
 // ---------------------------------------------------------------------------
-// fused production kernel: energy, gradient contributions and the clamped
+// fused production bond pass: energy, gradient contributions and the clamped
 // reduced blocks (energy_terms + build_clamped_pieces, solver.py:141-162)
 // ---------------------------------------------------------------------------
-// 64-thread CTAs, 8 per SM (128 registers): 1.7% faster than 128 x 4 (finer
-// CTA granularity at the same 16 warps per SM); 96 x 5 and 256 x 2 slower
+// One thread per SELL row: it walks the row's i-role slots (the bonds with
+// i == e in ascending id; lane = row & 31, so slot k of a warp's 32 rows is
+// one contiguous 256-byte segment per plane) and
+//   * writes the bond's SpMV coupling coefficients (scoef) and the pieces the
+//     element pass gathers for the j end (stage: kc, dE/dq_j, (j,j) quadrant);
+//   * adds the i-end pieces (-kc n, dE/dq_i, a+, (i,i) quadrant, energy) to
+//     the row's partial sums in exactly the order the element pass used to
+//     (np.add.at, integrator.py:100-103), so the gathered gradient and
+//     diagonal blocks are unchanged bit for bit while the i-role pieces
+//     never travel through HBM.  The partial sums live in shared memory
+//     (one column per thread) so they do not compete with the bond
+//     arithmetic for registers.
+// A rotation block that fails the register PSD certificate is queued for
+// the eigen-clamp pass (k_bond_clamp), which rewrites it after this kernel;
+// from that slot on the row stages its (i,i) quadrants (ikpre) and the
+// element pass continues the sum from there.
+// 64-thread CTAs, 6 per SM (168 registers, 52 B of spills; at 8 per SM the
+// 128-register cap spilled ~320 B per bond through L1, 441 vs 461 us on the
+// plate, scratch/r02/ab_rows.sh).
 #ifndef BDEM_ASM_MINB
-#define BDEM_ASM_MINB 8
+#define BDEM_ASM_MINB 6
+#endif
+#ifndef BDEM_ROWS_HOIST
+#define BDEM_ROWS_HOIST 0
+#endif
+#ifndef BDEM_ROWS_SMEM
+#define BDEM_ROWS_SMEM 1
+#endif
+#if BDEM_ROWS_SMEM
+#define ACC_T volatile double
+#else
+#define ACC_T double
+#endif
+#ifndef BDEM_ROWS_PREFETCH
+#define BDEM_ROWS_PREFETCH 0
 #endif
 #ifndef BDEM_ASM_THREADS
 #define BDEM_ASM_THREADS 64
 #endif
-__global__ void __launch_bounds__(BDEM_ASM_THREADS, BDEM_ASM_MINB) k_bond_assemble(bdem_system_t S, const double *p,
+// row partial sums in shared memory: acc[first + c][t] += v[c] for c < N,
+// all loads issued before the adds and all stores after them (volatile
+// accesses keep program order, so an interleaved load/add/store sequence
+// would serialise on the shared-memory latency)
+template <int N>
+__device__ __forceinline__ void acc_add(ACC_T (*acc)[BDEM_ASM_THREADS], int first, int t,
+                                        const double v[N]) {
+  double cur[N];
+#pragma unroll
+  for (int c = 0; c < N; ++c) cur[c] = acc[first + c][t];
+#pragma unroll
+  for (int c = 0; c < N; ++c) cur[c] += v[c];
+#pragma unroll
+  for (int c = 0; c < N; ++c) acc[first + c][t] = cur[c];
+}
+
+__global__ void __launch_bounds__(BDEM_ASM_THREADS, BDEM_ASM_MINB) k_bond_rows(bdem_system_t S, const double *p,
                                                        const double *q) {
-  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  __shared__ double acc_sh[BDEM_IP_COUNT][BDEM_ASM_THREADS];
+  // volatile: every partial-sum update is a shared-memory read-modify-write
+  // (the compiler would otherwise keep the 20 sums in registers and spill)
+#if BDEM_ROWS_SMEM
+  volatile double(*acc)[BDEM_ASM_THREADS] = acc_sh;
+#else
+  double(*acc)[BDEM_ASM_THREADS] = acc_sh;
+#endif
+  const int t = threadIdx.x;
+  const int64_t nrow = ((S.n_elem + 31) >> 5) << 5;
+  const int64_t row = blockIdx.x * (int64_t)BDEM_ASM_THREADS + t;
+  if (row >= nrow) return;
+#pragma unroll
+  for (int k = 0; k < BDEM_IP_COUNT; ++k) acc[k][t] = 0.0;
+  const int sl = (int)(row >> 5), lane = (int)(row & 31);
+  const int e = S.row_elem[row];
   const int64_t nb = S.n_bond;
-  if (b >= nb) return;
   double *st_out = S.stage;
-  if (S.status[b] == 2) {  // broken or padding: no energy, no coupling
-#pragma unroll
-    for (int k = 0; k < BDEM_ST_COUNT; ++k) st_out[k * nb + b] = 0.0;
-    const double zero[BDEM_CF_COUNT] = {};
-    store_coef(S.scoef + cf_idx(b, 0), zero);
-    return;
-  }
-  // Outputs are stored as soon as each piece is final so the stretch state
-  // is dead before the rotation block is formed (register pressure).
-  const int bi = S.bond_i[b], bj = S.bond_j[b];
   const double *g = S.geom;
-  const double scale = S.bstate[BDEM_BS_SCALE * nb + b];
-  double *cf = S.scoef + cf_idx(b, 0);
-  double pi[3], pj[3], qi[4], qj[4];
-  load_pq(p, q, bi, pi, qi);
-  load_pq(p, q, bj, pj, qj);
-
-  // stretch: energy, gradient (kc n) and the closed-form clamp of
-  // [[a,-a],[-a,a]]: a+ = k (nn + max(c/l,0) (I - nn)) = alpha nn + beta I
-  double e_s;
-  {
-    const double ks = scale * g[BDEM_BG_KN * nb + b];
-    const Stretch st = stretch_eval(pi, pj, g[BDEM_BG_L0 * nb + b], ks);
-    if (st.degenerate) flag_error(S.err, BDEM_ERR_DEGENERATE_BOND, b);
-    const double f = st.c_over_l > 0.0 ? st.c_over_l : 0.0;
-    const double beta = ks * f;
-    const double alpha = ks - beta;
-    e_s = st.E;
-    st_out[BDEM_ST_KC * nb + b] = st.kc;
+  int kpre = (S.asm_flags & BDEM_ASM_STAGE_ALL_A) ? 0 : -1;
+  const int64_t b_end = S.slice_base[sl + 1];
+#if BDEM_ROWS_HOIST
+  double pi[3] = {0.0, 0.0, 0.0}, qi[4] = {0.0, 0.0, 0.0, 1.0};
+  if (e >= 0) load_pq(p, q, e, pi, qi);
+#endif
+  int k = 0;
+  const int64_t b_beg = S.slice_base[sl] + lane;
+#if BDEM_ROWS_PREFETCH
+  // software pipeline on the slot's status and j index: the next slot's
+  // (dependent-gather-feeding) index is in flight while this bond computes
+  int8_t stat_n = b_beg < b_end ? S.status[b_beg] : (int8_t)2;
+  int bj_n = b_beg < b_end ? S.bond_j[b_beg] : 0;
+#endif
+#pragma unroll 1
+  for (int64_t b = b_beg; b < b_end; b += 32, ++k) {
+    double *cf = S.scoef + cf_idx(b, 0);
+#if BDEM_ROWS_PREFETCH
+    const int8_t stat = stat_n;
+    const int bj = bj_n;
+    if (b + 32 < b_end) {
+      stat_n = S.status[b + 32];
+      bj_n = S.bond_j[b + 32];
+    }
+#else
+    const int8_t stat = S.status[b];
+#endif
+    if (stat == 2) {  // broken or padding: no energy, no coupling
 #pragma unroll
-    for (int c = 0; c < 3; ++c) cf[cf_rel(BDEM_CF_N + c)] = st.n[c];
-    cf[cf_rel(BDEM_CF_ALPHA)] = alpha;
-    cf[cf_rel(BDEM_CF_BETA)] = beta;
-  }
+      for (int c = 0; c < BDEM_ST_COUNT; ++c) st_out[c * nb + b] = 0.0;
+      const double zero[BDEM_CF_COUNT] = {};
+      store_coef(cf, zero);
+      continue;
+    }
+    // pieces are stored (and summed) as soon as they are final so the
+    // stretch state is dead before the rotation block is formed
+#if !BDEM_ROWS_PREFETCH
+    const int bj = S.bond_j[b];
+#endif
+    const double scale = S.bstate[BDEM_BS_SCALE * nb + b];
+    double pj[3], qj[4];
+#if !BDEM_ROWS_HOIST
+    double pi[3], qi[4];
+    load_pq(p, q, e, pi, qi);
+#endif
+    load_pq(p, q, bj, pj, qj);
 
-  double S6[21];
-  {
-    double d0[3], F[3][3], kds[3];
+    // stretch: energy, gradient (kc n) and the closed-form clamp of
+    // [[a,-a],[-a,a]]: a+ = k (nn + max(c/l,0) (I - nn)) = alpha nn + beta I
+    double e_s;
+    {
+      const double ks = scale * g[BDEM_BG_KN * nb + b];
+      const Stretch st = stretch_eval(pi, pj, g[BDEM_BG_L0 * nb + b], ks);
+      if (st.degenerate) flag_error(S.err, BDEM_ERR_DEGENERATE_BOND, b);
+      const double f = st.c_over_l > 0.0 ? st.c_over_l : 0.0;
+      const double beta = ks * f;
+      const double alpha = ks - beta;
+      e_s = st.E;
+      st_out[BDEM_ST_KC * nb + b] = st.kc;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) cf[cf_rel(BDEM_CF_N + c)] = st.n[c];
+      cf[cf_rel(BDEM_CF_ALPHA)] = alpha;
+      cf[cf_rel(BDEM_CF_BETA)] = beta;
+      double apos[6], gpc[3];
+      stretch_apos(alpha, beta, st.n, apos);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) gpc[c] = acc[BDEM_IP_GP + c][t];
+      // same expression as the element pass's j-role sum (same contraction)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) gpc[c] += -(st.kc * st.n[c]);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[BDEM_IP_GP + c][t] = gpc[c];
+      acc_add<6>(acc, BDEM_IP_P, t, apos);
+    }
+
+    double S6[21];
+    {
+      double d0[3], F[3][3], kds[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) F[r][c] = g[(BDEM_BG_FRAME + 3 * r + c) * nb + b];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) kds[c] = scale * g[(BDEM_BG_KDIAG + c) * nb + b];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) d0[c] = g[(BDEM_BG_D0 + c) * nb + b];
+      const Shear sh = shear_eval(qi, qj, d0, scale * g[BDEM_BG_KT * nb + b]);
+      if (sh.antipodal) flag_error(S.err, BDEM_ERR_ANTIPODAL, b);
+      const RotGrad ro = rot_grad(qi, qj, F, kds);
+      double eg[5];
+      eg[0] = (e_s + sh.E) + ro.E_b;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        eg[1 + c] = sh.g[c] + ro.gbi[c];
+        st_out[(BDEM_ST_GQJ + c) * nb + b] = sh.g[c] + ro.gbj[c];
+      }
+      acc_add<1>(acc, BDEM_IP_E, t, eg);
+      acc_add<4>(acc, BDEM_IP_GQ, t, eg + 1);
+      rot_block(qi, qj, d0, F, kds, sh, ro.rs, ro.rv, ro.w, S6);
+    }
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) F[r][c] = g[(BDEM_BG_FRAME + 3 * r + c) * nb + b];
+      for (int c = 0; c < 3; ++c) cf[cf_rel(BDEM_CF_C + 3 * r + c)] = S6[sidx<6>(r, c + 3)];
+    const int pr[6] = {0, 0, 0, 1, 1, 2}, pc[6] = {0, 1, 2, 1, 2, 2};
 #pragma unroll
-    for (int c = 0; c < 3; ++c) kds[c] = scale * g[(BDEM_BG_KDIAG + c) * nb + b];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) d0[c] = g[(BDEM_BG_D0 + c) * nb + b];
-    const Shear sh = shear_eval(qi, qj, d0, scale * g[BDEM_BG_KT * nb + b]);
-    if (sh.antipodal) flag_error(S.err, BDEM_ERR_ANTIPODAL, b);
-    const RotGrad ro = rot_grad(qi, qj, F, kds);
-    st_out[BDEM_ST_E * nb + b] = (e_s + sh.E) + ro.E_b;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      st_out[(BDEM_ST_GQI + c) * nb + b] = sh.g[c] + ro.gbi[c];
-      st_out[(BDEM_ST_GQJ + c) * nb + b] = sh.g[c] + ro.gbj[c];
-    }
-    rot_block(qi, qj, d0, F, kds, sh, ro.rs, ro.rv, ro.w, S6);
-  }
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) cf[cf_rel(BDEM_CF_C + 3 * r + c)] = S6[sidx<6>(r, c + 3)];
-  const int pr[6] = {0, 0, 0, 1, 1, 2}, pc[6] = {0, 1, 2, 1, 2, 2};
-#pragma unroll
-  for (int t = 0; t < 6; ++t) {
-    st_out[(BDEM_ST_A + t) * nb + b] = S6[sidx<6>(pr[t], pc[t])];
-    st_out[(BDEM_ST_D + t) * nb + b] = S6[sidx<6>(pr[t] + 3, pc[t] + 3)];
-  }
+    for (int u = 0; u < 6; ++u) st_out[(BDEM_ST_D + u) * nb + b] = S6[sidx<6>(pr[u] + 3, pc[u] + 3)];
 
-  // PSD blocks (all of them at identity orientations) are final as staged;
-  // indefinite ones are queued for the register-resident eigen-clamp pass
-  // (k_bond_clamp), which overwrites the staged block
-  double mx = 0.0;
+    // PSD blocks (all of them at identity orientations) are final; an
+    // indefinite one is queued for the register-resident eigen-clamp pass
+    // (k_bond_clamp), which overwrites its staged quadrants and coefficients
+    double mx = 0.0;
 #pragma unroll
-  for (int t = 0; t < 21; ++t) mx = fmax(mx, fabs(S6[t]));
-  if (mx != 0.0 && !psd6_regs(S6, 4e-14 * mx)) {
-    const unsigned int slot = atomicAdd(S.counter + kClampCounter, 1u);
-    S.clamp_list[slot] = (int32_t)b;
+    for (int u = 0; u < 21; ++u) mx = fmax(mx, fabs(S6[u]));
+    if (mx != 0.0 && !psd6_regs(S6, 4e-14 * mx)) {
+      const unsigned int slot = atomicAdd(S.counter + kClampCounter, 1u);
+      S.clamp_list[slot] = (int32_t)b;
+      if (kpre < 0) kpre = k;
+    }
+    if (kpre < 0) {
+      double a6[6];
+#pragma unroll
+      for (int u = 0; u < 6; ++u) a6[u] = S6[sidx<6>(pr[u], pc[u])];
+      acc_add<6>(acc, BDEM_IP_R, t, a6);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 6; ++u) st_out[(BDEM_ST_A + u) * nb + b] = S6[sidx<6>(pr[u], pc[u])];
+    }
   }
+#pragma unroll
+  for (int c = 0; c < BDEM_IP_COUNT; ++c) S.ipart[c * nrow + row] = acc[c][t];
+  S.ikpre[row] = kpre;
 }
 
 // ---------------------------------------------------------------------------
@@ -434,7 +550,9 @@ int bdem_bond_assemble(const bdem_system_t *sys, const double *p, const double *
   if (sys->n_bond == 0) return BDEM_OK;
   cudaStream_t st = as_stream(stream);
   cudaMemsetAsync(sys->counter + kClampCounter, 0, sizeof(unsigned int), st);
-  k_bond_assemble<<<grid_for(sys->n_bond, BDEM_ASM_THREADS), BDEM_ASM_THREADS, 0, st>>>(*sys, p, q);
+  const int64_t nrow = ((sys->n_elem + 31) >> 5) << 5;
+  if (nrow > (int64_t)grid_for(nrow, BDEM_ASM_THREADS) * BDEM_ASM_THREADS) return BDEM_ERR_ARG;
+  k_bond_rows<<<grid_for(nrow, BDEM_ASM_THREADS), BDEM_ASM_THREADS, 0, st>>>(*sys, p, q);
   // the clamp pass reads the queue length on the device; idle threads exit
   k_bond_clamp<<<kRedBlocks * (128 / BDEM_CLAMP_THREADS), BDEM_CLAMP_THREADS, 0, st>>>(*sys);
   return launch_status(2);

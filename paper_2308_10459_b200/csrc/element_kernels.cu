@@ -36,21 +36,22 @@ __device__ __forceinline__ double stage_stretch(const double *st, const double *
   const double *cb = cf + cf_idx(b, 0);
 #pragma unroll
   for (int c = 0; c < 3; ++c) n[c] = cb[cf_rel(BDEM_CF_N + c)];
-  const double al = cb[cf_rel(BDEM_CF_ALPHA)], be = cb[cf_rel(BDEM_CF_BETA)];
-  const int pr[6] = {0, 0, 0, 1, 1, 2}, pc[6] = {0, 1, 2, 1, 2, 2};
-#pragma unroll
-  for (int t = 0; t < 6; ++t) a[t] = al * (n[pr[t]] * n[pc[t]]) + (pr[t] == pc[t] ? be : 0.0);
+  stretch_apos(cb[cf_rel(BDEM_CF_ALPHA)], cb[cf_rel(BDEM_CF_BETA)], n, a);
   return st[BDEM_ST_KC * nb + b];
 }
 
 // ---------------------------------------------------------------------------
 // element assembly
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads, 2) k_element_assemble(bdem_system_t S, const double *p,
+#ifndef BDEM_ELEM_MINB
+#define BDEM_ELEM_MINB 2
+#endif
+__global__ void __launch_bounds__(kThreads, BDEM_ELEM_MINB) k_element_assemble(bdem_system_t S, const double *p,
                                                                const double *q, double *z) {
   __shared__ double sh[kThreads / 32];
   double acc_f = 0.0, acc_g2 = 0.0, acc_c2 = 0.0, acc_dev = 0.0, acc_sing = 0.0;
   const int64_t nb = S.n_bond, pc = S.pair_cap;
+  const int64_t nrow = ((S.n_elem + 31) >> 5) << 5;
   const double *st = S.stage;
   bool any_col_hess = false;
   for (int i = 0; i < S.n_colliders; ++i) any_col_hess |= S.colliders[i].kind != BDEM_COLLIDER_HALFSPACE;
@@ -66,21 +67,28 @@ __global__ void __launch_bounds__(kThreads, 2) k_element_assemble(bdem_system_t 
     double P[6] = {0, 0, 0, 0, 0, 0}, R[6] = {0, 0, 0, 0, 0, 0};
     double ebond = 0.0;
     const int sl = (int)(row >> 5), lane = (int)(row & 31);
-    // bonds with i == e: this element's SELL row (padding stages zeros)
-#pragma unroll 2
-    for (int64_t b = S.slice_base[sl] + lane; b < S.slice_base[sl + 1]; b += 32) {
-      double n[3], apos[6];
-      const double kc = stage_stretch(st, S.scoef, nb, b, n, apos);
+    // bonds with i == e: their pieces were summed in order by the bond pass
+    // (ipart); slots from ikpre on staged their (i,i) rotation quadrant
+    if (nb > 0) {
+      const double *ip = S.ipart;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) gp[c] += -(kc * n[c]);
+      for (int c = 0; c < 3; ++c) gp[c] = ip[(BDEM_IP_GP + c) * nrow + row];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) gq[c] += st[(BDEM_ST_GQI + c) * nb + b];
+      for (int c = 0; c < 4; ++c) gq[c] = ip[(BDEM_IP_GQ + c) * nrow + row];
 #pragma unroll
       for (int t = 0; t < 6; ++t) {
-        P[t] += apos[t];
-        R[t] += st[(BDEM_ST_A + t) * nb + b];
+        P[t] = ip[(BDEM_IP_P + t) * nrow + row];
+        R[t] = ip[(BDEM_IP_R + t) * nrow + row];
       }
-      ebond += st[BDEM_ST_E * nb + b];
+      ebond = ip[BDEM_IP_E * nrow + row];
+      const int kpre = S.ikpre[row];
+      if (kpre >= 0) {
+        for (int64_t b = S.slice_base[sl] + lane + 32 * (int64_t)kpre; b < S.slice_base[sl + 1];
+             b += 32) {
+#pragma unroll
+          for (int t = 0; t < 6; ++t) R[t] += st[(BDEM_ST_A + t) * nb + b];
+        }
+      }
     }
     // bonds with j == e (ascending bond id)
 #pragma unroll 2

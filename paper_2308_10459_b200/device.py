@@ -221,6 +221,10 @@ class DeviceSystem:
         self.err = torch.zeros(L.ERRSLOT_COUNT, dtype=I32, device=dev)
         self.counter = torch.zeros(L.N_COUNTERS, dtype=torch.int32, device=dev)
         self.clamp_list = torch.zeros(npos, dtype=I32, device=dev)
+        # i-role partial sums of the bond pass, one column per SELL row
+        nrow = int(sell.row_elem.shape[0])
+        self.ipart = torch.zeros((L.IP["COUNT"], nrow), dtype=F64, device=dev)
+        self.ikpre = torch.zeros(nrow, dtype=I32, device=dev)
         # host staging for scalar read-backs
         self.h_scalars = torch.zeros(L.SC["COUNT"], dtype=F64).pin_memory()
         self.h_pcg = torch.zeros(L.PCG["COUNT"], dtype=F64).pin_memory()
@@ -261,6 +265,7 @@ class DeviceSystem:
         s.red, s.scalars, s.pcg = _ptr(self.red), _ptr(self.scalars), _ptr(self.pcg_state)
         s.err, s.counter = _ptr(self.err), _ptr(self.counter)
         s.clamp_list = _ptr(self.clamp_list)
+        s.ipart, s.ikpre = _ptr(self.ipart), _ptr(self.ikpre)
         self.sysp = C.pointer(s)
         # contact pairs (capacity grows on demand)
         self.n_pair = 0

@@ -2,7 +2,7 @@
 predictor state: CUDA events over repeated launches, plus a perturbed-q state
 (every rotation block through the eigen-clamp)."""
 import json, os, sys
-sys.path.insert(0, os.getcwd())
+sys.path.insert(0, os.getcwd())  # the tree under test (cwd)
 import torch
 from paper_2308_10459_b200 import configs
 from paper_2308_10459_b200.scene import Scene

@@ -173,7 +173,21 @@ def test_assembly_vs_golden(cuda_ok, tag):
     from paper_2308_10459_b200 import _lib as L
     d = load("newton_pieces.npz")
     dev, prob = _gpu_problem(d, tag)
+    # production path: i-role pieces summed by the bond pass's row threads
+    f0, g0, _, _ = prob.assemble(dev.xp, dev.xq)
+    kpre = dev.ikpre[:dev.n].clone()
+    ref = [t.clone() for t in (dev.z, dev.diag, dev.minv)]
+    if tag == "rand":   # random q: every rotation block goes through the eigen-clamp
+        assert int(dev.counter[5]) > 0
+        assert bool((kpre[(dev.ipart[L.IP["E"], :dev.n] != 0)] >= 0).all())
+    # every (i,i) quadrant staged (ikpre = 0) so the blocks can be read back;
+    # the element pass then sums them itself: same bits
+    dev.sys.asm_flags = L.ASM_STAGE_ALL_A
     f, gnorm, cnorm, _ = prob.assemble(dev.xp, dev.xq)
+    dev.sys.asm_flags = 0
+    assert (f, gnorm) == (f0, g0)
+    for a, b_ in zip(ref, (dev.z, dev.diag, dev.minv)):
+        assert torch.equal(a, b_)
     assert f == pytest.approx(float(d[f"{tag}_f"]), rel=1e-12)
     assert gnorm == pytest.approx(float(d[f"{tag}_gnorm"]), rel=1e-10)
     z = _aos(dev.z, dev)
