@@ -95,6 +95,16 @@ def peaks():
         return FALLBACK_HBM_GBS, "fallback"
 
 
+def fp64_peak():
+    """Measured FP64 DFMA throughput of this B200 (profiles/r02/fp64_peak.json,
+    scratch/r02/fp64/fp64_peak.cu), TFLOP/s."""
+    try:
+        with open(os.path.join(REPO, "profiles", "r02", "fp64_peak.json")) as fh:
+            return float(json.load(fh)["fp64_dfma_tflops"]), "measured (profiles/r02/fp64_peak.json)"
+    except Exception:
+        return None, None
+
+
 # ---------------------------------------------------------------------------
 # the reference on the host cores (BASELINE.md §3)
 # ---------------------------------------------------------------------------
@@ -233,7 +243,8 @@ def run_reference(args):
 def config_block(args):
     return {"workload": f"C3 plate impact {args.nx}x{args.ny} (BASELINE configs[2])",
             "spheres": args.nx * args.ny, "epsilon": args.epsilon, "dt": 5e-6,
-            "l2": "inputs larger than L2 (bond staging 39 x n_bond fp64 >> 126 MB)",
+            "l2": "inputs larger than L2 (bond geometry 24 + staging 17 + coefficient 14 "
+                  "planes x n_bond fp64 = 1.97 GB >> 126 MB)",
             "parallelism": f"replicas x{args.gpus}"}
 
 
@@ -363,6 +374,21 @@ def c5_leg(n_side, peak):
            "bonds_per_sec_assembled": dev.nb / (asm_ms * 1e-3),
            "spmv_ms": spmv_ms, "spmv_bytes": sb, "spmv_gbs": sb / (spmv_ms * 1e-3) / 1e9,
            "spmv_frac": sb / (spmv_ms * 1e-3) / 1e9 / peak}
+    # FP64 view of the random-q assembly (every rotation block through the
+    # register Jacobi eigen-clamp): ncu FP64 operation counts of the same
+    # launch (2 flops per DFMA) over the live CUDA-event time
+    c5n = load_ncu_traffic().get("c5_block", {})
+    flops = _sum_or_none(c5n.get(k, {}).get("fp64_flops_per_launch")
+                         for k in ("k_bond_rows", "k_bond_clamp"))
+    fpk, fpk_src = fp64_peak()
+    if flops and fpk:
+        ach = flops / (asm_ms * 1e-3) / 1e12
+        out["fp64"] = {"bound": "fp64", "achieved": ach, "peak": fpk, "unit": "TFLOP/s",
+                       "frac": ach / fpk, "flops_per_launch": flops,
+                       "pipe_frac": {k: c5n.get(k, {}).get("fp64_pipe_frac")
+                                     for k in ("k_bond_rows", "k_bond_clamp")},
+                       "source": "ncu sm__sass_thread_inst_executed_op_{dfma,dmul,dadd} "
+                                 "(profiles/ncu_traffic.json)", "peak_source": fpk_src}
     del scene, dev
     torch.cuda.empty_cache()
     return out
@@ -426,6 +452,11 @@ def l2_roofline(ncu, spmv_ms, clocks):
     return {"bytes_per_launch": 32.0 * sectors, "achieved": achieved, "cap": cap, "unit": "GB/s",
             "frac": achieved / cap, "source": "ncu lts__t_sectors.sum x 32 B (profiles/ncu_traffic.json)",
             "cap_source": f"{L2_BYTES_PER_CLK:.0f} B/clk x sampled SM clock, {L2_CAP_SOURCE}"}
+
+
+def _sum_or_none(vals):
+    vals = list(vals)
+    return None if any(v is None for v in vals) else float(sum(vals))
 
 
 def load_ncu_traffic():
@@ -623,7 +654,13 @@ def run_ours(args):
                      "launches": len(basm), "bytes": ab,
                      "bytes_rule": "SURVEY 8(d): n_b (161 + 288) + n_f (136+144+144+48+56)",
                      "achieved_gbs": ab / (asm_ms * 1e-3) / 1e9,
-                     "frac": ab / (asm_ms * 1e-3) / 1e9 / peak},
+                     "frac": ab / (asm_ms * 1e-3) / 1e9 / peak,
+                     "traffic": _sum_or_none(traffic.get(k, {}).get("dram_bytes_per_launch")
+                                             for k in ("k_bond_rows", "k_element_assemble")),
+                     "fp64_pipe_frac": {k: traffic.get(k, {}).get("fp64_pipe_frac")
+                                        for k in ("k_bond_rows", "k_element_assemble")},
+                     "traffic_source": "ncu dram__bytes_read+write per launch "
+                                       "(profiles/ncu_traffic.json)"},
         "spmv": {"ms": spmv_ms, "launches": len(spmv), "bytes": sb, "achieved_gbs": achieved,
                  "timing": "CUDA events around every SpMV launch in a replay of the timed steps "
                            "(the timed region itself runs uninstrumented)",
