@@ -80,6 +80,9 @@ def parse():
     ap.add_argument("--ref-starts", type=lambda s: s.split(","),
                     default=["mid-solve", "predictor"],
                     help="reference start points, headline first")
+    ap.add_argument("--ref-workers", default="cores",
+                    help="SolverConfig.workers of the reference runs: 'cores', 'both' "
+                         "(cores and 1; BASELINE.md §3) or an integer")
     ap.add_argument("--max-retries", type=int, default=2,
                     help="dt-halving levels per timed step (runner.py:47-71)")
     return ap.parse_args()
@@ -205,7 +208,16 @@ def run_reference(args):
         return 0
     cores = os.cpu_count() or 1
     nx, ny = args.ref_plate if args.ref_plate else (args.nx, args.ny)
-    workers = sorted({cores, 1}, reverse=True)
+    # workers only threads spd_project (solver.py:48,107-110); measured on the
+    # GPU box: 172.7 s (16) vs 166.3 s (1) for the mid-solve start, 102.8 vs
+    # 97.2 s from the predictor (profiles/r02/reference_arm.json), so the
+    # default run uses cpu_count only and '--ref-workers both' adds workers=1
+    if args.ref_workers == "both":
+        workers = sorted({cores, 1}, reverse=True)
+    elif args.ref_workers == "cores":
+        workers = [cores]
+    else:
+        workers = [int(args.ref_workers)]
     mid = gpu_mid_iterate(__import__("paper_2308_10459_b200.configs", fromlist=["plate"])
                           .plate(nx=nx, ny=ny, epsilon=args.epsilon), args.epsilon) \
         if "mid-solve" in args.ref_starts else None

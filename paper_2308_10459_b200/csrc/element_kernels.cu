@@ -43,9 +43,6 @@ __device__ __forceinline__ double stage_stretch(const double *st, const double *
 // ---------------------------------------------------------------------------
 // element assembly
 // ---------------------------------------------------------------------------
-#ifndef BDEM_ELEM_JPREF
-#define BDEM_ELEM_JPREF 0
-#endif
 #ifndef BDEM_ELEM_MINB
 #define BDEM_ELEM_MINB 2
 #endif
@@ -93,37 +90,6 @@ __global__ void __launch_bounds__(kThreads, BDEM_ELEM_MINB) k_element_assemble(b
         }
       }
     }
-#if BDEM_ELEM_JPREF
-    // bonds with j == e (ascending bond id); the positions of the next pair
-    // of j-role slots are loaded while the current pair's pieces arrive
-    {
-      const int64_t j0 = S.jslice_base[sl] + lane, j1 = S.jslice_base[sl + 1];
-      int64_t b0 = j0 < j1 ? S.jpos[j0] : -1, b1 = j0 + 32 < j1 ? S.jpos[j0 + 32] : -1;
-#pragma unroll 1
-      for (int64_t k = j0; k < j1; k += 64) {
-        const int64_t n0 = k + 64 < j1 ? S.jpos[k + 64] : -1;
-        const int64_t n1 = k + 96 < j1 ? S.jpos[k + 96] : -1;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int64_t b = h == 0 ? b0 : b1;
-          if (b < 0) continue;
-          double n[3], apos[6];
-          const double kc = stage_stretch(st, S.scoef, nb, b, n, apos);
-#pragma unroll
-          for (int c = 0; c < 3; ++c) gp[c] += kc * n[c];
-#pragma unroll
-          for (int c = 0; c < 4; ++c) gq[c] += st[(BDEM_ST_GQJ + c) * nb + b];
-#pragma unroll
-          for (int t = 0; t < 6; ++t) {
-            P[t] += apos[t];
-            R[t] += st[(BDEM_ST_D + t) * nb + b];
-          }
-        }
-        b0 = n0;
-        b1 = n1;
-      }
-    }
-#else
     // bonds with j == e (ascending bond id)
 #pragma unroll 2
     for (int64_t k = S.jslice_base[sl] + lane; k < S.jslice_base[sl + 1]; k += 32) {
@@ -141,7 +107,6 @@ __global__ void __launch_bounds__(kThreads, BDEM_ELEM_MINB) k_element_assemble(b
         R[t] += st[(BDEM_ST_D + t) * nb + b];
       }
     }
-#endif
     // contacts: pairs then colliders into a separate accumulator (integrator.py:56-85,104-105)
     double gc[3] = {0.0, 0.0, 0.0};
     double epair = 0.0, ecol = 0.0;

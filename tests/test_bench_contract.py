@@ -20,7 +20,7 @@ def test_reference_arm_json_line():
         pytest.skip("reference bdem unavailable")
     out = subprocess.run(
         [sys.executable, os.path.join(REPO, "bench.py"), "--impl", "reference", "--steps", "3",
-         "--warmup", "0", "--ref-plate", "24", "14", "--ref-k", "1"],
+         "--warmup", "0", "--ref-plate", "24", "14", "--ref-k", "1", "--ref-workers", "both"],
         capture_output=True, text=True, timeout=600, cwd=REPO)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
