@@ -148,23 +148,11 @@ __global__ void __launch_bounds__(128) k_bond_ambient(bdem_system_t S, const dou
 #ifndef BDEM_ASM_MINB
 #define BDEM_ASM_MINB 6
 #endif
-#ifndef BDEM_ROWS_HOIST
-#define BDEM_ROWS_HOIST 0
-#endif
-#ifndef BDEM_ROWS_SMEM
-#define BDEM_ROWS_SMEM 1
-#endif
-#if BDEM_ROWS_SMEM
-#define ACC_T volatile double
-#else
-#define ACC_T double
-#endif
-#ifndef BDEM_ROWS_PREFETCH
-#define BDEM_ROWS_PREFETCH 0
-#endif
 #ifndef BDEM_ASM_THREADS
 #define BDEM_ASM_THREADS 64
 #endif
+#define ACC_T volatile double
+
 // row partial sums in shared memory: acc[first + c][t] += v[c] for c < N,
 // all loads issued before the adds and all stores after them (volatile
 // accesses keep program order, so an interleaved load/add/store sequence
@@ -186,11 +174,7 @@ __global__ void __launch_bounds__(BDEM_ASM_THREADS, BDEM_ASM_MINB) k_bond_rows(b
   __shared__ double acc_sh[BDEM_IP_COUNT][BDEM_ASM_THREADS];
   // volatile: every partial-sum update is a shared-memory read-modify-write
   // (the compiler would otherwise keep the 20 sums in registers and spill)
-#if BDEM_ROWS_SMEM
-  volatile double(*acc)[BDEM_ASM_THREADS] = acc_sh;
-#else
-  double(*acc)[BDEM_ASM_THREADS] = acc_sh;
-#endif
+  ACC_T(*acc)[BDEM_ASM_THREADS] = acc_sh;
   const int t = threadIdx.x;
   const int64_t nrow = ((S.n_elem + 31) >> 5) << 5;
   const int64_t row = blockIdx.x * (int64_t)BDEM_ASM_THREADS + t;
@@ -201,34 +185,16 @@ __global__ void __launch_bounds__(BDEM_ASM_THREADS, BDEM_ASM_MINB) k_bond_rows(b
   const int e = S.row_elem[row];
   const int64_t nb = S.n_bond;
   double *st_out = S.stage;
-  const double *g = S.geom;
   int kpre = (S.asm_flags & BDEM_ASM_STAGE_ALL_A) ? 0 : -1;
   const int64_t b_end = S.slice_base[sl + 1];
-#if BDEM_ROWS_HOIST
-  double pi[3] = {0.0, 0.0, 0.0}, qi[4] = {0.0, 0.0, 0.0, 1.0};
-  if (e >= 0) load_pq(p, q, e, pi, qi);
-#endif
-  int k = 0;
   const int64_t b_beg = S.slice_base[sl] + lane;
-#if BDEM_ROWS_PREFETCH
-  // software pipeline on the slot's status and j index: the next slot's
-  // (dependent-gather-feeding) index is in flight while this bond computes
-  int8_t stat_n = b_beg < b_end ? S.status[b_beg] : (int8_t)2;
-  int bj_n = b_beg < b_end ? S.bond_j[b_beg] : 0;
-#endif
+  const double *g = S.geom;
+  int k = 0;
 #pragma unroll 1
   for (int64_t b = b_beg; b < b_end; b += 32, ++k) {
     double *cf = S.scoef + cf_idx(b, 0);
-#if BDEM_ROWS_PREFETCH
-    const int8_t stat = stat_n;
-    const int bj = bj_n;
-    if (b + 32 < b_end) {
-      stat_n = S.status[b + 32];
-      bj_n = S.bond_j[b + 32];
-    }
-#else
     const int8_t stat = S.status[b];
-#endif
+#define GEO(f) g[(f) * nb + b]
     if (stat == 2) {  // broken or padding: no energy, no coupling
 #pragma unroll
       for (int c = 0; c < BDEM_ST_COUNT; ++c) st_out[c * nb + b] = 0.0;
@@ -238,23 +204,17 @@ __global__ void __launch_bounds__(BDEM_ASM_THREADS, BDEM_ASM_MINB) k_bond_rows(b
     }
     // pieces are stored (and summed) as soon as they are final so the
     // stretch state is dead before the rotation block is formed
-#if !BDEM_ROWS_PREFETCH
-    const int bj = S.bond_j[b];
-#endif
-    const double scale = S.bstate[BDEM_BS_SCALE * nb + b];
-    double pj[3], qj[4];
-#if !BDEM_ROWS_HOIST
-    double pi[3], qi[4];
+    double pi[3], qi[4], pj[3], qj[4];
     load_pq(p, q, e, pi, qi);
-#endif
-    load_pq(p, q, bj, pj, qj);
+    const double scale = S.bstate[BDEM_BS_SCALE * nb + b];
+    load_pq(p, q, S.bond_j[b], pj, qj);
 
     // stretch: energy, gradient (kc n) and the closed-form clamp of
     // [[a,-a],[-a,a]]: a+ = k (nn + max(c/l,0) (I - nn)) = alpha nn + beta I
     double e_s;
     {
-      const double ks = scale * g[BDEM_BG_KN * nb + b];
-      const Stretch st = stretch_eval(pi, pj, g[BDEM_BG_L0 * nb + b], ks);
+      const double ks = scale * GEO(BDEM_BG_KN);
+      const Stretch st = stretch_eval(pi, pj, GEO(BDEM_BG_L0), ks);
       if (st.degenerate) flag_error(S.err, BDEM_ERR_DEGENERATE_BOND, b);
       const double f = st.c_over_l > 0.0 ? st.c_over_l : 0.0;
       const double beta = ks * f;
@@ -283,12 +243,12 @@ __global__ void __launch_bounds__(BDEM_ASM_THREADS, BDEM_ASM_MINB) k_bond_rows(b
 #pragma unroll
       for (int r = 0; r < 3; ++r)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) F[r][c] = g[(BDEM_BG_FRAME + 3 * r + c) * nb + b];
+        for (int c = 0; c < 3; ++c) F[r][c] = GEO(BDEM_BG_FRAME + 3 * r + c);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) kds[c] = scale * g[(BDEM_BG_KDIAG + c) * nb + b];
+      for (int c = 0; c < 3; ++c) kds[c] = scale * GEO(BDEM_BG_KDIAG + c);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) d0[c] = g[(BDEM_BG_D0 + c) * nb + b];
-      const Shear sh = shear_eval(qi, qj, d0, scale * g[BDEM_BG_KT * nb + b]);
+      for (int c = 0; c < 3; ++c) d0[c] = GEO(BDEM_BG_D0 + c);
+      const Shear sh = shear_eval(qi, qj, d0, scale * GEO(BDEM_BG_KT));
       if (sh.antipodal) flag_error(S.err, BDEM_ERR_ANTIPODAL, b);
       const RotGrad ro = rot_grad(qi, qj, F, kds);
       double eg[5];
@@ -302,6 +262,7 @@ __global__ void __launch_bounds__(BDEM_ASM_THREADS, BDEM_ASM_MINB) k_bond_rows(b
       acc_add<4>(acc, BDEM_IP_GQ, t, eg + 1);
       rot_block(qi, qj, d0, F, kds, sh, ro.rs, ro.rv, ro.w, S6);
     }
+#undef GEO
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll

@@ -396,6 +396,53 @@ def gold_rope100k():
     save("traj_rope100k.npz", **out)
 
 
+def gold_cube22():
+    """BASELINE configs[1] at its full size (22^3 = 10,648 jittered spheres,
+    radii U(0.9r, 1.1r), E = 3e9, PlasticParams(1e-3, 6e-4, 0.5, 2), a rigid
+    plane descending at 0.5 m/s, dt = 1e-4) in the identity-q variant SURVEY
+    8(d) prescribes for trajectory parity (random q is un-steppable by the
+    reference).  The first steps of the reference, eps 1e-6: p, v on a strided
+    subsample of rows plus both ends, whole-array norms, counts, the first
+    Newton record (predictor) and the fracture / yield state of every bond."""
+    spec = C.cube(random_q=False, epsilon=1e-6)
+    sched = spec.collider_schedule
+    sc = ref_scene(spec)
+    cfg = rsv.SolverConfig(epsilon=1e-6, max_iterations=300)
+    rows = _subsample_rows(spec.elements.n, 37)
+    rec = {k: [] for k in ("p", "v", "newton", "pcg", "committed", "gnorm", "p_norm",
+                           "v_norm", "rec0_f", "rec0_gnorm", "n_yielded", "reason")}
+    events = []
+    t0 = time.time()
+    for s in range(int(os.environ.get("CUBE22_STEPS", 4))):
+        sc.colliders = ref_colliders(sched(sc.time + sc.dt))
+        rep = rsv.stable_step(sc, cfg)
+        el = sc.elements
+        rec["p"].append(el.p[rows].copy())
+        rec["v"].append(el.v[rows].copy())
+        rec["p_norm"].append(float(np.linalg.norm(el.p)))
+        rec["v_norm"].append(float(np.linalg.norm(el.v)))
+        rec["newton"].append(rep.solve.iterations)
+        rec["pcg"].append(rep.solve.pcg_total)
+        rec["committed"].append(rep.committed)
+        rec["gnorm"].append(rep.solve.grad_norm)
+        rec["reason"].append(rep.solve.reason)
+        rec["rec0_f"].append(rep.solve.records[0].f)
+        rec["rec0_gnorm"].append(rep.solve.records[0].grad_norm)
+        rec["n_yielded"].append(int(np.count_nonzero(sc.bonds.status == 1)))
+        events += [(s, b, sg, tu) for (b, sg, tu) in rep.broken]
+        print(f"    step {s}: newton {rep.solve.iterations} pcg {rep.solve.pcg_total} "
+              f"{rep.solve.reason} gnorm {rep.solve.grad_norm:.3e} yielded "
+              f"{rec['n_yielded'][-1]} broken {len(rep.broken)} ({time.time() - t0:.0f}s)",
+              flush=True)
+    out = {k: np.array(v) for k, v in rec.items()}
+    out["events"] = np.array(events, dtype=float).reshape(-1, 4)
+    out.update(pack("final_b_", sc.bonds, ("status", "stiffness_scale", "damage",
+                                           "plastic_strain", "sigma", "tau")))
+    out.update({"rows": rows, "n": spec.elements.n, "epsilon": 1e-6,
+                "seconds": time.time() - t0})
+    save("traj_cube22.npz", **out)
+
+
 def gold_plate600k():
     """The north-star config at full size (BASELINE configs[2], SURVEY 8(d) C3:
     1000x600 plate, 3,591,004 bonds, eps 1e-3): the step-1 problem exactly as

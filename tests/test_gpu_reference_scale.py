@@ -112,3 +112,43 @@ def test_rope100k_twist_vs_reference(cuda_ok):
         qdn = float(torch.linalg.vector_norm(dev.qdot))
         assert qdn == pytest.approx(float(g["qdot_norm"][s]), rel=1e-6)
     assert float(g["q_dev_norm"][-1]) > 1e-3      # the rotation path really moved
+
+
+def test_cube22_identity_q_vs_reference(cuda_ok):
+    """BASELINE configs[1] at full size (22^3 = 10,648 jittered spheres,
+    radii U(0.9r, 1.1r), plasticity and fracture, plane descending at 0.5
+    m/s) in SURVEY 8(d)'s identity-q variant: the reference's first steps
+    (``traj_cube22.npz``).  Positions rtol 1e-8 + 10 eps/(m/dt^2) on a
+    strided subsample and as whole-array norms; the predictor's Newton record;
+    the yield / fracture state of every bond exactly."""
+    import torch
+
+    from paper_2308_10459_b200 import SolverConfig, configs as C, stable_step
+    from paper_2308_10459_b200.scene import Scene
+    g = load("traj_cube22.npz")
+    spec = C.cube(random_q=False, epsilon=float(g["epsilon"]))
+    sched = spec.collider_schedule
+    scene = Scene.from_spec(spec, host_sync=False)
+    dev = scene.device
+    assert dev.n == int(g["n"])
+    rows = torch.as_tensor(g["rows"]).cuda()
+    cfg = SolverConfig(epsilon=float(g["epsilon"]), max_iterations=300)
+    m_dt2 = float((spec.elements.mass / spec.dt**2).min())
+    atol_p = 10 * cfg.epsilon / m_dt2
+    for s in range(g["p"].shape[0]):
+        scene.colliders = sched(scene.time + scene.dt)
+        rep = stable_step(scene, cfg)
+        assert rep.committed == bool(g["committed"][s])
+        r0 = rep.solve.records[0]     # at the predictor: same inputs up to the last step's tolerance
+        assert r0.f == pytest.approx(float(g["rec0_f"][s]), rel=1e-9)
+        assert r0.grad_norm == pytest.approx(float(g["rec0_gnorm"][s]), rel=1e-6)
+        got_p = dev.p[rows].cpu().numpy()
+        _assert_close(got_p, g["p"][s], 1e-8, atol_p, f"p {s}")
+        _assert_close(dev.v[rows].cpu().numpy(), g["v"][s], 1e-6, atol_p / spec.dt, f"v {s}")
+        assert float(torch.linalg.vector_norm(dev.p)) == pytest.approx(float(g["p_norm"][s]),
+                                                                       rel=1e-10)
+    scene.sync_to_host()
+    b = scene.bonds
+    np.testing.assert_array_equal(b.status, g["final_b_status"])
+    for k in ("stiffness_scale", "damage", "plastic_strain"):
+        _assert_close(getattr(b, k), g[f"final_b_{k}"], 1e-8, 1e-12, k)
