@@ -300,7 +300,10 @@ int bdem_pair_assemble(const bdem_system_t *sys, const double *p, int energy_onl
  * inertia (integrator.py:195-200), colliders (contact.py:227-248), reduced
  * gradient z (solver.py:116-123), diagonal blocks + element terms
  * (solver.py:164-173, 198-248), block-Jacobi inverses (linalg.py:100-128) and
- * the objective / |z| / constraint reductions. */
+ * the objective / |z| / constraint reductions.  Continues the i-role partial
+ * sums of the bdem_bond_assemble call at the same (p, q) (sys->ipart,
+ * sys->ikpre) with the j-role pieces it staged: call bdem_bond_assemble (and,
+ * with contact pairs, bdem_pair_assemble) first. */
 int bdem_element_assemble(const bdem_system_t *sys, const double *p, const double *q,
                           double *z, void *stream);
 
