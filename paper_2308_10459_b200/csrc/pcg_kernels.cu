@@ -161,7 +161,8 @@ __device__ __forceinline__ void spmv_tail(const bdem_system_t &S, const double *
               ps[(BDEM_PS_A + sidx<3>(c, 2)) * pc + k] * x[2 * nf + o];
       }
     }
-    const double xc = xs[rr];
+    // (a select, not xs[rr]: a run-time index would put xs in local memory)
+    const double xc = rr == 0 ? xs[0] : (rr == 1 ? xs[1] : xs[2]);
     if (boost != 0.0) yc = yc + boost * xc;
     y[c * nf + s] = yc;
     acc_xy += xc * yc;
