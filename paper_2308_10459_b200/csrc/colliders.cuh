@@ -47,9 +47,12 @@ __device__ inline void collider_eval(const bdem_collider_t &C, const double p[3]
         H[t] = div_nz(act - n[pr[t]] * n[pc[t]], ons);
       }
     } else {
+      // first axis of largest d (selects, not d[ax]: a run-time index would
+      // put d in local memory)
       int ax = 0;
-      if (d[1] > d[ax]) ax = 1;
-      if (d[2] > d[ax]) ax = 2;
+      double dmax = d[0];
+      if (d[1] > dmax) { ax = 1; dmax = d[1]; }
+      if (d[2] > dmax) ax = 2;
 #pragma unroll
       for (int c = 0; c < 3; ++c) dg[c] = (c == ax ? 1.0 : 0.0) * sign[c];
     }
