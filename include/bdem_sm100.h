@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define BDEM_ABI_VERSION 6
+#define BDEM_ABI_VERSION 7
 
 enum {
   BDEM_OK = 0,
@@ -238,6 +238,9 @@ typedef struct {
   int32_t *clamp_list;           /* (n_bond) queue of indefinite rotation blocks */
   double *ipart;                 /* BDEM_IP_COUNT planes x n_rows: i-role partial sums */
   int32_t *ikpre;                /* (n_rows) first slot with a staged (i,i) quadrant, -1 */
+  double *grad_p, *grad_q;       /* optional (n,3) / (n,4): bdem_element_assemble writes the
+                                    ambient gradient of the incremental potential
+                                    (ImplicitProblem.value_and_gradient); NULL = off */
   /* physics */
   double gravity[3];
   double k_contact, k_element;
@@ -293,6 +296,16 @@ int bdem_bond_update(const bdem_system_t *sys, const double *p, const double *q,
  * clamped pair blocks (spd_project, solver.py:162) into sys->pstage. */
 int bdem_pair_assemble(const bdem_system_t *sys, const double *p, int energy_only,
                        void *stream);
+
+/* Ambient contact Hessian blocks at p (PotentialModel.hessian_blocks,
+ * integrator.py:111-129): pair_pp (n_pair, 6, 6) = [[a, -a], [-a, a]] with
+ * a = k_element (nn - (depth / l)(I - nn)) for touching pairs, else 0
+ * (self_repulsion_terms, contact.py:180-224); elem_pp (n_elem, 3, 3) = the
+ * sum over colliders of k_contact (grad g grad g^T + g hess g) for
+ * penetrating centers (external_repulsion_terms, contact.py:227-248).
+ * Row-major; either output may be NULL. */
+int bdem_contact_blocks(const bdem_system_t *sys, const double *p, double *pair_pp,
+                        double *elem_pp, void *stream);
 
 /* ---- elements ---------------------------------------------------------- */
 

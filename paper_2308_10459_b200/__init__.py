@@ -21,6 +21,8 @@ __all__ = [
     "energy_terms", "label_components", "minimize_second_order", "relative_tolerance",
     "stable_step", "stretch_driver", "twist_driver", "update_bond_states",
     "rotation_free_pcg", "BROKEN", "INTACT", "WEAKENED",
+    "ImplicitProblem", "PotentialBlocks", "PotentialModel", "StepContext",
+    "incremental_potential",
 ]
 
 
@@ -44,4 +46,8 @@ def __getattr__(name):
     if name == "energy_terms":
         from .bond_api import energy_terms
         return energy_terms
+    if name in ("ImplicitProblem", "PotentialBlocks", "PotentialModel", "StepContext",
+                "incremental_potential"):
+        from . import problem
+        return getattr(problem, name)
     raise AttributeError(name)

@@ -30,7 +30,7 @@ SC = dict(F=0, GNORM2=1, CNORM2=2, MAXDEV=3, SLOPE=4, FT=5, NSING=6, EBOND=7, EC
 PCG = dict(RZ=0, PAP=1, ALPHA=2, BETA=3, RR=4, BNORM=5, REL=6, TOL=7, BOOST=8, APNORM2=9,
            PNORM2=10, K=11, MAXIT=12, STATE=13, ROTZERO=14, COUNT=16)
 PCG_RUNNING, PCG_CONVERGED, PCG_BREAKDOWN, PCG_MAXIT = 0, 1, 2, 3
-ABI_VERSION = 6
+ABI_VERSION = 7
 RED_BLOCKS = 1184
 MAX_COLLIDERS = 8
 N_COUNTERS = 16
@@ -55,7 +55,7 @@ class System(C.Structure):
         ("pair_i", _p), ("pair_j", _p), ("pi_ptr", _p), ("pj_ptr", _p), ("pj_idx", _p),
         ("stage", _p), ("scoef", _p), ("pstage", _p), ("diag", _p), ("minv", _p), ("red", _p),
         ("scalars", _p), ("pcg", _p), ("err", _p), ("counter", _p), ("clamp_list", _p),
-        ("ipart", _p), ("ikpre", _p),
+        ("ipart", _p), ("ikpre", _p), ("grad_p", _p), ("grad_q", _p),
         ("gravity", C.c_double * 3), ("k_contact", C.c_double), ("k_element", C.c_double),
         ("n_colliders", C.c_int32), ("asm_flags", C.c_int32),
         ("colliders", Collider * MAX_COLLIDERS),
@@ -84,6 +84,7 @@ SIGNATURES = {
     "bdem_reduce_finish": (_int, [_sys, _int, _int, _int, _p]),
     "bdem_trial_point": (_int, [_sys, _p, _p, _p, _p, _dbl, _p, _p, _p]),
     "bdem_element_energy": (_int, [_sys, _p, _p, _int, _p]),
+    "bdem_contact_blocks": (_int, [_sys, _p, _p, _p, _p]),
     "bdem_kinetic": (_int, [_sys, _p, _p, _p]),
     "bdem_normalize_free": (_int, [_sys, _p, _p]),
     "bdem_direction": (_int, [_sys, _p, _p, _dbl, _p, _p, _p]),

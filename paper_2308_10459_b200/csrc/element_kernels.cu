@@ -214,6 +214,11 @@ __global__ void __launch_bounds__(kThreads, BDEM_ELEM_MINB) k_element_assemble(b
         for (int t = 0; t < 6; ++t) { mi[t * nf] = Pi[t]; mi[(6 + t) * nf] = Ri[t]; }
       }
     }
+    if (S.grad_p != nullptr) {   // ImplicitProblem.value_and_gradient (integrator.py:195-200)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) S.grad_p[3 * e + c] = gp[c];
+      store_q(S.grad_q, e, gq);
+    }
     acc_f += fe;
   }
   double v;
@@ -467,6 +472,67 @@ __global__ void k_reset_errors(int32_t *err) {
                  ? 0x7fffffff : 0;
 }
 
+// ambient contact Hessian blocks (PotentialModel.hessian_blocks): pairs
+// [[a,-a],[-a,a]] (contact.py:209-223) and summed collider blocks
+// (contact.py:243-247, integrator.py:76-83), row-major
+__global__ void __launch_bounds__(kThreads) k_contact_blocks(bdem_system_t S, const double *p,
+                                                             double *pair_pp, double *elem_pp) {
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (pair_pp != nullptr) {
+    for (int64_t k = t0; k < S.n_pair; k += stride) {
+      const int64_t i = S.pair_i[k], j = S.pair_j[k];
+      double d[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) d[c] = p[3 * j + c] - p[3 * i + c];
+      const double len = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+      const double depth = fmax(0.0, (S.radius[i] + S.radius[j]) - len);
+      double n[3];
+      if (len < 1e-12) {
+        n[0] = 1.0; n[1] = 0.0; n[2] = 0.0;
+      } else {
+        const double l = fmax(len, 1e-300);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) n[c] = div_nz(d[c], l);
+      }
+      const bool touch = depth > 0.0;
+      const double f = depth / fmax(len, 1e-300);
+      double *H = pair_pp + 36 * k;
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double nn = n[r] * n[c];
+          const double a = touch ? S.k_element * (nn - f * ((r == c ? 1.0 : 0.0) - nn)) : 0.0;
+          H[6 * r + c] = a;
+          H[6 * (r + 3) + c + 3] = a;
+          H[6 * r + c + 3] = -a;
+          H[6 * (r + 3) + c] = -a;
+        }
+    }
+  }
+  if (elem_pp != nullptr) {
+    for (int64_t e = t0; e < S.n_elem; e += stride) {
+      double pe[3];
+      load_p(p, e, pe);
+      double Hc[6] = {0, 0, 0, 0, 0, 0};
+      for (int ci = 0; ci < S.n_colliders; ++ci) {
+        double g, dg[3], Hs[6];
+        collider_eval(S.colliders[ci], pe, g, dg, Hs);
+        const int pr[6] = {0, 0, 0, 1, 1, 2}, pcc[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+        for (int t = 0; t < 6; ++t)
+          Hc[t] += g < 0.0 ? S.k_contact * (dg[pr[t]] * dg[pcc[t]] + g * Hs[t]) : 0.0;
+      }
+      double *H = elem_pp + 9 * e;
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) H[3 * r + c] = Hc[sidx<3>(r, c)];
+    }
+  }
+}
+
 }  // namespace bdem
 
 using namespace bdem;
@@ -494,6 +560,15 @@ int bdem_trial_point(const bdem_system_t *sys, const double *p, const double *q,
   if (!sys || !dp || !dq || !p_t || !q_t) return BDEM_ERR_ARG;
   k_element_energy<<<kRedBlocks, kThreads, 0, as_stream(stream)>>>(*sys, p, q, dp, dq, alpha,
                                                                     p_t, q_t, 1);
+  return launch_status();
+}
+
+int bdem_contact_blocks(const bdem_system_t *sys, const double *p, double *pair_pp,
+                        double *elem_pp, void *stream) {
+  if (!sys || !p) return BDEM_ERR_ARG;
+  const int64_t m = sys->n_pair > sys->n_elem ? sys->n_pair : sys->n_elem;
+  if (m == 0 || (!pair_pp && !elem_pp)) return BDEM_OK;
+  k_contact_blocks<<<grid_for(m), kThreads, 0, as_stream(stream)>>>(*sys, p, pair_pp, elem_pp);
   return launch_status();
 }
 

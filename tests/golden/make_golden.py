@@ -263,6 +263,63 @@ def gold_colliders():
     save("colliders.npz", **out)
 
 
+def gold_problem_protocol():
+    """The ImplicitProblem protocol (integrator.py:24-35, 39-138, 164-210) on a
+    scene with every term: bonds (some broken), frozen contact pairs across
+    a crack, a half-space, a sphere and a box collider, pinned elements,
+    perturbed orientations.  value, value_and_gradient, hessian_blocks,
+    inertia_diag and the model's value / energy_breakdown at a state where
+    every contact term is active."""
+    spec, rng = _small_problem(seed=81)
+    el = spec.elements
+    lo, hi = el.p.min(axis=0), el.p.max(axis=0)
+    mid = 0.5 * (lo + hi)
+    z_top = float(hi[2])
+    cols = [rc.HalfSpace((0.0, 0.0, -1.0), -(z_top - 0.3 * 0.002)),
+            rc.SphereCollider(tuple(mid + np.array([0.0, 0.0, 0.004])), 0.005),
+            rc.BoxCollider(tuple(np.array([lo[0], mid[1], mid[2]])), (0.003, 0.02, 0.02))]
+    b = spec.bonds
+    cross = (el.p[b.i, 0] < mid[0]) != (el.p[b.j, 0] < mid[0])
+    b.status[cross] = 2
+    sc = ref_scene(spec, colliders=cols)
+    e = sc.elements
+    pairs = rc.broad_phase(e.p, e.radius, 2.0 * float(e.radius.max()) + 1e-12)
+    pairs = pairs[(e.p[pairs[:, 0], 0] < mid[0]) != (e.p[pairs[:, 1], 0] < mid[0])]
+    ctx = ri.StepContext(sc.dt, sc.p_prev.copy(), sc.q_prev.copy(), e.p.copy(), e.q.copy())
+    model = ri.PotentialModel(e, sc.bonds, pairs, sc.colliders, sc.gravity, sc.k_contact,
+                              sc.k_element)
+    prob = ri.ImplicitProblem(model, ctx)
+    p0, q = ri.predict_state(ctx, e.v, e.qdot, prob.free)
+    # push the halves into each other so the pairs overlap
+    p = p0 + 1e-5 * rng.normal(size=p0.shape) * prob.free[:, None]
+    p[:, 0] += np.where(p[:, 0] < mid[0], 4e-4, -4e-4) * prob.free
+    f, gp, gq = prob.value_and_gradient(p, q)
+    hb = prob.hessian_blocks(p, q)
+    mp, mq = prob.inertia_diag()
+    touching = int(np.count_nonzero(np.abs(hb.pair_pp).sum(axis=(1, 2)) > 0))
+    inside = int(np.count_nonzero(np.abs(hb.elem_pp).sum(axis=(1, 2)) > 0))
+    print(f"  problem protocol: {pairs.shape[0]} pairs ({touching} touching), {inside} elements "
+          f"in a collider, {int(np.count_nonzero(cross))} broken bonds")
+    out = pack("el_", spec.elements, ELEM_FIELDS)
+    out.update(pack("b_", spec.bonds, BOND_FIELDS))
+    out.update({
+        "dt": sc.dt, "kc": sc.k_contact, "ke": sc.k_element, "gravity": sc.gravity,
+        "hs": np.array([*cols[0].normal, cols[0].offset]),
+        "sphere": np.array([*cols[1].center, cols[1].radius]),
+        "box": np.array([*cols[2].center, *cols[2].half_extents]),
+        "pairs": pairs, "p_prev": ctx.p_prev, "q_prev": ctx.q_prev, "p_curr": ctx.p_curr,
+        "q_curr": ctx.q_curr, "p": p, "q": q, "f": f, "gp": gp, "gq": gq,
+        "value": prob.value(p, q), "model_value": model.value(p, q),
+        "eb_bond": model.energy_breakdown(p, q)["bond"],
+        "eb_contact": model.energy_breakdown(p, q)["contact"],
+        "eb_gravity": model.energy_breakdown(p, q)["gravity"],
+        "hb_bond_i": hb.bond_i, "hb_bond_j": hb.bond_j, "hb_bond_pp": hb.bond_pp,
+        "hb_bond_qq": hb.bond_qq, "hb_pair_pp": hb.pair_pp, "hb_elem_pp": hb.elem_pp,
+        "mp_dt2": mp, "mq_dt2": mq,
+    })
+    save("problem_protocol.npz", **out)
+
+
 def gold_runner():
     """run_simulation + _step_with_retries + stats.csv (runner.py:20-164): a
     plain run, a run whose third frame needs dt halving (max_iterations=4),

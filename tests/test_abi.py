@@ -24,7 +24,7 @@ def test_exports_every_header_symbol(lib):
 
 
 def test_struct_layout_and_version(lib):
-    assert lib.bdem_abi_version() == L.ABI_VERSION == 6
+    assert lib.bdem_abi_version() == L.ABI_VERSION == 7
     assert lib.bdem_system_size() == ctypes.sizeof(L.System)
 
 
