@@ -406,6 +406,38 @@ def c5_leg(n_side, peak):
     return out
 
 
+def pcg_leg(dev, peak, traffic, chunk=32, reps=3):
+    """One PCG iteration as a whole (SpMV + r/z update + p update, the loop
+    that takes ~85% of a Newton iteration): a chunk of iterations of
+    bdem_pcg_iterate on the last assembled system (full 6-DOF, tolerance 0
+    so every launch works), CUDA events around the chunk, best of reps;
+    against the ncu DRAM bytes of the three kernels per iteration."""
+    import torch
+    ptrs = (dev.y.data_ptr(), dev.r.data_ptr(), dev.zv.data_ptr(), dev.pv.data_ptr())
+    best = float("inf")
+    for _ in range(reps):
+        dev.call("bdem_pcg_init", dev.sysp, dev.z.data_ptr(), -1.0, *ptrs, 1e-30, 100000, 0.0,
+                 dev.stream)
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        dev.call("bdem_pcg_iterate", dev.sysp, *ptrs, dev.ap.data_ptr(), chunk, dev.stream)
+        b.record()
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b) * 1e3 / chunk)
+    dram = _sum_or_none(traffic.get(k, {}).get("dram_bytes_per_launch")
+                        for k in ("k_spmv", "k_pcg_update", "k_pcg_pupdate"))
+    out = {"us": best, "chunk": chunk, "dram_bytes": dram,
+           "timing": "CUDA events around bdem_pcg_iterate chunks on the last assembled system"}
+    if dram:
+        out.update({"achieved_gbs": dram / (best * 1e-6) / 1e9,
+                    "frac": dram / (best * 1e-6) / 1e9 / peak,
+                    "bytes_source": "ncu dram__bytes_read+write of the three in-chain kernels "
+                                    "(profiles/ncu_traffic.json)"})
+    return out
+
+
 def reduce_across_ranks(times_ms, counts, world, device):
     """Replica aggregation: device times -> max over ranks, work -> sum."""
     import torch
@@ -567,6 +599,8 @@ def run_ours(args):
     durations = timer.resolve()
     dev.timer = None
 
+    pcg_it = pcg_leg(dev, peaks()[0], load_ncu_traffic())
+
     # e2e: the same steps again, from the same state, through the same public
     # call with host buffers every stable_step (H2D of the state before, D2H after)
     n_e2e = args.e2e_steps if args.e2e_steps is not None else args.steps
@@ -677,6 +711,7 @@ def run_ours(args):
                  "timing": "CUDA events around every SpMV launch in a replay of the timed steps "
                            "(the timed region itself runs uninstrumented)",
                  "replay_newton_iterations": replay["newton"]},
+        "pcg_iteration": pcg_it,
         "roofline": {"kernel": "bdem::k_spmv (PCG SpMV)", "bound": "hbm", "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": peak_kind,
