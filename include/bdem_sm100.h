@@ -374,12 +374,6 @@ int bdem_finish_step(const bdem_system_t *sys, const double *p, const double *q,
  * solver.py:198-258, applied as `mat @ v`, solver.py:475).  Also writes the
  * per-block partials of x.y, |y|^2, |x|^2 for PCG. */
 int bdem_spmv(const bdem_system_t *sys, const double *x, double *y, void *stream);
-/* PCG update path of bdem_pcg_iterate: 0 = k_pcg_update + k_pcg_pupdate
- * (default), 1 = one fused kernel over a co-resident grid (grid barrier
- * between the r/z and the x/p halves; bit-identical iterates; used only when
- * n_free <= BDEM_RED_BLOCKS * 512).  Returns the previous setting; any other
- * value only queries.  BDEM_FUSED_UPD=1 selects it at load time. */
-int bdem_pcg_set_fused(int on);
 /* Rotation-free PCG: when on and the rotation half of the right-hand side
  * is identically zero at bdem_pcg_init (e.g. identity orientations with no
  * rotational load, as on the BASELINE plate), the rotation halves of every

@@ -108,7 +108,6 @@ SIGNATURES = {
     "bdem_components": (_int, [_i64, _i64, _p, _p, _p, _p, _p, C.POINTER(C.c_int64), _p]),
     "bdem_select_workspace": (_i64, [_i64]),
     "bdem_select_flagged": (_int, [_p, _i64, _p, _p, C.POINTER(C.c_int64), _p]),
-    "bdem_pcg_set_fused": (_int, [_int]),
     "bdem_pcg_set_rot_skip": (_int, [_int]),
     "bdem_friction_workspace": (_i64, [_i64, _i64]),
     "bdem_friction": (_int, [_p, _p, _p, _p, _p, _dbl, _dbl, _dbl, _p, C.POINTER(C.c_int64), _p]),

@@ -574,174 +574,6 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(bdem_system_t S, doubl
   TL_EXIT(2, tl_it)
 }
 
-// ---------------------------------------------------------------------------
-// Fused PCG update (k_pcg_update + k_pcg_pupdate in one resident grid):
-//   phase 1: r -= alpha Ap; z = M^-1 r (z kept in shared memory); r.r, r.z
-//            partials per virtual block;
-//   grid barrier; every block sums the partials in the fixed order of
-//            sum_partials (identical scalars in every block) and applies the
-//            state transition of k_pcg_update (linalg.py:79-91);
-//   phase 2: x += alpha p and p = z + beta p from one read of p.
-// Work is laid out in kRedBlocks VIRTUAL blocks of kThreads threads with the
-// thread -> slot-pair map of k_pcg_update, and each resident block runs
-// virtual blocks b, b + gridDim.x, ...  Partial sums are formed per virtual
-// block exactly as there, so every scalar -- and hence the iterate -- is
-// bit-identical to the two-kernel path.  Per free row this moves 432 bytes
-// instead of 576 (z never leaves the SM, p is read once).  The grid must be
-// co-resident (launched with the occupancy-sized grid, see upd_fused_grid).
-// ---------------------------------------------------------------------------
-constexpr int kFusedMaxV = 2;  // virtual blocks per resident block
-enum { CNT_BAR_COUNT = 7, CNT_BAR_GEN = 8 };
-
-__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int *p) {
-  unsigned int v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// sense-reversing (generation) barrier over a co-resident grid
-__device__ __forceinline__ void grid_barrier(unsigned int *count, unsigned int *gen) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int g = ld_acquire_u32(gen);
-    __threadfence();
-    if (atomicAdd(count, 1u) == gridDim.x - 1) {
-      *count = 0u;
-      __threadfence();
-      atomicAdd(gen, 1u);
-    } else {
-      while (ld_acquire_u32(gen) == g) __nanosleep(64);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(kThreads, 4) k_pcg_update_fused(bdem_system_t S, double *x,
-                                                                   double *r, const double *ap,
-                                                                   double *p) {
-  extern __shared__ double2 zsh[];  // [kFusedMaxV][6][kThreads]
-  __shared__ double sh[kThreads / 32];
-  griddep_wait();
-  double *pcg = S.pcg;
-  if (pcg[BDEM_PCG_STATE] != PCG_RUNNING) return;
-  const double alpha = pcg[BDEM_PCG_ALPHA];
-  const double rz_old = pcg[BDEM_PCG_RZ], k_old = pcg[BDEM_PCG_K];
-  const double bnorm = pcg[BDEM_PCG_BNORM], tol = pcg[BDEM_PCG_TOL];
-  const double maxit = pcg[BDEM_PCG_MAXIT];
-  const int halves = pcg_rot_active(pcg) ? 2 : 1;
-  const int64_t nf = S.vstride;
-  const int64_t h2 = nf >> 1;
-  const double2 *ap2 = reinterpret_cast<const double2 *>(ap);
-  double2 *r2 = reinterpret_cast<double2 *>(r);
-  const double2 *mi2 = reinterpret_cast<const double2 *>(S.minv);
-  // phase 1 (k_pcg_update's loop body, one slot pair per virtual thread)
-#pragma unroll
-  for (int v = 0; v < kFusedMaxV; ++v) {
-    const int vb = blockIdx.x + v * gridDim.x;
-    if (vb >= kRedBlocks) break;
-    double acc_rr = 0.0, acc_rz = 0.0;
-    const int64_t t = (int64_t)vb * kThreads + threadIdx.x;
-    if (t < h2) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (h >= halves) break;
-        double ra[3], rb[3], ma[6], mb[6], za[3], zb[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const int64_t k = (3 * h + c) * h2 + t;
-          const double2 rv = __ldcs(r2 + k), av = __ldcs(ap2 + k);
-          ra[c] = rv.x - alpha * av.x;
-          rb[c] = rv.y - alpha * av.y;
-          __stcs(r2 + k, make_double2(ra[c], rb[c]));
-        }
-#pragma unroll
-        for (int tt = 0; tt < 6; ++tt) {
-          const double2 m = __ldcs(mi2 + (6 * h + tt) * h2 + t);
-          ma[tt] = m.x;
-          mb[tt] = m.y;
-        }
-        symv3(ma, ra, za);
-        symv3(mb, rb, zb);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          zsh[(v * 6 + 3 * h + c) * kThreads + threadIdx.x] = make_double2(za[c], zb[c]);
-          acc_rr += ra[c] * ra[c];
-          acc_rz += ra[c] * za[c];
-        }
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          acc_rr += rb[c] * rb[c];
-          acc_rz += rb[c] * zb[c];
-        }
-      }
-    }
-    double s = block_sum<kThreads>(acc_rr, sh);
-    if (threadIdx.x == 0) *red_slot(S.red, RC_RR, vb) = s;
-    s = block_sum<kThreads>(acc_rz, sh);
-    if (threadIdx.x == 0) *red_slot(S.red, RC_RZ, vb) = s;
-  }
-  grid_barrier(S.counter + CNT_BAR_COUNT, S.counter + CNT_BAR_GEN);
-  // every block: the scalars k_pcg_update's last block would compute
-  __shared__ double scal[2];
-  {
-    const double rr = sum_partials<kThreads>(S.red, RC_RR, kRedBlocks, sh);
-    const double rz_new = sum_partials<kThreads>(S.red, RC_RZ, kRedBlocks, sh);
-    if (threadIdx.x == 0) {
-      scal[0] = rr;
-      scal[1] = rz_new;
-    }
-    __syncthreads();
-  }
-  const double rr = scal[0], rz_new = scal[1];
-  const double kk = k_old + 1.0;
-  const double rel = sqrt(rr) / bnorm;
-  const bool converged = rel <= tol;
-  const double beta = rz_new / rz_old;
-  const bool running = !converged && !(kk >= maxit);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    pcg[BDEM_PCG_K] = kk;
-    pcg[BDEM_PCG_RR] = rr;
-    pcg[BDEM_PCG_REL] = rel;
-    if (converged) {
-      pcg[BDEM_PCG_STATE] = PCG_CONVERGED;
-    } else {
-      pcg[BDEM_PCG_BETA] = beta;
-      pcg[BDEM_PCG_RZ] = rz_new;
-      if (kk >= maxit) pcg[BDEM_PCG_STATE] = PCG_MAXIT;
-    }
-  }
-  // phase 2: x += alpha p; p = z + beta p (while running)
-  double2 *x2 = reinterpret_cast<double2 *>(x);
-  double2 *p2 = reinterpret_cast<double2 *>(p);
-#pragma unroll
-  for (int v = 0; v < kFusedMaxV; ++v) {
-    const int vb = blockIdx.x + v * gridDim.x;
-    if (vb >= kRedBlocks) break;
-    const int64_t t = (int64_t)vb * kThreads + threadIdx.x;
-    if (t >= h2) continue;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (h >= halves) break;
-      double2 pv[3], xv[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        pv[c] = p2[(3 * h + c) * h2 + t];
-        xv[c] = __ldcs(x2 + (3 * h + c) * h2 + t);
-      }
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int64_t k = (3 * h + c) * h2 + t;
-        __stcs(x2 + k, make_double2(xv[c].x + alpha * pv[c].x, xv[c].y + alpha * pv[c].y));
-        if (running) {
-          const double2 zz = zsh[(v * 6 + 3 * h + c) * kThreads + threadIdx.x];
-          p2[k] = make_double2(zz.x + beta * pv[c].x, zz.y + beta * pv[c].y);
-        }
-      }
-    }
-  }
-}
-
 // x = 0, r = sign b, z = M^-1 r, p = z, r.z, |b| (linalg.py:52-68)
 __global__ void __launch_bounds__(kThreads) k_pcg_init(bdem_system_t S, const double *b,
                                                        double sign, double *x, double *r,
@@ -887,12 +719,6 @@ static unsigned int spmv_grid() {
   return g;
 }
 
-// Resident grid of k_pcg_update_fused, or 0 when the fused path is off
-// (default: on the 600K plate it measures the same per-PCG-iteration time as
-// the two PDL-chained kernels, 200.7 vs 199.4 us, profiles/r01/README.md),
-// there are not enough co-resident blocks for the virtual layout, or more
-// slot pairs than virtual threads.
-static constexpr size_t kFusedSmem = sizeof(double2) * kFusedMaxV * 6 * kThreads;
 static int g_rot_skip = -1;
 static int rot_skip_on() {
   if (g_rot_skip < 0) {
@@ -900,57 +726,6 @@ static int rot_skip_on() {
     g_rot_skip = env ? (atoi(env) != 0) : 0;
   }
   return g_rot_skip;
-}
-static int g_fused_on = -1;
-static int fused_on() {
-  if (g_fused_on < 0) {
-    const char *env = getenv("BDEM_FUSED_UPD");
-    g_fused_on = env ? (atoi(env) != 0) : 0;
-  }
-  return g_fused_on;
-}
-static unsigned int upd_fused_grid(const bdem_system_t &S) {
-  static int g = -1;
-  if (!fused_on()) return 0;
-  if (g < 0) {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_pcg_update_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kFusedSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg_update_fused, kThreads,
-                                                  kFusedSmem);
-    const long long want = (long long)(kRedBlocks + kFusedMaxV - 1) / kFusedMaxV;
-    g = ((long long)sms * occ >= want) ? (int)want : 0;
-    cudaGetLastError();
-  }
-  if (g == 0 || (S.vstride >> 1) > (int64_t)kRedBlocks * kThreads) return 0;
-  return (unsigned int)g;
-}
-
-static void launch_update_fused(unsigned int grid, cudaStream_t st, bool pdl,
-                                const bdem_system_t &S, double *x, double *r, const double *ap,
-                                double *p) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kFusedSmem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  int na = 0;
-  // co-residency is required by the grid barrier: a cooperative launch
-  // fails instead of hanging if the grid cannot be resident
-  attr[na].id = cudaLaunchAttributeCooperative;
-  attr[na].val.cooperative = 1;
-  ++na;
-  if (pdl) {
-    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[na].val.programmaticStreamSerializationAllowed = 1;
-    ++na;
-  }
-  cfg.attrs = attr;
-  cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, k_pcg_update_fused, S, x, r, ap, p);
 }
 
 // one SpMV launch (plain or PCG mode)
@@ -986,12 +761,6 @@ int bdem_pcg_set_rot_skip(int on) {
   if (on == 0 || on == 1) g_rot_skip = on;
   return prev;
 }
-int bdem_pcg_set_fused(int on) {
-  const int prev = fused_on();
-  if (on == 0 || on == 1) g_fused_on = on;
-  return prev;
-}
-
 
 int bdem_spmv(const bdem_system_t *sys, const double *x, double *y, void *stream) {
   if (!sys) return BDEM_ERR_ARG;
@@ -1023,17 +792,6 @@ int bdem_pcg_iterate(const bdem_system_t *sys, double *x, double *r, double *zv,
   // programmatic dependent launch chain SpMV -> update -> p update
   auto spmv_k = k_spmv;
   const bool pdl = pdl_enabled();
-  const unsigned int fg = upd_fused_grid(*sys);
-  if (fg > 0) {
-    for (int it = 0; it < n_iter; ++it) {
-      if (pdl)
-        launch_pdl(spmv_k, spmv_grid(), kSpmvThreads, st, *sys, (const double *)pv, ap, 1);
-      else
-        launch_spmv(*sys, pv, ap, 1, st);
-      launch_update_fused(fg, st, pdl, *sys, x, r, (const double *)ap, pv);
-    }
-    return launch_status(2 * (int64_t)n_iter);
-  }
   for (int it = 0; it < n_iter; ++it) {
     if (pdl) {
       launch_pdl(spmv_k, spmv_grid(), kSpmvThreads, st, *sys, (const double *)pv, ap, 1);

@@ -11,7 +11,8 @@ Memory layout (HBM):
             p_prev, q_prev, p_hat, q_hat, mass, radius, m/dt^2, mq/dt^2
   bonds     i, j (int32), status (int8), 24 geometry planes, 5 state planes
             (structure-of-arrays, one plane = n_bond doubles)
-  staging   39 planes x n_bond written by the fused bond kernel
+  staging   17 planes x n_bond (j-end pieces) + 14 AoSoA coupling coefficients
+            per bond + 20 row partial-sum planes, written by the bond pass
   reduced   z, y, r, zv, pv, Ap (6 doubles per free element), diag and
             block-Jacobi inverses (12 doubles per free element)
 """
