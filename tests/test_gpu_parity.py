@@ -720,3 +720,37 @@ def test_rot_skip_with_fracture(cuda_ok):
     # half was skipped
     assert sum(len(e) for e in e0) > 0
     assert all(f == 0.0 for f in f0) and all(f == 1.0 for f in f1)
+
+
+def test_assembly_rows_with_mixed_clamp(cuda_ok):
+    """Rows whose first i-role blocks pass the PSD certificate and a later one
+    goes through the eigen-clamp (ikpre > 0): the bond pass folds the PSD
+    prefix into the row sums and stages the rest, the element pass continues
+    the sum.  Identity orientations with every third element turned to a
+    random orientation give such rows; z, diag and minv must be bit-identical
+    to the run that stages every (i,i) quadrant (ikpre = 0)."""
+    import torch
+    from paper_2308_10459_b200 import _lib as L
+    from paper_2308_10459_b200 import configs as C
+    spec = C.cube(n_side=5, random_q=False, seed=5)
+    rng = np.random.default_rng(5)
+    q = spec.elements.q
+    turned = np.arange(0, q.shape[0], 3)
+    r = rng.normal(size=(turned.size, 4))
+    q[turned] = r / np.linalg.norm(r, axis=1, keepdims=True)
+    dev = _assembled(spec)
+    from paper_2308_10459_b200.newton import GPUProblem
+    prob = GPUProblem(dev)
+    f0, g0, _, _ = prob.assemble(dev.xp, dev.xq)
+    kpre = dev.ikpre[:dev.n].cpu().numpy()
+    assert int(dev.counter[5]) > 0
+    assert (kpre > 0).sum() > 0 and (kpre < 0).sum() > 0, np.bincount(kpre + 1)
+    ref = [t.clone() for t in (dev.z, dev.diag, dev.minv)]
+    dev.sys.asm_flags = L.ASM_STAGE_ALL_A
+    try:
+        f1, g1, _, _ = prob.assemble(dev.xp, dev.xq)
+    finally:
+        dev.sys.asm_flags = 0
+    assert (f0, g0) == (f1, g1)
+    for a, b_ in zip(ref, (dev.z, dev.diag, dev.minv)):
+        assert torch.equal(a, b_)
