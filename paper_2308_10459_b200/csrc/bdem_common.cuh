@@ -16,25 +16,13 @@ constexpr int kThreads = 256;
 // inside it, coefficient k of lane l sits at 64 (k >> 1) + 2 l + (k & 1)
 // (pairs of coefficients interleaved per lane), so a lane reads its 14
 // values as 7 aligned 16-byte loads and a warp's load of one pair is a
-// contiguous 512-byte segment.  BDEM_CF_PAIRED=0 selects the plain
-// plane-per-coefficient record (32 k + l).
-#ifndef BDEM_CF_PAIRED
-#define BDEM_CF_PAIRED 1
-#endif
+// contiguous 512-byte segment.
 // offset of coefficient k from the lane's base cf_idx(pos, 0)
 __host__ __device__ __forceinline__ constexpr int cf_rel(int k) {
-#if BDEM_CF_PAIRED
   return 64 * (k >> 1) + (k & 1);
-#else
-  return 32 * k;
-#endif
 }
 __host__ __device__ __forceinline__ int64_t cf_idx(int64_t pos, int k) {
-#if BDEM_CF_PAIRED
   return (pos & ~int64_t(31)) * BDEM_CF_COUNT + 2 * (pos & 31) + cf_rel(k);
-#else
-  return (pos & ~int64_t(31)) * BDEM_CF_COUNT + (pos & 31) + cf_rel(k);
-#endif
 }
 
 // the 14 coupling coefficients of one position
@@ -44,7 +32,6 @@ struct Coef {
 template <bool kGlobal>
 __device__ __forceinline__ Coef load_coef(const double *base) {
   Coef c;
-#if BDEM_CF_PAIRED
   double v[BDEM_CF_COUNT];
   const double2 *b2 = reinterpret_cast<const double2 *>(base);
 #pragma unroll
@@ -59,14 +46,6 @@ __device__ __forceinline__ Coef load_coef(const double *base) {
   c.be = v[BDEM_CF_BETA];
 #pragma unroll
   for (int t = 0; t < 9; ++t) c.C[t] = v[BDEM_CF_C + t];
-#else
-#pragma unroll
-  for (int t = 0; t < 3; ++t) c.n[t] = kGlobal ? __ldg(base + cf_rel(BDEM_CF_N + t)) : base[cf_rel(BDEM_CF_N + t)];
-  c.al = kGlobal ? __ldg(base + cf_rel(BDEM_CF_ALPHA)) : base[cf_rel(BDEM_CF_ALPHA)];
-  c.be = kGlobal ? __ldg(base + cf_rel(BDEM_CF_BETA)) : base[cf_rel(BDEM_CF_BETA)];
-#pragma unroll
-  for (int t = 0; t < 9; ++t) c.C[t] = kGlobal ? __ldg(base + cf_rel(BDEM_CF_C + t)) : base[cf_rel(BDEM_CF_C + t)];
-#endif
   return c;
 }
 __device__ __forceinline__ void store_coef(double *base, const double v[BDEM_CF_COUNT]) {

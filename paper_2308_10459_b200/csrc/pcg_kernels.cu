@@ -63,26 +63,19 @@ enum { CNT_SPMV = 2, CNT_UPDATE = 3, CNT_INIT = 4 };
 enum { RC_PAP = 20, RC_AP2 = 21, RC_PP2 = 22, RC_RR = 23, RC_RZ = 24, RC_IRR = 25, RC_IRZ = 26,
        RC_IRN = 27 };
 
-// BDEM_SPMV_KEEP: the SpMV's gathers of x (each row's block is gathered by
+// The SpMV's gathers of x (each row's block is gathered by
 // ~12 bonds) carry an L2 evict-last cache policy, so the streamed
 // coefficients evict them last (1% per PCG iteration; the same hint on the
 // slot indices and diagonal blocks measured 1% slower)
-#ifndef BDEM_SPMV_KEEP
-#define BDEM_SPMV_KEEP 1
-#endif
 __device__ __forceinline__ uint64_t l2_evict_last_policy() {
   uint64_t pol;
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
 __device__ __forceinline__ double ld_keep(const double *a) {
-#if BDEM_SPMV_KEEP
   double v;
   asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(l2_evict_last_policy()));
   return v;
-#else
-  return __ldg(a);
-#endif
 }
 
 // reduced vectors are 6 planes of stride vstride: component c of slot s at
@@ -224,9 +217,6 @@ __device__ __forceinline__ void spmv_pcg_epilogue(const bdem_system_t &S, double
 #ifndef BDEM_SPMV_WARPS
 #define BDEM_SPMV_WARPS 4
 #endif
-#ifndef BDEM_SPMV_BLOCKED
-#define BDEM_SPMV_BLOCKED 0
-#endif
 #ifndef BDEM_SPMV_MINB
 #define BDEM_SPMV_MINB 8
 #endif
@@ -266,18 +256,12 @@ __device__ __forceinline__ void slot_apply(const bdem_system_t &S, const double 
     double xo[3], n[3];
 #pragma unroll
     for (int t = 0; t < 3; ++t) xo[t] = __ldg(x + t * S.vstride + r.o);
-#if BDEM_CF_PAIRED
     // n0 n1 | n2 alpha | beta (C0): three 16-byte loads
     const double2 *b2 = reinterpret_cast<const double2 *>(base);
     const double2 c01 = __ldg(b2), c23 = __ldg(b2 + 32), c45 = __ldg(b2 + 64);
     n[0] = c01.x; n[1] = c01.y; n[2] = c23.x;
     const double al = c23.y, be = c45.x;
     static_assert(BDEM_CF_N == 0 && BDEM_CF_ALPHA == 3 && BDEM_CF_BETA == 4, "pair layout");
-#else
-#pragma unroll
-    for (int t = 0; t < 3; ++t) n[t] = __ldg(base + cf_rel(BDEM_CF_N + t));
-    const double al = __ldg(base + cf_rel(BDEM_CF_ALPHA)), be = __ldg(base + cf_rel(BDEM_CF_BETA));
-#endif
     const double nx = al * ((n[0] * xo[0] + n[1] * xo[1]) + n[2] * xo[2]);
 #pragma unroll
     for (int c = 0; c < 3; ++c) acc[c] -= nx * n[c] + be * xo[c];
@@ -347,16 +331,7 @@ __device__ __forceinline__ void spmv_slices(const bdem_system_t &S, const double
                                             double &acc_xy, double &acc_yy, double &acc_xx) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ns = (int)((S.n_elem + 31) >> 5);
-#if BDEM_SPMV_BLOCKED
-  // contiguous slice ranges per CTA: neighbouring rows (and their x blocks)
-  // are processed by the same SM, so gathers reuse L1/L2 lines
-  const int per = (ns + gridDim.x - 1) / gridDim.x;
-  const int s_begin = blockIdx.x * per;
-  const int s_end = min(ns, s_begin + per);
-  const int step = 1;
-#else
   const int s_begin = blockIdx.x, s_end = ns, step = gridDim.x;
-#endif
   int buf = 0;
 #pragma unroll 1
   for (int sl = s_begin; sl < s_end; sl += step, buf ^= 1) {
@@ -429,9 +404,6 @@ __global__ void __launch_bounds__(kSpmvThreads, BDEM_SPMV_MINB) k_spmv(bdem_syst
 #ifndef BDEM_UPD_MINB
 #define BDEM_UPD_MINB 4
 #endif
-#ifndef BDEM_UPD_STREAM
-#define BDEM_UPD_STREAM 1
-#endif
 __global__ void __launch_bounds__(kThreads, BDEM_UPD_MINB) k_pcg_update(bdem_system_t S, double *x, double *r,
                                                          double *zv, const double *p,
                                                          const double *ap) {
@@ -472,7 +444,6 @@ __global__ void __launch_bounds__(kThreads, BDEM_UPD_MINB) k_pcg_update(bdem_sys
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const int64_t k = (3 * h + c) * h2 + t;
-#if BDEM_UPD_STREAM
         // x, r, Ap and M^-1 are next touched an SpMV later (0.5 GB of
         // coefficients streamed in between): evict-first loads / stores keep
         // them from displacing the SpMV's L2 working set
@@ -481,21 +452,10 @@ __global__ void __launch_bounds__(kThreads, BDEM_UPD_MINB) k_pcg_update(bdem_sys
         ra[c] = rv.x - alpha * av.x;
         rb[c] = rv.y - alpha * av.y;
         __stcs(r2 + k, make_double2(ra[c], rb[c]));
-#else
-        const double2 xv = x2[k], rv = r2[k], pv = p2[k], av = ap2[k];
-        x2[k] = make_double2(xv.x + alpha * pv.x, xv.y + alpha * pv.y);
-        ra[c] = rv.x - alpha * av.x;
-        rb[c] = rv.y - alpha * av.y;
-        r2[k] = make_double2(ra[c], rb[c]);
-#endif
       }
 #pragma unroll
       for (int tt = 0; tt < 6; ++tt) {
-#if BDEM_UPD_STREAM
         const double2 m = __ldcs(mi2 + (6 * h + tt) * h2 + t);
-#else
-        const double2 m = mi2[(6 * h + tt) * h2 + t];
-#endif
         ma[tt] = m.x;
         mb[tt] = m.y;
       }
@@ -564,11 +524,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(bdem_system_t S, doubl
   const double2 *z2 = reinterpret_cast<const double2 *>(zv);
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n6;
        k += (int64_t)gridDim.x * blockDim.x) {
-#if BDEM_UPD_STREAM
     const double2 zz = __ldcs(z2 + k), pp = p2[k];   // last use of z this iteration
-#else
-    const double2 zz = z2[k], pp = p2[k];
-#endif
     p2[k] = make_double2(zz.x + beta * pp.x, zz.y + beta * pp.y);
   }
   TL_EXIT(2, tl_it)
