@@ -684,10 +684,32 @@ static int rot_skip_on() {
   return g_rot_skip;
 }
 
+// Problem-sized grids.  Every PCG kernel strides its grid over work items
+// (slices, slot pairs, rows) and sums per-block partials over gridDim.x.
+// When a system has fewer items than the full grid has threads (slices) --
+// small and mid-size systems -- each busy thread (CTA) already handles a
+// single item, and the surplus blocks only add +0.0 partials; launching
+// just the busy blocks gives the same partials in the same order
+// (bit-identical scalars) without the idle CTAs' launch, barrier and
+// last-block costs.
+static unsigned int fit_grid(int64_t items, int64_t per_block, unsigned int cap) {
+  const int64_t g = (items + per_block - 1) / per_block;
+  return g < 1 ? 1u : (g < (int64_t)cap ? (unsigned int)g : cap);
+}
+static unsigned int spmv_fit(const bdem_system_t &S) {
+  return fit_grid((S.n_elem + 31) >> 5, 1, spmv_grid());
+}
+static unsigned int update_fit(const bdem_system_t &S) {
+  return fit_grid(S.vstride >> 1, kThreads, kRedBlocks);    // slot pairs
+}
+static unsigned int pupdate_fit(const bdem_system_t &S) {
+  return fit_grid(3 * S.vstride, kThreads, kRedBlocks);     // double2 units, 6 planes
+}
+
 // one SpMV launch (plain or PCG mode)
 static void launch_spmv(const bdem_system_t &S, const double *x, double *y, int mode,
                         cudaStream_t st) {
-  k_spmv<<<spmv_grid(), kSpmvThreads, 0, st>>>(S, x, y, mode);
+  k_spmv<<<spmv_fit(S), kSpmvThreads, 0, st>>>(S, x, y, mode);
 }
 
 }  // namespace bdem
@@ -735,9 +757,8 @@ int bdem_pcg_init(const bdem_system_t *sys, const double *b, double sign, double
                   double *zv, double *pv, double tol, int max_iter, double boost,
                   void *stream) {
   if (!sys) return BDEM_ERR_ARG;
-  k_pcg_init<<<kRedBlocks, kThreads, 0, as_stream(stream)>>>(*sys, b, sign, x, r, zv, pv, tol,
-                                                              (double)max_iter, boost,
-                                                              rot_skip_on());
+  k_pcg_init<<<fit_grid(sys->n_free, kThreads, kRedBlocks), kThreads, 0, as_stream(stream)>>>(
+      *sys, b, sign, x, r, zv, pv, tol, (double)max_iter, boost, rot_skip_on());
   return launch_status();
 }
 
@@ -750,14 +771,14 @@ int bdem_pcg_iterate(const bdem_system_t *sys, double *x, double *r, double *zv,
   const bool pdl = pdl_enabled();
   for (int it = 0; it < n_iter; ++it) {
     if (pdl) {
-      launch_pdl(spmv_k, spmv_grid(), kSpmvThreads, st, *sys, (const double *)pv, ap, 1);
-      launch_pdl(k_pcg_update, kRedBlocks, kThreads, st, *sys, x, r, zv, (const double *)pv,
-                 (const double *)ap);
-      launch_pdl(k_pcg_pupdate, kRedBlocks, kThreads, st, *sys, pv, (const double *)zv);
+      launch_pdl(spmv_k, spmv_fit(*sys), kSpmvThreads, st, *sys, (const double *)pv, ap, 1);
+      launch_pdl(k_pcg_update, update_fit(*sys), kThreads, st, *sys, x, r, zv,
+                 (const double *)pv, (const double *)ap);
+      launch_pdl(k_pcg_pupdate, pupdate_fit(*sys), kThreads, st, *sys, pv, (const double *)zv);
     } else {
       launch_spmv(*sys, pv, ap, 1, st);
-      k_pcg_update<<<kRedBlocks, kThreads, 0, st>>>(*sys, x, r, zv, pv, ap);
-      k_pcg_pupdate<<<kRedBlocks, kThreads, 0, st>>>(*sys, pv, zv);
+      k_pcg_update<<<update_fit(*sys), kThreads, 0, st>>>(*sys, x, r, zv, pv, ap);
+      k_pcg_pupdate<<<pupdate_fit(*sys), kThreads, 0, st>>>(*sys, pv, zv);
     }
   }
   return launch_status(3 * (int64_t)n_iter);
@@ -773,8 +794,8 @@ int bdem_pcg_update(const bdem_system_t *sys, double *x, double *r, double *zv, 
                     const double *ap, void *stream) {
   if (!sys) return BDEM_ERR_ARG;
   cudaStream_t st = as_stream(stream);
-  k_pcg_update<<<kRedBlocks, kThreads, 0, st>>>(*sys, x, r, zv, pv, ap);
-  k_pcg_pupdate<<<kRedBlocks, kThreads, 0, st>>>(*sys, pv, zv);
+  k_pcg_update<<<update_fit(*sys), kThreads, 0, st>>>(*sys, x, r, zv, pv, ap);
+  k_pcg_pupdate<<<pupdate_fit(*sys), kThreads, 0, st>>>(*sys, pv, zv);
   return launch_status(2);
 }
 

@@ -6,9 +6,6 @@ import torch
 from paper_2308_10459_b200 import SolverConfig, configs as C, stable_step
 from paper_2308_10459_b200.scene import Scene
 res = {}
-MODE = int(os.environ.get("GRAPH", "-1"))
-from paper_2308_10459_b200 import _lib as L
-L.load().bdem_pcg_set_graph(MODE)
 for name, spec, eps in (("rope100k", C.rope(), 1e-5), ("cube22", C.cube(random_q=False), 1e-6)):
     scene = Scene.from_spec(spec, host_sync=False)
     cfg = SolverConfig(epsilon=eps, max_iterations=300)
