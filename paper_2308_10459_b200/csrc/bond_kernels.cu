@@ -274,9 +274,7 @@ __global__ void __launch_bounds__(BDEM_ASM_THREADS, BDEM_ASM_MINB) k_bond_rows(b
     // PSD blocks (all of them at identity orientations) are final; an
     // indefinite one is queued for the register-resident eigen-clamp pass
     // (k_bond_clamp), which overwrites its staged quadrants and coefficients
-    double mx = 0.0;
-#pragma unroll
-    for (int u = 0; u < 21; ++u) mx = fmax(mx, fabs(S6[u]));
+    const double mx = max_abs21(S6);
     if (mx != 0.0 && !psd6_regs(S6, 4e-14 * mx)) {
       const unsigned int slot = atomicAdd(S.counter + kClampCounter, 1u);
       S.clamp_list[slot] = (int32_t)b;
