@@ -196,12 +196,24 @@ __global__ void __launch_bounds__(kThreads, BDEM_ELEM_MINB) k_element_assemble(b
       double *mi = S.minv + s;
 #pragma unroll
       for (int t = 0; t < 6; ++t) { dg[t * nf] = P[t]; dg[(6 + t) * nf] = R[t]; }
-      // block-Jacobi (linalg.py:100-121): singular -> identity
-      double lp, ap_, lr, ar;
-      eig3_minmax(P, lp, ap_);
-      eig3_minmax(R, lr, ar);
-      const double scale = fmax(fmax(ap_, ar), 1e-300);
-      if (fmin(lp, lr) <= 1e-12 * scale) {
+      // block-Jacobi (linalg.py:100-121): singular -> identity.  The
+      // eigenvalue test lambda_min <= 1e-12 max|lambda| is decided by a cheap
+      // certificate when it can be (pd_certify3: both blocks positive
+      // definite with lambda_min >= det / |S|_F^2 far above the threshold),
+      // else by the eigenvalues themselves; same decision either way
+      bool singular;
+      double fp_, lbp, fr_, lbr;
+      const bool okp = pd_certify3(P, fp_, lbp), okr = pd_certify3(R, fr_, lbr);
+      if (okp && okr && fmin(lbp, lbr) > 2e-12 * sqrt(fmax(fp_, fr_))) {
+        singular = false;
+      } else {
+        double lp, ap_, lr, ar;
+        eig3_minmax(P, lp, ap_);
+        eig3_minmax(R, lr, ar);
+        const double scale = fmax(fmax(ap_, ar), 1e-300);
+        singular = fmin(lp, lr) <= 1e-12 * scale;
+      }
+      if (singular) {
         const double I6[6] = {1, 0, 0, 1, 0, 1};
 #pragma unroll
         for (int t = 0; t < 6; ++t) { mi[t * nf] = I6[t]; mi[(6 + t) * nf] = I6[t]; }
