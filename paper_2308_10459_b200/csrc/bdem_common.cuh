@@ -48,9 +48,14 @@ __device__ __forceinline__ Coef load_coef(const double *base) {
   for (int t = 0; t < 9; ++t) c.C[t] = v[BDEM_CF_C + t];
   return c;
 }
+// coefficients 2j and 2j + 1 of one position as one 16-byte store (a warp's
+// store of a pair is one contiguous 512-byte segment)
+__device__ __forceinline__ void store_coef_pair(double *base, int j, double a, double b) {
+  *reinterpret_cast<double2 *>(base + cf_rel(2 * j)) = make_double2(a, b);
+}
 __device__ __forceinline__ void store_coef(double *base, const double v[BDEM_CF_COUNT]) {
 #pragma unroll
-  for (int k = 0; k < BDEM_CF_COUNT; ++k) base[cf_rel(k)] = v[k];
+  for (int j = 0; j < BDEM_CF_COUNT / 2; ++j) store_coef_pair(base, j, v[2 * j], v[2 * j + 1]);
 }
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }

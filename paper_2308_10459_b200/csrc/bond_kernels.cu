@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(BDEM_ASM_THREADS, BDEM_ASM_MINB) k_bond_rows(b
 
     // stretch: energy, gradient (kc n) and the closed-form clamp of
     // [[a,-a],[-a,a]]: a+ = k (nn + max(c/l,0) (I - nn)) = alpha nn + beta I
-    double e_s;
+    double e_s, beta_cf;
     {
       const double ks = scale * GEO(BDEM_BG_KN);
       const Stretch st = stretch_eval(pi, pj, GEO(BDEM_BG_L0), ks);
@@ -221,10 +221,11 @@ __global__ void __launch_bounds__(BDEM_ASM_THREADS, BDEM_ASM_MINB) k_bond_rows(b
       const double alpha = ks - beta;
       e_s = st.E;
       st_out[BDEM_ST_KC * nb + b] = st.kc;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) cf[cf_rel(BDEM_CF_N + c)] = st.n[c];
-      cf[cf_rel(BDEM_CF_ALPHA)] = alpha;
-      cf[cf_rel(BDEM_CF_BETA)] = beta;
+      static_assert(BDEM_CF_N == 0 && BDEM_CF_ALPHA == 3 && BDEM_CF_BETA == 4 && BDEM_CF_C == 5,
+                    "coefficient pairs: (n0 n1) (n2 alpha) (beta C00) (C01 C02) ...");
+      store_coef_pair(cf, 0, st.n[0], st.n[1]);
+      store_coef_pair(cf, 1, st.n[2], alpha);
+      beta_cf = beta;   // shares its pair with C00
       double apos[6], gpc[3];
       stretch_apos(alpha, beta, st.n, apos);
 #pragma unroll
@@ -263,10 +264,11 @@ __global__ void __launch_bounds__(BDEM_ASM_THREADS, BDEM_ASM_MINB) k_bond_rows(b
       rot_block(qi, qj, d0, F, kds, sh, ro.rs, ro.rv, ro.w, S6);
     }
 #undef GEO
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) cf[cf_rel(BDEM_CF_C + 3 * r + c)] = S6[sidx<6>(r, c + 3)];
+    store_coef_pair(cf, 2, beta_cf, S6[sidx<6>(0, 3)]);
+    store_coef_pair(cf, 3, S6[sidx<6>(0, 4)], S6[sidx<6>(0, 5)]);
+    store_coef_pair(cf, 4, S6[sidx<6>(1, 3)], S6[sidx<6>(1, 4)]);
+    store_coef_pair(cf, 5, S6[sidx<6>(1, 5)], S6[sidx<6>(2, 3)]);
+    store_coef_pair(cf, 6, S6[sidx<6>(2, 4)], S6[sidx<6>(2, 5)]);
     const int pr[6] = {0, 0, 0, 1, 1, 2}, pc[6] = {0, 1, 2, 1, 2, 2};
 #pragma unroll
     for (int u = 0; u < 6; ++u) st_out[(BDEM_ST_D + u) * nb + b] = S6[sidx<6>(pr[u] + 3, pc[u] + 3)];
