@@ -33,10 +33,11 @@ __device__ __forceinline__ void store_q(double *q, int64_t e, const double qe[4]
 // clamped block a+ = alpha n n^T + beta I (sym6)
 __device__ __forceinline__ double stage_stretch(const double *st, const double *cf, int64_t nb,
                                                 int64_t b, double n[3], double a[6]) {
-  const double *cb = cf + cf_idx(b, 0);
-#pragma unroll
-  for (int c = 0; c < 3; ++c) n[c] = cb[cf_rel(BDEM_CF_N + c)];
-  stretch_apos(cb[cf_rel(BDEM_CF_ALPHA)], cb[cf_rel(BDEM_CF_BETA)], n, a);
+  // pairs (n0 n1) (n2 alpha) (beta C00): three 16-byte loads
+  const double2 *cb = reinterpret_cast<const double2 *>(cf + cf_idx(b, 0));
+  const double2 c01 = cb[0], c23 = cb[32], c45 = cb[64];
+  n[0] = c01.x; n[1] = c01.y; n[2] = c23.x;
+  stretch_apos(c23.y, c45.x, n, a);
   return st[BDEM_ST_KC * nb + b];
 }
 
