@@ -115,6 +115,28 @@ def gold_bond_terms():
     save("bond_terms.npz", **out)
 
 
+def gold_block_sample():
+    """BASELINE configs[4] (C5: 126^3 jittered block, random unit q, ~12M
+    bonds) is too large for a reference step, so its bonds are checked the
+    way SURVEY 8(d) asks: the reference's BondSet.energy_terms
+    (bonds.py:473-504) on a seeded sample of the block's own bonds, at the
+    generator's state (the step-1 predictor with zero velocities)."""
+    spec = C.block(random_q=True)
+    b = spec.bonds
+    rng = np.random.default_rng(5)
+    pick = np.sort(rng.choice(b.n, 1000, replace=False))
+    sub = rb.BondSet(**{**{f: np.array(getattr(b, f))[pick] for f in BOND_FIELDS},
+                        "face_i": np.zeros(pick.size, dtype=np.int64),
+                        "face_j": np.zeros(pick.size, dtype=np.int64)})
+    el = spec.elements
+    idx, e, gpi, gpj, gqi, gqj, hpp, hqq = sub.energy_terms(el.p, el.q, want_hess=True)
+    # the elements the sample touches (p, q rows), so the fixture is checkable
+    # without regenerating the block
+    rows = np.unique(np.r_[sub.i, sub.j])
+    save("block_sample.npz", pick=pick, n=el.n, n_bonds=b.n, rows=rows, p_rows=el.p[rows],
+         q_rows=el.q[rows], idx=idx, E=e, gpi=gpi, gpj=gpj, gqi=gqi, gqj=gqj, hpp=hpp, hqq=hqq)
+
+
 def _small_problem(seed=21, random_q=False, qspread=0.05):
     spec = C.cube(n_side=4, r=0.002, seed=seed, random_q=random_q, youngs=3e8,
                   k_contact=1e8)

@@ -152,3 +152,35 @@ def test_cube22_identity_q_vs_reference(cuda_ok):
     np.testing.assert_array_equal(b.status, g["final_b_status"])
     for k in ("stiffness_scale", "damage", "plastic_strain"):
         _assert_close(getattr(b, k), g[f"final_b_{k}"], 1e-8, 1e-12, k)
+
+
+def test_block_2m_bond_sample_vs_reference(cuda_ok):
+    """BASELINE configs[4] at full size (C5: 126^3 jittered block, random unit
+    q, 11.86M bonds): the B200 bond kernel against the reference's own
+    BondSet.energy_terms on 1,000 of the block's bonds (``block_sample.npz``,
+    made by the reference at the generator's state): energies, gradients and
+    ambient Hessians at rtol 1e-10 plus atol 1e-12 x the bond's stiffness."""
+    from paper_2308_10459_b200 import configs as C
+    from paper_2308_10459_b200.state import BondSet
+    g = load("block_sample.npz")
+    spec = C.block(random_q=True)
+    el, b = spec.elements, spec.bonds
+    assert el.n == int(g["n"]) and b.n == int(g["n_bonds"])
+    rows = g["rows"]
+    np.testing.assert_array_equal(el.p[rows], g["p_rows"])   # same generator state
+    np.testing.assert_array_equal(el.q[rows], g["q_rows"])
+    pick = g["pick"]
+    sub = BondSet(**{f: np.asarray(getattr(b, f))[pick] for f in b.__dataclass_fields__})
+    got = sub.energy_terms(el.p, el.q, want_hess=True)
+    np.testing.assert_array_equal(got[0], g["idx"])
+    sc = sub.stiffness_scale
+    kn = sc * sub.kn
+    krot = sc * (sub.kt + sub.k_diag.sum(axis=1))
+    l0 = sub.rest_length
+    for name, got_, scale in zip(("E", "gpi", "gpj", "gqi", "gqj", "hpp", "hqq"), got[1:],
+                                 (kn * l0**2 + krot, kn * l0 + krot, kn * l0 + krot, krot, krot,
+                                  kn + krot, kn + krot)):
+        want = g[name]
+        atol = 1e-12 * scale.reshape((-1,) + (1,) * (want.ndim - 1))
+        err = np.abs(got_ - want) - (1e-10 * np.abs(want) + atol)
+        assert err.max() <= 0, f"{name}: worst excess {err.max():.3e}"
