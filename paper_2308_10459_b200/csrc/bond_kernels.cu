@@ -152,6 +152,22 @@ __global__ void __launch_bounds__(128) k_bond_ambient(bdem_system_t S, const dou
 #define BDEM_ASM_THREADS 64
 #endif
 #define ACC_T volatile double
+// 1: the next slot's operand lines are prefetched into L2 while the current
+// slot computes (387 -> 368 us on the plate).  Two slots ahead, only the
+// early operands, one lane per line, and prefetches paired with the loads
+// were all measured slower or equal (profiles/r02/README.md, session 4).
+#ifndef BDEM_ASM_PF
+#define BDEM_ASM_PF 1
+#endif
+// row blocks in descending order: the rows the element pass (ascending)
+// starts with are the ones this pass wrote last, still in L2 (bond + element
+// 505.8 -> 500.0 us)
+#ifndef BDEM_ASM_REVERSE
+#define BDEM_ASM_REVERSE 1
+#endif
+__device__ __forceinline__ void prefetch_l2(const void *a) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+}
 
 // row partial sums in shared memory: acc[first + c][t] += v[c] for c < N,
 // all loads issued before the adds and all stores after them (volatile
@@ -177,7 +193,12 @@ __global__ void __launch_bounds__(BDEM_ASM_THREADS, BDEM_ASM_MINB) k_bond_rows(b
   ACC_T(*acc)[BDEM_ASM_THREADS] = acc_sh;
   const int t = threadIdx.x;
   const int64_t nrow = ((S.n_elem + 31) >> 5) << 5;
-  const int64_t row = blockIdx.x * (int64_t)BDEM_ASM_THREADS + t;
+#if BDEM_ASM_REVERSE
+  const unsigned int blk = gridDim.x - 1 - blockIdx.x;
+#else
+  const unsigned int blk = blockIdx.x;
+#endif
+  const int64_t row = blk * (int64_t)BDEM_ASM_THREADS + t;
   if (row >= nrow) return;
 #pragma unroll
   for (int k = 0; k < BDEM_IP_COUNT; ++k) acc[k][t] = 0.0;
@@ -194,6 +215,18 @@ __global__ void __launch_bounds__(BDEM_ASM_THREADS, BDEM_ASM_MINB) k_bond_rows(b
   for (int64_t b = b_beg; b < b_end; b += 32, ++k) {
     double *cf = S.scoef + cf_idx(b, 0);
     const int8_t stat = S.status[b];
+#if BDEM_ASM_PF
+    // the next slot's operands are pulled into L2 while this slot computes
+    // (no registers held): its loads then pay the L2 latency, not DRAM's
+    if (b + 32 < b_end) {
+      const int64_t bn = b + 32;
+      prefetch_l2(S.status + bn);
+      prefetch_l2(S.bond_j + bn);
+      prefetch_l2(S.bstate + BDEM_BS_SCALE * nb + bn);
+#pragma unroll
+      for (int f = 0; f < BDEM_BG_KDIAG + 3; ++f) prefetch_l2(g + f * nb + bn);
+    }
+#endif
 #define GEO(f) g[(f) * nb + b]
     if (stat == 2) {  // broken or padding: no energy, no coupling
 #pragma unroll

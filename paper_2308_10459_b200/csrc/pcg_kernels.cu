@@ -78,6 +78,18 @@ __device__ __forceinline__ double ld_keep(const double *a) {
   return v;
 }
 
+// 1: the slice's diagonal rows (read after the slice barrier) are prefetched
+// into L2 at the top of the slice: 123.2 -> 122.0 us, PCG iteration 176.9 ->
+// 175.8 us.  Prefetching the CTA's next slice (records, index lines: 152-162
+// us, a grid-wide wave ahead overflows what L2 retains) or the warp's next
+// in-slice records (no gain) was measured and dropped (profiles/r02/README.md).
+#ifndef BDEM_SPMV_PF
+#define BDEM_SPMV_PF 1
+#endif
+__device__ __forceinline__ void prefetch_l2(const void *a) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+}
+
 // reduced vectors are 6 planes of stride vstride: component c of slot s at
 // x[c * vstride + s], so a warp touching 32 consecutive slots reads 256 contiguous
 // bytes per component
@@ -342,6 +354,14 @@ __device__ __forceinline__ void spmv_slices(const bdem_system_t &S, const double
     const SliceBounds cb = slice_bounds(S, sl, ns);
     const int s_row = __ldg(S.row_slot + (int64_t)sl * 32 + lane);
     double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#if BDEM_SPMV_PF
+    // this slice's diagonal rows (read after the barrier) into L2 now
+    if (s_row >= 0) {
+#pragma unroll
+      for (int t = 0; t < 12 / kSpmvWarps; ++t)
+        prefetch_l2(S.diag + (int64_t)(w + kSpmvWarps * t) * S.vstride + s_row);
+    }
+#endif
     // software pipeline on the (cheap, integer) slot indices: the next slot's
     // index loads are in flight while this slot's coefficients arrive
     const int kt = cb.ki + cb.kj;

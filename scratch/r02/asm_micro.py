@@ -37,6 +37,15 @@ for tag, pert in (("rest", 0.0), ("pert", float(os.environ.get("PERT", "1e-3")))
     timeit(f"bond_us_{tag}", bond)
     timeit(f"element_us_{tag}", elem)
     timeit(f"both_us_{tag}", lambda: (bond(), elem()))
+    if hasattr(dev.lib, "bdem_assemble_fused") and os.environ.get("NO_FUSED") is None:
+        from paper_2308_10459_b200 import _lib as L
+        fused = lambda: dev.call("bdem_assemble_fused", dev.sysp, dev.xp.data_ptr(), dev.xq.data_ptr(), dev.z.data_ptr(), dev.stream)
+        bond(); elem(); torch.cuda.synchronize()
+        zr, dr, mr = dev.z.clone(), dev.diag.clone(), dev.minv.clone()
+        timeit(f"fused_us_{tag}", fused)
+        torch.cuda.synchronize()
+        res[f"fused_nclamp_{tag}"] = float(dev.scalars[L.SC["NCLAMP"]].item())
+        res[f"fused_identical_{tag}"] = bool(torch.equal(zr, dev.z) and torch.equal(dr, dev.diag) and torch.equal(mr, dev.minv))
     torch.cuda.synchronize()
     res[f"clamp_queue_{tag}"] = int(dev.counter[5].item())
     res[f"z_sum_{tag}"] = float(dev.z.abs().sum())
