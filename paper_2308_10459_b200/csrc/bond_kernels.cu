@@ -162,6 +162,14 @@ __global__ void __launch_bounds__(128) k_bond_ambient(bdem_system_t S, const dou
 // row blocks in descending order: the rows the element pass (ascending)
 // starts with are the ones this pass wrote last, still in L2 (bond + element
 // 505.8 -> 500.0 us)
+// the 18 geometry planes are read once per assembly: evict-first loads keep
+// them from displacing the outputs the element pass is about to read (bond
+// pass 340.0 -> 333.8 us, bond + element 496.6 -> 490.5 us; the same hint on
+// status / j index / scale, or evict-first stores of the C coefficients, did
+// not help)
+#ifndef BDEM_ASM_GEO_CS
+#define BDEM_ASM_GEO_CS 1
+#endif
 #ifndef BDEM_ASM_REVERSE
 #define BDEM_ASM_REVERSE 1
 #endif
@@ -227,7 +235,11 @@ __global__ void __launch_bounds__(BDEM_ASM_THREADS, BDEM_ASM_MINB) k_bond_rows(b
       for (int f = 0; f < BDEM_BG_KDIAG + 3; ++f) prefetch_l2(g + f * nb + bn);
     }
 #endif
+#if BDEM_ASM_GEO_CS
+#define GEO(f) __ldcs(g + (f) * nb + b)
+#else
 #define GEO(f) g[(f) * nb + b]
+#endif
     if (stat == 2) {  // broken or padding: no energy, no coupling
 #pragma unroll
       for (int c = 0; c < BDEM_ST_COUNT; ++c) st_out[c * nb + b] = 0.0;

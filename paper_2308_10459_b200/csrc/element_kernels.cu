@@ -11,6 +11,19 @@
 #include "bdem_math.cuh"
 #include "colliders.cuh"
 
+// the staged pieces and row sums (1) and the j-end coefficient pairs (2) are
+// read once here: evict-first loads keep the bond pass's not-yet-read outputs
+// in L2 longer (bond + element 498.7 -> 496.7 us, then 490.2 -> 485.6 us)
+#ifndef BDEM_ELEM_CS
+#define BDEM_ELEM_CS 2
+#endif
+#if BDEM_ELEM_CS
+#define LDS1(a) __ldcs(a)
+#else
+#define LDS1(a) (*(a))
+#endif
+
+
 namespace bdem {
 
 __device__ __forceinline__ void load_p(const double *p, int64_t e, double pe[3]) {
@@ -35,10 +48,14 @@ __device__ __forceinline__ double stage_stretch(const double *st, const double *
                                                 int64_t b, double n[3], double a[6]) {
   // pairs (n0 n1) (n2 alpha) (beta C00): three 16-byte loads
   const double2 *cb = reinterpret_cast<const double2 *>(cf + cf_idx(b, 0));
+#if BDEM_ELEM_CS >= 2
+  const double2 c01 = __ldcs(cb), c23 = __ldcs(cb + 32), c45 = __ldcs(cb + 64);
+#else
   const double2 c01 = cb[0], c23 = cb[32], c45 = cb[64];
+#endif
   n[0] = c01.x; n[1] = c01.y; n[2] = c23.x;
   stretch_apos(c23.y, c45.x, n, a);
-  return st[BDEM_ST_KC * nb + b];
+  return LDS1(st + BDEM_ST_KC * nb + b);
 }
 
 // ---------------------------------------------------------------------------
@@ -73,15 +90,15 @@ __global__ void __launch_bounds__(kThreads, BDEM_ELEM_MINB) k_element_assemble(b
     if (nb > 0) {
       const double *ip = S.ipart;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) gp[c] = ip[(BDEM_IP_GP + c) * nrow + row];
+      for (int c = 0; c < 3; ++c) gp[c] = LDS1(ip + (BDEM_IP_GP + c) * nrow + row);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) gq[c] = ip[(BDEM_IP_GQ + c) * nrow + row];
+      for (int c = 0; c < 4; ++c) gq[c] = LDS1(ip + (BDEM_IP_GQ + c) * nrow + row);
 #pragma unroll
       for (int t = 0; t < 6; ++t) {
-        P[t] = ip[(BDEM_IP_P + t) * nrow + row];
-        R[t] = ip[(BDEM_IP_R + t) * nrow + row];
+        P[t] = LDS1(ip + (BDEM_IP_P + t) * nrow + row);
+        R[t] = LDS1(ip + (BDEM_IP_R + t) * nrow + row);
       }
-      ebond = ip[BDEM_IP_E * nrow + row];
+      ebond = LDS1(ip + BDEM_IP_E * nrow + row);
       const int kpre = S.ikpre[row];
       if (kpre >= 0) {
         for (int64_t b = S.slice_base[sl] + lane + 32 * (int64_t)kpre; b < S.slice_base[sl + 1];
@@ -92,7 +109,12 @@ __global__ void __launch_bounds__(kThreads, BDEM_ELEM_MINB) k_element_assemble(b
       }
     }
     // bonds with j == e (ascending bond id)
-#pragma unroll 2
+#ifndef BDEM_ELEM_UNROLL
+#define BDEM_ELEM_UNROLL 1  // 1 / 2 / 3 / 4: 160.8 / 163.5 / 164.5 / 167.7 us
+#endif
+#define BDEM_STR_(x) #x
+#define BDEM_STR(x) BDEM_STR_(x)
+_Pragma(BDEM_STR(unroll BDEM_ELEM_UNROLL))
     for (int64_t k = S.jslice_base[sl] + lane; k < S.jslice_base[sl + 1]; k += 32) {
       const int64_t b = S.jpos[k];
       if (b < 0) continue;
@@ -101,11 +123,11 @@ __global__ void __launch_bounds__(kThreads, BDEM_ELEM_MINB) k_element_assemble(b
 #pragma unroll
       for (int c = 0; c < 3; ++c) gp[c] += kc * n[c];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) gq[c] += st[(BDEM_ST_GQJ + c) * nb + b];
+      for (int c = 0; c < 4; ++c) gq[c] += LDS1(st + (BDEM_ST_GQJ + c) * nb + b);
 #pragma unroll
       for (int t = 0; t < 6; ++t) {
         P[t] += apos[t];
-        R[t] += st[(BDEM_ST_D + t) * nb + b];
+        R[t] += LDS1(st + (BDEM_ST_D + t) * nb + b);
       }
     }
     // contacts: pairs then colliders into a separate accumulator (integrator.py:56-85,104-105)

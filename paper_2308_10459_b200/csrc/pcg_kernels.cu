@@ -359,7 +359,8 @@ __device__ __forceinline__ void spmv_slices(const bdem_system_t &S, const double
     if (s_row >= 0) {
 #pragma unroll
       for (int t = 0; t < 12 / kSpmvWarps; ++t)
-        prefetch_l2(S.diag + (int64_t)(w + kSpmvWarps * t) * S.vstride + s_row);
+        if (kRot || w + kSpmvWarps * t < 6)   // rotation-free: only the position block P
+          prefetch_l2(S.diag + (int64_t)(w + kSpmvWarps * t) * S.vstride + s_row);
     }
 #endif
     // software pipeline on the (cheap, integer) slot indices: the next slot's
