@@ -109,12 +109,8 @@ __global__ void __launch_bounds__(kThreads, BDEM_ELEM_MINB) k_element_assemble(b
       }
     }
     // bonds with j == e (ascending bond id)
-#ifndef BDEM_ELEM_UNROLL
-#define BDEM_ELEM_UNROLL 1  // 1 / 2 / 3 / 4: 160.8 / 163.5 / 164.5 / 167.7 us
-#endif
-#define BDEM_STR_(x) #x
-#define BDEM_STR(x) BDEM_STR_(x)
-_Pragma(BDEM_STR(unroll BDEM_ELEM_UNROLL))
+    // not unrolled: 1 / 2 / 3 / 4 iterations in flight ran 160.8 / 163.5 / 164.5 / 167.7 us
+#pragma unroll 1
     for (int64_t k = S.jslice_base[sl] + lane; k < S.jslice_base[sl + 1]; k += 32) {
       const int64_t b = S.jpos[k];
       if (b < 0) continue;
