@@ -149,6 +149,24 @@ def cantilever(nx=40, ny=4, nz=4, h=0.01, r=0.005, youngs=1e7, nu=0.3, density=1
                      notes="SC lattice, cutoff 1.01h, pinned x=0 face, no fracture")
 
 
+def twisted_beam(nx=40, ny=4, nz=4, rate=10.0, epsilon=1e-8, **kw) -> SceneSpec:
+    """The cantilever lattice with its x = max face pinned and twist-driven at
+    `rate` rad/s about the beam axis.  SURVEY 8(d) (C4 caution): the
+    reference's clamped Newton iteration stalls on this scene (gnorm stuck
+    above epsilon, alpha = 1, one PCG iteration per Newton iteration, residual
+    in the rotation DOFs next to the driven layer) and the step is not
+    committed; the GPU path has to reproduce the stall, not fix it."""
+    spec = cantilever(nx=nx, ny=ny, nz=nz, epsilon=epsilon, **kw)
+    el = spec.elements
+    x = el.p[:, 0]
+    ids = np.nonzero(x > x.max() - 1e-9)[0]
+    el.pinned[ids] = True
+    spec.driver = DriverSpec("twist", ids, el.p[ids].copy(), axis_point=np.zeros(3), rate=rate)
+    spec.name = "twisted_beam"
+    spec.notes = "cantilever lattice, x = max face twist-driven; the reference stalls"
+    return spec
+
+
 # ---------------------------------------------------------------------------
 # C2: jittered cube compressed by a descending plane
 # ---------------------------------------------------------------------------

@@ -434,6 +434,37 @@ def gold_trajectories():
     _run_traj("cube", spec, 6, 1e-6, schedule=sched)
 
 
+def gold_stall():
+    """SURVEY 8(d) (C4 caution): the twist-driven 40x4x4 lattice beam.  The
+    reference's clamped Newton iteration stalls at gnorm 1.84e-3 for the whole
+    300-iteration budget (alpha = 1 throughout) and stable_step does not
+    commit; the GPU path must reproduce the stall (solver.py:511-562, 917-939)."""
+    spec = C.twisted_beam()
+    drv = spec.driver
+    sc = ref_scene(spec, driver=rs.twist_driver(drv.ids, drv.p0, drv.axis_point, drv.rate))
+    cfg = rsv.SolverConfig(epsilon=spec.epsilon, max_iterations=300)
+    out = pack("init_el_", spec.elements, ELEM_FIELDS)
+    out.update(pack("init_b_", spec.bonds, BOND_FIELDS))
+    t0 = time.time()
+    rep = rsv.stable_step(sc, cfg)
+    r = rep.solve
+    el = sc.elements
+    out.update({"iterations": r.iterations, "pcg_total": r.pcg_total, "committed": rep.committed,
+                "reason": r.reason, "grad_norm": r.grad_norm, "converged": r.converged,
+                "rec_gnorm": np.array([x.grad_norm for x in r.records]),
+                "rec_f": np.array([x.f for x in r.records]),
+                "rec_alpha": np.array([x.alpha for x in r.records]),
+                "rec_pcg": np.array([x.pcg_iterations for x in r.records]),
+                "after_p": el.p.copy(), "after_q": el.q.copy(), "after_v": el.v.copy(),
+                "after_qdot": el.qdot.copy(), "time_after": sc.time,
+                "dt": spec.dt, "youngs": spec.youngs, "epsilon": spec.epsilon,
+                "k_contact": spec.k_contact, "k_element": spec.k_element,
+                "gravity": np.array(spec.gravity)})
+    print(f"  stall: {r.iterations} Newton / {r.pcg_total} PCG, reason {r.reason}, committed "
+          f"{rep.committed}, gnorm {r.grad_norm:.6e} in {time.time() - t0:.1f}s")
+    save("stall_beam.npz", **out)
+
+
 def _subsample_rows(n, stride):
     return np.unique(np.r_[np.arange(0, n, stride), np.arange(max(n - 3, 0), n)])
 

@@ -19,7 +19,7 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
-from _fixtures import close, elements_from, load
+from _fixtures import bonds_from, close, elements_from, load
 
 pytestmark = pytest.mark.gpu
 
@@ -184,3 +184,45 @@ def test_degenerate_bond_through_stable_step(cuda_ok):
     with pytest.raises(DegenerateBondError) as exc:
         stable_step(scene, SolverConfig(epsilon=1e-7))
     assert str(exc.value) == str(f["deg_msg"])
+
+
+def test_newton_stall_not_committed_twisted_beam(cuda_ok):
+    """SURVEY 8(d), C4 caution: the twist-driven 40x4x4 lattice beam.  The
+    reference's clamped Newton iteration (solver.py:511-562) settles on a
+    fixed point with gnorm 1.84e-3 > epsilon -- alpha = 1 and one PCG
+    iteration per Newton iteration, residual in the rotation DOFs next to the
+    driven layer -- burns its 300 iterations, returns reason
+    "max-iterations", and stable_step does not commit (solver.py:917-939).
+    The GPU path must reproduce the stall, not fix it."""
+    from paper_2308_10459_b200 import Scene, SolverConfig, stable_step
+    from paper_2308_10459_b200 import configs as C
+    from paper_2308_10459_b200.scene import TwistDriver
+    d = load("stall_beam.npz")
+    el, b = elements_from(d, "init_el_"), bonds_from(d, "init_b_")
+    drv = C.twisted_beam().driver
+    scene = Scene("twisted_beam", None, el, b, gravity=d["gravity"], dt=float(d["dt"]),
+                  youngs=float(d["youngs"]), k_contact=float(d["k_contact"]),
+                  k_element=float(d["k_element"]),
+                  driver=TwistDriver(drv.ids, drv.p0, drv.axis_point, drv.rate))
+    rep = stable_step(scene, SolverConfig(epsilon=float(d["epsilon"]), max_iterations=300))
+    r = rep.solve
+    assert not rep.committed and not r.converged
+    assert r.reason == str(d["reason"]) == "max-iterations"
+    assert r.iterations == int(d["iterations"]) == 300
+    # the descent into the fixed point and the plateau itself
+    gn = np.array([x.grad_norm for x in r.records])
+    ref = d["rec_gnorm"]
+    assert gn.shape == ref.shape
+    assert np.all(np.abs(gn[:6] - ref[:6]) <= 1e-8 * ref[:6])
+    assert np.all(np.abs(gn[6:] - ref[6:]) <= 1e-6 * ref[6:])
+    assert abs(r.grad_norm - float(d["grad_norm"])) <= 1e-6 * float(d["grad_norm"])
+    assert all(x.alpha == 1.0 for x in r.records)
+    pcg = np.array([x.pcg_iterations for x in r.records])
+    assert np.array_equal(pcg[:12], d["rec_pcg"][:12]) and np.all(pcg[12:] == 1)
+    assert abs(r.pcg_total - int(d["pcg_total"])) <= 2
+    # a step that is not committed leaves the state and the clock untouched
+    assert scene.time == float(d["time_after"]) == 0.0
+    assert np.array_equal(scene.elements.p, d["after_p"])
+    assert np.array_equal(scene.elements.q, d["after_q"])
+    assert np.array_equal(scene.elements.v, d["after_v"])
+    assert np.array_equal(scene.elements.qdot, d["after_qdot"])

@@ -232,3 +232,23 @@ def test_mesh_drop_trajectory():
         _assert_close(st.elements.q, d["q"][s], 1e-8, 1e-9, f"step {s} q")
     assert events == [(int(a), int(b)) for a, b, _, _ in d["events"]]
     assert np.array_equal(st.bonds.status, d["final_status"])
+
+
+def test_newton_stall_twisted_beam():
+    """The reference's max-iterations stall on the twist-driven lattice beam
+    (SURVEY 8(d), C4 caution; stall_beam.npz made by the reference): the oracle
+    reproduces the fixed point, the reason and the non-commit."""
+    from paper_2308_10459_b200 import configs as C
+    d = load("stall_beam.npz")
+    drv = C.twisted_beam().driver
+    st = _oracle_state(d, "twisted_beam",
+                       TwistDriver(drv.ids, drv.p0, drv.axis_point, drv.rate))
+    out = O.step(st, O.Config(epsilon=float(d["epsilon"]), max_iterations=300))
+    s = out.solve
+    assert not out.committed and s.reason == str(d["reason"]) == "max-iterations"
+    assert s.iterations == int(d["iterations"])
+    gn = np.array([r.grad_norm for r in s.records])
+    assert np.all(np.abs(gn - d["rec_gnorm"]) <= 1e-6 * d["rec_gnorm"])
+    assert abs(s.pcg_total - int(d["pcg_total"])) <= 2
+    assert st.time == 0.0
+    assert np.array_equal(st.elements.p, d["after_p"]) and np.array_equal(st.elements.q, d["after_q"])
