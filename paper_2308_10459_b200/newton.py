@@ -10,6 +10,7 @@ flow branches on (f, |z|, PCG state per chunk, slope, f_t).
 
 from __future__ import annotations
 
+import logging
 import math
 from dataclasses import dataclass, field
 
@@ -17,6 +18,10 @@ import numpy as np
 import torch
 
 from . import _lib as L
+
+# the reference logs its solver's recoveries (linalg.py:95,118, solver.py:545);
+# same messages here
+logger = logging.getLogger(__name__)
 
 EPS = float(np.finfo(float).eps)
 
@@ -127,6 +132,9 @@ class GPUProblem:
         d.call("bdem_reduce_finish", s, 0, 7, L.RED_BLOCKS, st)
         d.eval_pq = (p, q)
         sc = d.read_scalars()
+        nsing = int(sc[L.SC["NSING"]])
+        if nsing:
+            logger.warning("block-jacobi: %d singular blocks fall back to identity", nsing)
         f = float(sc[L.SC["F"]])
         gnorm = math.sqrt(float(sc[L.SC["GNORM2"]]))
         cnorm = math.sqrt(float(sc[L.SC["CNORM2"]]))
@@ -213,6 +221,7 @@ class GPUProblem:
             if state == L.PCG_BREAKDOWN:
                 restarts += 1
                 boost = float(h[L.PCG["BOOST"]])
+                logger.warning("pcg breakdown; restarting with diagonal boost %.3e", boost)
                 if restarts > 3:
                     return PCGResult(k, False, rel, restarts)
                 continue
@@ -280,6 +289,8 @@ def minimize_second_order(problem: GPUProblem, p0, q0, cfg: SolverConfig) -> Sol
         slope = problem.dot(d.z, d.y, nf6)
         problem.direction(q, d.y, 1.0)
         if not math.isfinite(slope) or slope >= 0.0:
+            logger.warning("newton direction not a descent direction; "
+                           "falling back to the gradient")
             problem.direction(q, d.z, -1.0)
             slope = -gnorm * gnorm
         # line search (solver.py:387-406)

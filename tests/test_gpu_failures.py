@@ -36,7 +36,7 @@ def _pack_sym6(blocks):
 
 
 @pytest.mark.parametrize("tag", ["cured", "giveup"])
-def test_pcg_breakdown_restart(cuda_ok, tag):
+def test_pcg_breakdown_restart(cuda_ok, tag, caplog):
     """An indefinite reduced operator through bdem_pcg_init/iterate: the
     breakdown test p.Ap <= 0, the boost max(100 b, 1e-10 max(|Ap|/|p|, 1)),
     the restart from x = 0 and the 3-restart cap follow linalg.py:74-97."""
@@ -53,7 +53,12 @@ def test_pcg_breakdown_restart(cuda_ok, tag):
         vals = np.concatenate([_pack_sym6(blocks[:, :3, :3]), _pack_sym6(blocks[:, 3:, 3:])])
         planes[:, cols] = torch.from_numpy(vals).cuda()
     dev.z.copy_(_soa(d["near_z"], dev))
-    res = prob.solve_pcg(float(f["pcg_tol"]), 2000)
+    with caplog.at_level("WARNING", logger="paper_2308_10459_b200.newton"):
+        res = prob.solve_pcg(float(f["pcg_tol"]), 2000)
+    # the reference's warning, once per restart (linalg.py:95)
+    msgs = [r.getMessage() for r in caplog.records]
+    assert sum(m.startswith("pcg breakdown; restarting with diagonal boost") for m in msgs) \
+        == res.restarts
     assert res.restarts == int(f[f"pcg_{tag}_restarts"])
     assert res.converged == bool(f[f"pcg_{tag}_converged"])
     want_it = int(f[f"pcg_{tag}_it"])
@@ -68,7 +73,7 @@ def test_pcg_breakdown_restart(cuda_ok, tag):
         _assert_close(y, f[f"pcg_{tag}_x"], 1e-4, 1e-6 * np.abs(y).max(), "x")
 
 
-def test_block_jacobi_identity_fallback_in_stable_step(cuda_ok):
+def test_block_jacobi_identity_fallback_in_stable_step(cuda_ok, caplog):
     """Zero-mass (zero 6x6 block) and zero-radius (singular rotation block)
     free elements next to a cantilever: BlockJacobi falls back to identity on
     both whole 6x6 blocks; three steps match the reference."""
@@ -81,7 +86,10 @@ def test_block_jacobi_identity_fallback_in_stable_step(cuda_ok):
     cfg = SolverConfig(epsilon=1e-7, max_iterations=300)
     m_dt2 = (spec.elements.mass / spec.dt**2).min()
     for s in range(3):
-        rep = stable_step(scene, cfg)
+        with caplog.at_level("WARNING", logger="paper_2308_10459_b200.newton"):
+            rep = stable_step(scene, cfg)
+        # linalg.py:118's warning at every preconditioner build
+        assert "block-jacobi: 2 singular blocks fall back to identity" in caplog.text
         assert rep.committed == bool(f["sing_committed"][s])
         assert rep.solve.iterations == int(f["sing_newton"][s])
         assert abs(rep.solve.pcg_total - int(f["sing_pcg"][s])) <= rep.solve.iterations
@@ -94,7 +102,7 @@ def test_block_jacobi_identity_fallback_in_stable_step(cuda_ok):
         assert np.array_equal(minv, np.tile(ident, (2, 1))), minv
 
 
-def test_non_descent_fallback(cuda_ok):
+def test_non_descent_fallback(cuda_ok, caplog):
     """With a linear solve returning x = -b (slope z.y > 0) every Newton
     iteration falls back to the steepest-descent direction -z with slope
     -|z|^2 (solver.py:542-548); the alphas, values and iterate match."""
@@ -126,9 +134,12 @@ def test_non_descent_fallback(cuda_ok):
         return PCGResult(1, True, 1.0)
 
     prob.solve_pcg = ascent
-    sol = minimize_second_order(prob, torch.from_numpy(d["p0"]).cuda(),
-                                torch.from_numpy(d["q0"]).cuda(),
-                                SolverConfig(epsilon=1e-9, max_iterations=6))
+    with caplog.at_level("WARNING", logger="paper_2308_10459_b200.newton"):
+        sol = minimize_second_order(prob, torch.from_numpy(d["p0"]).cuda(),
+                                    torch.from_numpy(d["q0"]).cuda(),
+                                    SolverConfig(epsilon=1e-9, max_iterations=6))
+    # solver.py:545's warning at every fallback
+    assert caplog.text.count("newton direction not a descent direction") == len(sol.records)
     assert sol.reason == str(f["nd_reason"])
     assert sol.iterations == int(f["nd_iterations"])
     assert [r.alpha for r in sol.records] == list(f["nd_rec_alpha"])
