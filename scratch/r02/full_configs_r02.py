@@ -9,6 +9,7 @@ import torch
 from paper_2308_10459_b200 import SolverConfig, configs
 from paper_2308_10459_b200.runner import StepFailure, advance
 from paper_2308_10459_b200.scene import Scene
+from paper_2308_10459_b200.state import DegenerateBondError, DegenerateShearError
 
 guard = float(sys.argv[2]) if len(sys.argv) > 2 else 1200.0
 which = sys.argv[3:] or ["C1", "C2", "C3", "C4", "C5"]
@@ -39,6 +40,13 @@ for name in which:
             done = advance(scene, cfg, attempts=att)
         except StepFailure as exc:
             stop = f"StepFailure at step {s}: {exc}"
+            newton += sum(a.solve.iterations for a in att)
+            pcg += sum(a.solve.pcg_total for a in att)
+            break
+        except (DegenerateBondError, DegenerateShearError) as exc:
+            # the reference does not catch these either: a degenerate bond or an
+            # antipodal pair at a line-search trial point ends the run
+            stop = f"{type(exc).__name__} at step {s}: {exc}"
             newton += sum(a.solve.iterations for a in att)
             pcg += sum(a.solve.pcg_total for a in att)
             break
