@@ -51,6 +51,10 @@ enum {
   BDEM_ERRSLOT_DEGENERATE_FIRST = 1, /* smallest offending bond index */
   BDEM_ERRSLOT_ANTIPODAL_COUNT = 2,
   BDEM_ERRSLOT_ANTIPODAL_FIRST = 3,
+  BDEM_ERRSLOT_COINCIDENT_CONTACT = 4, /* not an error: contact pairs with coincident
+                                          centres took the +x fallback normal
+                                          (contact.py:200-203); the host logs the
+                                          reference's warning */
   BDEM_ERRSLOT_COUNT = 8
 };
 

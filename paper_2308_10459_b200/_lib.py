@@ -14,6 +14,7 @@ from ._build import lib_path
 BDEM_OK = 0
 ERR_DEGENERATE_BOND, ERR_ANTIPODAL, ERR_NONFINITE, ERR_ARG, ERR_CUDA, ERR_CAPACITY = 1, 2, 3, 4, 5, 6
 ERRSLOT_DEG_COUNT, ERRSLOT_DEG_FIRST, ERRSLOT_ANTI_COUNT, ERRSLOT_ANTI_FIRST = 0, 1, 2, 3
+ERRSLOT_COINCIDENT = 4
 ERRSLOT_COUNT = 8
 
 # bond geometry planes

@@ -636,6 +636,7 @@ __global__ void __launch_bounds__(kThreads) k_pair(bdem_system_t S, const double
     double n[3];
     if (len < 1e-12) {
       n[0] = 1.0; n[1] = 0.0; n[2] = 0.0;
+      atomicAdd(&S.err[BDEM_ERRSLOT_COINCIDENT_CONTACT], 1);   // host logs contact.py:202's warning
     } else {
       const double l = fmax(len, 1e-300);
 #pragma unroll

@@ -20,6 +20,7 @@ Memory layout (HBM):
 from __future__ import annotations
 
 import ctypes as C
+import logging
 import weakref
 
 import numpy as np
@@ -27,6 +28,8 @@ import torch
 
 from . import _lib as L
 from .state import DegenerateBondError, DegenerateShearError
+
+logger = logging.getLogger(__name__)
 
 F64 = torch.float64
 I32 = torch.int32
@@ -553,6 +556,10 @@ class DeviceSystem:
         self.h_err.copy_(self.err, non_blocking=True)
         torch.cuda.current_stream(self.device).synchronize()
         err = self.h_err.numpy()
+        if err[L.ERRSLOT_COINCIDENT]:
+            # contact.py:200-203: evaluated with the +x fallback normal, and logged
+            logger.warning("coincident contact centers; using +x fallback normal")
+            self.err[L.ERRSLOT_COINCIDENT] = 0
         if err[L.ERRSLOT_DEG_COUNT] or err[L.ERRSLOT_ANTI_COUNT]:
             self.raise_errors(err.copy())
         return self.h_scalars.numpy()

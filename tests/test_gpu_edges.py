@@ -125,3 +125,18 @@ def test_run_to_run_bit_reproducible(cuda_ok, name):
     assert a[5] == b[5]
     for x, y in zip(a[:5], b[:5]):
         assert np.array_equal(x, y)
+
+
+def test_coincident_contact_centres_take_the_fallback_normal(cuda_ok, caplog):
+    """Two unbonded spheres at the same point: self_repulsion_terms uses the +x
+    fallback normal and logs a warning (contact.py:200-203); the GPU pair
+    kernel does the same, the host logs the same message, and the steps match
+    the oracle (the spheres are pushed apart along x)."""
+    from paper_2308_10459_b200 import configs as C
+    pos = np.zeros((2, 3))
+    el = C._elements(pos, np.tile([0.0, 0.0, 0.0, 1.0], (2, 1)), np.full(2, 0.005), 1000.0)
+    b = C.build_bonds(pos, el.radius, np.zeros((0, 2), dtype=np.int64), 1e7, 4e6)
+    with caplog.at_level("WARNING", logger="paper_2308_10459_b200.device"):
+        reps = _run_both(el, b, 2, k_element=1e3, eps=1e-9)
+    assert reps[0].contact_pairs == 1
+    assert "coincident contact centers; using +x fallback normal" in caplog.text
